@@ -1,0 +1,158 @@
+// ref_runner.cpp -- C-ABI wrapper around the REFERENCE library itself (test
+// infrastructure only).  It #includes the reference's unchanged header-only
+// sources from /root/reference/proj/include (nothing is copied into this repo)
+// and is compiled by oracle/Makefile with the reference's Release flags
+// (-std=gnu++20 -O3 -DNDEBUG, proj/CMakeLists.txt:8-10) into
+// oracle/_ref/libsigcut_ref.so.  Tests use it to pin oracle/sigcut_oracle.c and
+// to generate tests/golden/ fixtures; bench.py --impl reference times it.
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sigcut/sigcut.hpp"
+
+#include "oracle.h"
+
+namespace {
+std::string g_err;
+
+int map_exc(const std::exception& e) {
+  g_err = e.what();
+  return dynamic_cast<const std::invalid_argument*>(&e) != nullptr ? 1 : 2;
+}
+
+std::vector<std::size_t> to_shape(int order, const uint64_t* shape) {
+  return std::vector<std::size_t>(shape, shape + order);
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+uint64_t ref_mix64(uint64_t z) { return sigcut::mix64(z); }
+uint64_t ref_substream(uint64_t seed, uint64_t index) { return sigcut::substream(seed, index); }
+
+void ref_fill_u64(uint64_t seed, uint64_t count, uint64_t* out) {
+  sigcut::Xoshiro256pp rng(seed);
+  for (uint64_t i = 0; i < count; ++i) out[i] = rng.next_u64();
+}
+
+void ref_fill_normal(uint64_t seed, uint64_t count, double* out) {
+  sigcut::Xoshiro256pp rng(seed);
+  for (uint64_t i = 0; i < count; ++i) out[i] = rng.next_normal();
+}
+
+void ref_fill_f64(uint64_t seed, uint64_t count, double* out) {
+  sigcut::Xoshiro256pp rng(seed);
+  for (uint64_t i = 0; i < count; ++i) out[i] = rng.next_f64();
+}
+
+int ref_greedy_decompose(const double* a, int order, const uint64_t* shape,
+                         const oracle_config* cfg, oracle_output* out) {
+  try {
+    const auto sh = to_shape(order, shape);
+    const std::size_t numel = sigcut::DenseTensor::checked_numel(sh);
+    sigcut::DenseTensor t(sh, std::vector<double>(a, a + numel));
+    sigcut::DecomposeConfig dc;
+    dc.width = cfg->width;
+    dc.flush_width = cfg->flush_width;
+    dc.search.seed = cfg->seed;
+    dc.search.restarts = cfg->restarts;
+    dc.search.max_sweeps = cfg->max_sweeps;
+    dc.record_curve = true;
+    dc.min_value_fraction = cfg->min_value_fraction;
+    dc.max_factor_bytes = cfg->max_factor_bytes;
+    auto [d, report] = sigcut::greedy_decompose(t, dc);
+    const std::size_t w = d.width();
+    for (std::size_t ax = 0; ax < d.factors.size(); ++ax) {
+      const std::size_t nw = sigcut::SignVector::word_count(sh[ax]);
+      for (std::size_t j = 0; j < w; ++j) {
+        const auto words = d.factors[ax].column(j).words();
+        std::memcpy(out->signs[ax] + j * nw, words.data(), nw * sizeof(uint64_t));
+      }
+    }
+    for (std::size_t j = 0; j < w; ++j) {
+      out->alpha[j] = d.coefficients[j];
+      out->cut_value[j] = report.steps[j].cut_value;
+      out->resid_norm[j] = report.steps[j].residual_norm;
+    }
+    out->width_done = w;
+    out->input_norm = report.input_norm;
+    out->final_residual_norm = report.final_residual_norm;
+    if (out->iterations != nullptr || out->remainder != nullptr) {
+      // The public driver does not expose per-term sweep counts or R_w; replay the
+      // identical term loop (decompose.hpp:332-347) on the reference internals.
+      sigcut::DenseTensor base = t;
+      std::vector<sigcut::detail::PendingTerm> pending;
+      std::vector<std::size_t> axes(sh.size());
+      for (std::size_t i = 0; i < axes.size(); ++i) axes[i] = i;
+      for (std::size_t term = 0; term < w; ++term) {
+        const auto scfg = sigcut::detail::term_search_config(dc.search, term);
+        sigcut::CutResult res = sigcut::detail::search_tensor_residual(base, pending, scfg, nullptr);
+        if (res.value != out->cut_value[term]) throw std::runtime_error("replay diverged");
+        if (out->iterations != nullptr) out->iterations[term] = res.iterations;
+        pending.push_back(sigcut::detail::PendingTerm{std::move(res.signs), res.value / double(numel)});
+        if (pending.size() >= dc.flush_width) sigcut::detail::flush_pending(base, pending, axes);
+      }
+      sigcut::detail::flush_pending(base, pending, axes);
+      if (out->remainder != nullptr) std::memcpy(out->remainder, base.data().data(), numel * 8);
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_signed_cut(const double* a, int order, const uint64_t* shape, uint64_t seed,
+                   uint64_t restarts, uint64_t max_sweeps, double* value, uint64_t** signs,
+                   uint64_t* iterations, double* sweep_values, uint64_t* n_sweep_values) {
+  try {
+    const auto sh = to_shape(order, shape);
+    const std::size_t numel = sigcut::DenseTensor::checked_numel(sh);
+    sigcut::DenseTensor t(sh, std::vector<double>(a, a + numel));
+    sigcut::SearchConfig sc{seed, restarts, max_sweeps};
+    sigcut::SearchDiagnostics diag;
+    const sigcut::CutResult res = sigcut::axial_greedy_cut(t, sc, &diag);
+    *value = res.value;
+    *iterations = res.iterations;
+    for (std::size_t ax = 0; ax < res.signs.size(); ++ax) {
+      const auto words = res.signs[ax].words();
+      std::memcpy(signs[ax], words.data(), words.size() * sizeof(uint64_t));
+    }
+    if (sweep_values != nullptr) {
+      for (std::size_t i = 0; i < diag.sweep_values.size(); ++i) sweep_values[i] = diag.sweep_values[i];
+    }
+    if (n_sweep_values != nullptr) *n_sweep_values = diag.sweep_values.size();
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+uint64_t ref_width_for_compression(int coeff_bits, int source_bits, int order,
+                                   const uint64_t* shape, double rate) {
+  try {
+    sigcut::StorageModel m{coeff_bits, source_bits, to_shape(order, shape), -1};
+    return sigcut::width_for_compression(m, rate);
+  } catch (const std::exception& e) {
+    map_exc(e);
+    return 0;
+  }
+}
+
+double ref_compression_rate(uint64_t k, int coeff_bits, int source_bits, int order,
+                            const uint64_t* shape) {
+  sigcut::StorageModel m{coeff_bits, source_bits, to_shape(order, shape), -1};
+  return sigcut::compression_rate(k, m);
+}
+
+void ref_quantize_bf16(uint64_t count, const double* in, double* out) {
+  auto t = sigcut::DenseTensor::from_raw({count}, std::vector<double>(in, in + count));
+  const auto q = sigcut::quantize_half(t, sigcut::HalfFormat::kBf16);
+  std::memcpy(out, q.data().data(), count * sizeof(double));
+}
+
+}  // extern "C"

@@ -1,0 +1,474 @@
+// capi.cpp -- host driver behind the C ABI (include/sigcut_b200.h).
+//
+// Owns the CUDA context/stream, validates problems with the reference's error
+// semantics, draws the per-cut start vectors with the reference's generator,
+// lays the remainder out in HBM (row pitch padded to 32 elements, pad zero),
+// sizes the shared-memory residency / TMA ring for the persistent kernel,
+// launches it cooperatively and rebuilds the reference's CutReport curve.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/sigcut_b200.h"
+#include "rng.h"
+#include "sweep.h"
+
+struct sc_ctx {
+  int device = 0;
+  int num_sms = 0;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+  // cached device arena and pinned staging
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+};
+
+namespace {
+
+constexpr const char* kVersion = "sigcut-b200 0.1 (sm_100a)";
+
+sc_status set_err(sc_ctx* ctx, sc_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return st;
+}
+
+#define SC_CUDA(ctx, call)                                                                \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(ctx, SC_CUDA_ERROR, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+uint64_t words64(uint64_t n) { return (n + 63) / 64; }
+
+sc_status validate(const sc_problem* p, std::string* msg) {
+  auto bad = [&](const char* m) {
+    if (msg) *msg = m;
+    return SC_INVALID_ARGUMENT;
+  };
+  if (p == nullptr) return bad("sc_problem: null");
+  if (p->dtype != SC_F32 && p->dtype != SC_F64) return bad("sc_problem: dtype must be F32 or F64");
+  // DenseTensor::checked_numel, dense_tensor.hpp:57-67
+  if (p->order < 1 || p->order > SC_MAX_ORDER) return bad("DenseTensor: order must be >= 1");
+  if (p->shape == nullptr) return bad("sc_problem: null shape");
+  uint64_t numel = 1;
+  for (int i = 0; i < p->order; ++i) {
+    if (p->shape[i] == 0) return bad("DenseTensor: zero-length axis");
+    if (p->shape[i] > UINT64_MAX / numel) return bad("DenseTensor: shape overflow");
+    numel *= p->shape[i];
+  }
+  if (p->data == nullptr) return bad("sc_problem: null data");
+  // check_decompose_config, decompose.hpp:290-298
+  if (p->flush_width < 1) return bad("DecomposeConfig: flush_width must be >= 1");
+  uint64_t per_term = sizeof(double);
+  for (int i = 0; i < p->order; ++i) per_term += words64(p->shape[i]) * sizeof(uint64_t);
+  if (p->width > 0 && per_term > p->max_factor_bytes / p->width)
+    return bad("DecomposeConfig: width exceeds the factor memory budget");
+  // best_of_restarts, search.hpp:217-218
+  if (p->restarts < 1) return bad("SearchConfig: restarts must be >= 1");
+  if (p->max_sweeps < 1) return bad("SearchConfig: max_sweeps must be >= 1");
+  if (p->seed_mode != SC_SEED_PER_TERM && p->seed_mode != SC_SEED_DIRECT)
+    return bad("sc_problem: unknown seed_mode");
+  return SC_OK;
+}
+
+uint64_t term_seed(const sc_problem* p, uint64_t term) {
+  // term_search_config (decompose.hpp:300-304); greedy_signed_cut uses the seed as given
+  if (p->seed_mode == SC_SEED_DIRECT && term == 0) return p->seed;
+  return scb::substream(p->seed, term);
+}
+
+// Start vectors of (term, restart): the rng of best_of_restarts (search.hpp:222)
+// draws s0 (discarded) then t0 for matrices (search.hpp:149-150), or one vector
+// per axis for order k (search.hpp:197).
+uint64_t start_vectors(const sc_problem* p, uint64_t term, uint64_t restart, uint64_t* out) {
+  scb::Xoshiro rng(scb::substream(term_seed(p, term), restart));
+  if (p->order == 2) {
+    rng.skip(words64(p->shape[0]));
+    rng.sign_words(p->shape[1], out);
+    return words64(p->shape[1]);
+  }
+  uint64_t off = 0;
+  for (int i = 0; i < p->order; ++i) {
+    rng.sign_words(p->shape[i], out + off);
+    off += words64(p->shape[i]);
+  }
+  return off;
+}
+
+template <typename T>
+T* carve(char*& cur, size_t count) {
+  T* p = reinterpret_cast<T*>(cur);
+  cur += (count * sizeof(T) + 255) & ~size_t(255);
+  return p;
+}
+
+size_t env_size(const char* name, size_t dflt) {
+  const char* v = std::getenv(name);
+  return v ? static_cast<size_t>(std::strtoull(v, nullptr, 10)) : dflt;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sc_version(void) { return kVersion; }
+int sc_abi_version(void) { return SC_ABI_VERSION; }
+
+sc_status sc_create(sc_ctx** out, int device) {
+  if (out == nullptr) return SC_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto* ctx = new sc_ctx();
+  ctx->device = device;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) {
+    delete ctx;
+    return SC_CUDA_ERROR;
+  }
+  cudaDeviceProp prop{};
+  if (cudaSetDevice(device) != cudaSuccess || cudaGetDeviceProperties(&prop, device) != cudaSuccess ||
+      prop.major != 10) {
+    delete ctx;
+    return SC_CUDA_ERROR;  // sm_100a kernels only; no fallback
+  }
+  ctx->num_sms = prop.multiProcessorCount;
+  ctx->smem_optin = prop.sharedMemPerBlockOptin;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+    delete ctx;
+    return SC_CUDA_ERROR;
+  }
+  *out = ctx;
+  return SC_OK;
+}
+
+void sc_destroy(sc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->arena) cudaFree(ctx->arena);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* sc_last_error(const sc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+sc_status sc_validate_problem(const sc_problem* problem, char* msg, size_t msg_len) {
+  std::string m;
+  const sc_status st = validate(problem, &m);
+  if (msg && msg_len) {
+    std::snprintf(msg, msg_len, "%s", m.c_str());
+  }
+  return st;
+}
+
+uint64_t sc_start_vectors(const sc_problem* problem, uint64_t term, uint64_t restart,
+                          uint64_t* out_words) {
+  if (validate(problem, nullptr) != SC_OK || out_words == nullptr) return 0;
+  return start_vectors(problem, term, restart, out_words);
+}
+
+void sc_fill_normal_f64(uint64_t seed, uint64_t count, double* out) {
+  scb::Xoshiro rng(seed);
+  for (uint64_t i = 0; i < count; ++i) out[i] = rng.next_normal();
+}
+
+void sc_fill_normal_f32(uint64_t seed, uint64_t count, float* out) {
+  scb::Xoshiro rng(seed);
+  for (uint64_t i = 0; i < count; ++i) out[i] = static_cast<float>(rng.next_normal());
+}
+
+uint64_t sc_width_for_compression(int coeff_bits, int source_bits, int order, const uint64_t* shape,
+                                  double rate) {
+  // width_for_compression, metrics.hpp:55-63
+  if (order < 1 || shape == nullptr || !(rate > 0.0) || rate > 1.0) return 0;
+  double numel = 1.0;
+  uint64_t sign_bits = 0;
+  for (int i = 0; i < order; ++i) {
+    numel *= static_cast<double>(shape[i]);
+    sign_bits += shape[i];
+  }
+  const double src = static_cast<double>(source_bits) * numel;
+  return static_cast<uint64_t>(std::floor(rate * src / static_cast<double>(coeff_bits + sign_bits)));
+}
+
+void sc_lpt_schedule(const double* costs, uint64_t count, uint32_t bins, uint32_t* bin_of_job) {
+  if (bins == 0) return;
+  std::vector<uint64_t> order(count);
+  std::iota(order.begin(), order.end(), uint64_t{0});
+  // longest first; ties by job index so every rank computes the same plan
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint64_t a, uint64_t b) { return costs[a] > costs[b]; });
+  std::vector<double> load(bins, 0.0);
+  for (uint64_t j : order) {
+    uint32_t best = 0;
+    for (uint32_t b = 1; b < bins; ++b)
+      if (load[b] < load[best]) best = b;
+    bin_of_job[j] = best;
+    load[best] += costs[j];
+  }
+}
+
+sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) {
+  const auto t_start = std::chrono::steady_clock::now();
+  if (ctx == nullptr) return SC_INVALID_ARGUMENT;
+  if (res == nullptr) return set_err(ctx, SC_INVALID_ARGUMENT, "sc_result: null");
+  std::string msg;
+  if (validate(p, &msg) != SC_OK) return set_err(ctx, SC_INVALID_ARGUMENT, "%s", msg.c_str());
+  if (p->order != 2)
+    return set_err(ctx, SC_NOT_SUPPORTED, "order-%d tensors are not supported by this build", p->order);
+  if (res->sign_words[0] == nullptr || res->sign_words[1] == nullptr || res->cut_value == nullptr)
+    return set_err(ctx, SC_INVALID_ARGUMENT, "sc_result: sign_words and cut_value are required");
+  SC_CUDA(ctx, cudaSetDevice(ctx->device));
+
+  const uint64_t m = p->shape[0], n = p->shape[1];
+  if (m > INT32_MAX / 2 || n > INT32_MAX / 2)
+    return set_err(ctx, SC_NOT_SUPPORTED, "matrix dimension too large for this build");
+  const int dt = p->dtype;
+  const size_t es = dt == SC_F32 ? 4 : 8;
+  const long long pitch = static_cast<long long>((n + 31) / 32 * 32);
+  scb::Variant var{};
+  if (scb::pick_variant(dt, pitch, &var) != 0)
+    return set_err(ctx, SC_NOT_SUPPORTED, "row length %llu exceeds the fused-kernel envelope",
+                   static_cast<unsigned long long>(n));
+
+  const int G = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(ctx->num_sms), m));
+  const int rows_base = static_cast<int>(m / G), rows_rem = static_cast<int>(m % G);
+  const int rows_max = rows_base + (rows_rem ? 1 : 0);
+  const int Q = static_cast<int>(pitch / 32);
+  const int sw = (rows_max + 31) / 32;
+  const int zl = std::max(1, std::min(4, (Q + G - 1) / G));
+  const size_t rowB = static_cast<size_t>(pitch) * es;
+  const int CW = var.nd + var.nz;
+  // dot warps sharing a row: wide rows are split across warps so fewer rows
+  // need to sit in the ring at once (more shared memory stays resident)
+  int ds = static_cast<int>(env_size("SCB_DS", rowB >= 8192 ? 2 : 1));
+  if (ds < 1 || var.nd % ds != 0) ds = 1;
+  auto smem_for = [&](int st_, int res_) {
+    return scb::make_layout(rowB, st_, res_, ds, rows_max, Q, zl, CW, sw).total;
+  };
+  const size_t cap = ctx->smem_optin;
+  int stages = 0, res_rows = rows_max;
+  if (smem_for(0, rows_max) > cap) {
+    stages = static_cast<int>(env_size("SCB_STAGES", static_cast<size_t>(var.nd / ds + 4)));
+    stages = std::max(2, std::min(stages, scb::kMaxStages));
+    while (stages > 2 && smem_for(stages, 0) > cap) --stages;
+    if (smem_for(stages, 0) > cap)
+      return set_err(ctx, SC_NOT_SUPPORTED, "row of %zu bytes does not fit the shared-memory ring", rowB);
+    res_rows = 0;
+    while (res_rows < rows_max && smem_for(stages, res_rows + 1) <= cap) ++res_rows;
+    res_rows = static_cast<int>(std::min<size_t>(env_size("SCB_RES_ROWS", static_cast<size_t>(res_rows)),
+                                                 static_cast<size_t>(res_rows)));
+  }
+  const size_t smem = smem_for(stages, res_rows);
+
+  const uint64_t w = p->width;
+  const uint64_t wm = words64(m), wn = words64(n);
+  const int t_stride = static_cast<int>(2 * wn), s_stride = static_cast<int>(2 * wm);
+  const int tw32 = std::max(Q, t_stride);
+  const uint64_t nstart = std::max<uint64_t>(w, 1) * p->restarts;
+
+  // ---- device arena ----
+  const size_t need = ((m * rowB + 255) & ~size_t(255)) + ((G * rowB * 8 / es + 255) & ~size_t(255)) +
+                      ((G * sizeof(scb::Slot) + 255) & ~size_t(255)) + 4 * 256 +
+                      3 * ((tw32 * 8 + 255) & ~size_t(255)) +
+                      ((nstart * wn * 8 + 255) & ~size_t(255)) +
+                      ((std::max<uint64_t>(w, 1) * (wm + wn) * 8 + 511) & ~size_t(255)) +
+                      ((std::max<uint64_t>(w, 1) * 8 + 255) & ~size_t(255)) * 2 +
+                      (((w + 1) * 8 + 255) & ~size_t(255)) + 8 * 256 + 4096;
+  if (need > ctx->arena_bytes) {
+    if (ctx->arena) cudaFree(ctx->arena);
+    ctx->arena = nullptr;
+    ctx->arena_bytes = 0;
+    SC_CUDA(ctx, cudaMalloc(&ctx->arena, need));
+    ctx->arena_bytes = need;
+  }
+  char* cur = static_cast<char*>(ctx->arena);
+  void* dR = carve<char>(cur, m * rowB);
+  double* zpart = carve<double>(cur, static_cast<size_t>(G) * pitch);
+  scb::Slot* slots = carve<scb::Slot>(cur, G);
+  unsigned* ctr = carve<unsigned>(cur, 8);  // [1..3] err_pass
+  unsigned long long* stats = carve<unsigned long long>(cur, 4);
+  unsigned long long* tb64 = carve<unsigned long long>(cur, 2 * static_cast<size_t>(tw32));
+  uint32_t* tbest = carve<uint32_t>(cur, tw32);
+  uint64_t* t0 = carve<uint64_t>(cur, nstart * wn);
+  uint64_t* S_out = carve<uint64_t>(cur, std::max<uint64_t>(w, 1) * wm);
+  uint64_t* T_out = carve<uint64_t>(cur, std::max<uint64_t>(w, 1) * wn);
+  double* c_out = carve<double>(cur, std::max<uint64_t>(w, 1));
+  uint32_t* sweeps_out = carve<uint32_t>(cur, std::max<uint64_t>(w, 1) * 2);
+  double* norm2 = carve<double>(cur, w + 1);
+
+  // ---- host staging (pinned) for the start vectors ----
+  const size_t t0_bytes = nstart * wn * 8;
+  if (t0_bytes > ctx->pinned_bytes) {
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    SC_CUDA(ctx, cudaMallocHost(&ctx->pinned, t0_bytes));
+    ctx->pinned_bytes = t0_bytes;
+  }
+  uint64_t* ht0 = static_cast<uint64_t*>(ctx->pinned);
+  for (uint64_t term = 0; term < w; ++term)
+    for (uint64_t r = 0; r < p->restarts; ++r) start_vectors(p, term, r, ht0 + (term * p->restarts + r) * wn);
+
+  cudaStream_t st = ctx->stream;
+  uint64_t h2d = 0, d2h = 0;
+  const cudaMemcpyKind in_kind = p->data_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (static_cast<uint64_t>(pitch) != n) SC_CUDA(ctx, cudaMemsetAsync(dR, 0, m * rowB, st));
+  SC_CUDA(ctx, cudaMemcpy2DAsync(dR, rowB, p->data, n * es, n * es, m, in_kind, st));
+  if (!p->data_on_device) h2d += m * n * es;
+  if (w > 0) {
+    SC_CUDA(ctx, cudaMemcpyAsync(t0, ht0, t0_bytes, cudaMemcpyHostToDevice, st));
+    h2d += t0_bytes;
+  }
+  SC_CUDA(ctx, cudaMemsetAsync(ctr, 0, 4, st));
+  SC_CUDA(ctx, cudaMemsetAsync(ctr + 1, 0xff, 12, st));
+  SC_CUDA(ctx, cudaMemsetAsync(slots, 0, static_cast<size_t>(G) * sizeof(scb::Slot), st));
+  SC_CUDA(ctx, cudaMemsetAsync(tb64, 0, 2 * static_cast<size_t>(tw32) * 8, st));
+  SC_CUDA(ctx, cudaMemsetAsync(tbest, 0, static_cast<size_t>(tw32) * 4, st));
+  SC_CUDA(ctx, cudaMemsetAsync(stats, 0, 32, st));
+  if (w > 0) SC_CUDA(ctx, cudaMemsetAsync(S_out, 0, w * wm * 8, st));
+
+  scb::KParams kp{};
+  kp.R = dR;
+  kp.pitch = pitch;
+  kp.m = static_cast<int>(m);
+  kp.n = static_cast<int>(n);
+  kp.G = G;
+  kp.rows_base = rows_base;
+  kp.rows_rem = rows_rem;
+  kp.res_rows = res_rows;
+  kp.ds = ds;
+  kp.rows_max = rows_max;
+  kp.stages = stages;
+  kp.Q = Q;
+  kp.sw = sw;
+  kp.zl = zl;
+  kp.t0 = reinterpret_cast<const uint32_t*>(t0);
+  kp.t0_stride = t_stride;
+  kp.tb64 = tb64;
+  kp.tbest = tbest;
+  kp.zpart = zpart;
+  kp.slots = slots;
+  kp.bar = ctr;
+  kp.err_pass = ctr + 1;
+  kp.S_out = reinterpret_cast<uint32_t*>(S_out);
+  kp.s_stride = s_stride;
+  kp.T_out = reinterpret_cast<uint32_t*>(T_out);
+  kp.t_stride = t_stride;
+  kp.c_out = c_out;
+  kp.sweeps_out = sweeps_out;
+  kp.norm2_out = norm2;
+  kp.stats = stats;
+  kp.width = static_cast<long long>(w);
+  kp.restarts = static_cast<long long>(p->restarts);
+  kp.max_sweeps = static_cast<long long>(std::min<uint64_t>(p->max_sweeps, 1ull << 40));
+  kp.min_frac = p->min_value_fraction;
+  kp.numel_d = static_cast<double>(m * n);
+
+  const bool prof = std::getenv("SCB_PROF") != nullptr;
+  unsigned long long* dprof = nullptr;
+  if (prof) {
+    SC_CUDA(ctx, cudaMalloc(&dprof, static_cast<size_t>(G) * 16 * 8));
+    SC_CUDA(ctx, cudaMemsetAsync(dprof, 0, static_cast<size_t>(G) * 16 * 8, st));
+  }
+  kp.prof = dprof;
+  SC_CUDA(ctx, scb::set_smem_limit(var, smem));
+  SC_CUDA(ctx, cudaEventRecord(ctx->ev0, st));
+  SC_CUDA(ctx, scb::launch_sweep(var, kp, smem, st));
+  SC_CUDA(ctx, cudaEventRecord(ctx->ev1, st));
+
+  // ---- results ----
+  unsigned h_ctr[4];
+  unsigned long long h_stats[4];
+  std::vector<double> h_norm2(w + 1);
+  SC_CUDA(ctx, cudaMemcpyAsync(h_ctr, ctr, 16, cudaMemcpyDeviceToHost, st));
+  SC_CUDA(ctx, cudaMemcpyAsync(h_stats, stats, 32, cudaMemcpyDeviceToHost, st));
+  SC_CUDA(ctx, cudaMemcpyAsync(h_norm2.data(), norm2, (w + 1) * 8, cudaMemcpyDeviceToHost, st));
+  SC_CUDA(ctx, cudaStreamSynchronize(st));
+  d2h += 16 + 32 + (w + 1) * 8;
+  float kms = 0.f;
+  cudaEventElapsedTime(&kms, ctx->ev0, ctx->ev1);
+  res->kernel_ms = kms;
+  res->kernel_launches = 1;
+  if (prof) {
+    std::vector<unsigned long long> hp(static_cast<size_t>(G) * 16);
+    cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost);
+    cudaFree(dprof);
+    double acc[8] = {0};
+    for (int g = 0; g < G; ++g)
+      for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(hp[g * 16 + i]) / G;
+    std::fprintf(stderr,
+                 "[scb prof] G=%d res_rows=%d stages=%d ds=%d nd=%d nz=%d zv=%d smem=%zu | cycles/CTA: "
+                 "fullwait=%.0f chunks=%.0f passend+bar=%.0f decision=%.0f reduce+bar=%.0f | z: readywait=%.0f loop=%.0f | prod emptywait=%.0f  (per pass: chunks %.0f) passes=%llu\n",
+                 G, res_rows, stages, ds, var.nd, var.nz, var.zv, smem, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7],
+                 acc[1] / std::max<double>(1.0, static_cast<double>(h_stats[1])),
+                 static_cast<unsigned long long>(h_stats[1]));
+  }
+  if (h_ctr[3] != 0xffffffffu) return set_err(ctx, SC_INVALID_ARGUMENT, "DenseTensor: non-finite value");
+  if (h_ctr[1] != 0xffffffffu || h_ctr[2] != 0xffffffffu)
+    return set_err(ctx, SC_INVALID_ARGUMENT, "sgn_vector: non-finite entry");
+
+  const uint64_t wd = h_stats[0];
+  res->width_done = wd;
+  res->passes = h_stats[1];
+  if (wd > 0) {
+    SC_CUDA(ctx, cudaMemcpyAsync(res->sign_words[0], S_out, wd * wm * 8, cudaMemcpyDeviceToHost, st));
+    SC_CUDA(ctx, cudaMemcpyAsync(res->sign_words[1], T_out, wd * wn * 8, cudaMemcpyDeviceToHost, st));
+    SC_CUDA(ctx, cudaMemcpyAsync(res->cut_value, c_out, wd * 8, cudaMemcpyDeviceToHost, st));
+    d2h += wd * (wm + wn + 1) * 8;
+    if (res->sweeps) {
+      SC_CUDA(ctx, cudaMemcpyAsync(res->sweeps, sweeps_out, wd * 4, cudaMemcpyDeviceToHost, st));
+      d2h += wd * 4;
+    }
+  }
+  if (res->remainder) {
+    SC_CUDA(ctx, cudaMemcpy2DAsync(res->remainder, n * es, dR, rowB, n * es, m, cudaMemcpyDeviceToHost, st));
+    d2h += m * n * es;
+  }
+  SC_CUDA(ctx, cudaStreamSynchronize(st));
+
+  // ---- CutReport reconstruction (decompose.hpp:317-359) ----
+  const double N = static_cast<double>(m * n);
+  res->input_norm = std::sqrt(h_norm2[0]);
+  double resid_sq = h_norm2[0];
+  for (uint64_t k = 0; k < wd; ++k) {
+    const double c = res->cut_value[k];
+    if (res->alpha) res->alpha[k] = c / N;
+    const double r2 = resid_sq - c * c / N;
+    resid_sq = (0.0 < r2) ? r2 : 0.0;
+    if ((k + 1) % p->flush_width == 0) resid_sq = h_norm2[k + 1];  // exact re-anchor
+    if (res->resid_norm) res->resid_norm[k] = std::sqrt(resid_sq);
+    if (res->resid_norm_exact) res->resid_norm_exact[k] = std::sqrt(h_norm2[k + 1]);
+  }
+  res->final_residual_norm = std::sqrt(h_norm2[wd]);
+  if (wd > 0 && res->resid_norm) res->resid_norm[wd - 1] = res->final_residual_norm;
+  res->h2d_bytes = h2d;
+  res->d2h_bytes = d2h;
+  res->total_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  return SC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// sweep.h -- launch parameters and shared-memory layout shared by the host
+// driver (capi.cpp) and the persistent fused-sweep kernel (sweep.cu).
+// No torch types anywhere.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace scb {
+
+// Pass kinds (bit flags) published by the consumer controller to the TMA
+// producer through shared memory.
+enum PassFlags : int {
+  F_DOT = 1,     // y = R t, s' = sgn(y), z = R^T s', c = <s, y>
+  F_UPD = 2,     // R -= alpha s t^T applied while streaming (fused rank-1 update)
+  F_NORM = 4,    // ||R||_F^2 accumulated (f64)
+  F_WB = 8,      // write SMEM-resident rows back to global (end of run)
+  F_CHECK = 16,  // reject non-finite input values (first pass)
+  K_TERM = 256,  // no more passes
+};
+
+enum ErrSlot : int { ERR_Y = 0, ERR_Z = 1, ERR_INPUT = 2 };
+
+// Per-CTA scalar partials of a pass, double-buffered by pass parity (a CTA can
+// run at most one pass ahead of the slowest reader).
+struct Slot {
+  double c[2];  // sum_i s_i y_i over the CTA's rows
+  double n[2];  // ||R_rows||^2
+};
+
+constexpr int kMaxStages = 16;
+
+// Per-CTA controller block in shared memory.
+struct Ctl {
+  unsigned long long full[kMaxStages];   // TMA -> dot warps
+  unsigned long long empty[kMaxStages];  // z warps -> TMA
+  volatile int decided;  // kinds of passes [0, decided) are published
+  volatile int stored;   // global-R writes of passes [0, stored) are complete
+  volatile int abort;
+  volatile int kind_ring[4];
+  // controller state (thread 0 writes, consumers read after a named barrier)
+  int kind, pp, term, restart, tsel, utsel, best_tsel, best_sweeps;
+  int cur, nxt, best, need_reduce, norm_idx, pad0;
+  double alpha, c_prev, best_c, first_value;
+  double cred[32];
+  double nred[32];
+};
+
+struct KParams {
+  void* R;             // m x pitch, row-major, pad columns zero
+  long long pitch;     // elements per row (multiple of 32)
+  int m, n;
+  int G;               // CTAs (one per SM)
+  int rows_base, rows_rem;
+  int res_rows;        // rows per CTA kept resident in shared memory
+  int ds;              // dot warps sharing one row (column segments)
+  int stages;          // TMA ring depth (one row per stage)
+  int Q;               // 32-column slices = pitch / 32
+  int sw;              // u32 words of per-CTA sign bits
+  int zl;              // local slices per reduction group (zseg capacity)
+  int rows_max;        // max rows per CTA
+  const uint32_t* t0;  // [width][restarts][t0_stride] start vectors (u32 view)
+  int t0_stride;       // u32 words per start vector (= 2 * ceil(n/64))
+  unsigned long long* tb64;  // [2][Q] t words tagged with the consuming pass: (P << 32) | word
+  uint32_t* tbest;     // [Q] t of the best restart so far (restarts > 1)
+  double* zpart;       // [G][pitch] per-CTA column partials
+  Slot* slots;         // [G] c / ||R||^2 partials
+  unsigned* bar;       // grid barrier counter
+  unsigned* err_pass;  // [3] first pass index that saw an error (UINT_MAX = none)
+  uint32_t* S_out;     // [width][s_stride] u32 view of packed row signs
+  int s_stride;
+  uint32_t* T_out;     // [width][t_stride]
+  int t_stride;
+  double* c_out;       // [width]
+  uint32_t* sweeps_out;  // [width]
+  double* norm2_out;   // [width + 1]: [0] = ||A||^2, [k+1] = ||R after term k||^2
+  unsigned long long* stats;  // [0] width_done, [1] passes
+  long long width, restarts, max_sweeps;
+  double min_frac;
+  double numel_d;
+  unsigned long long* prof;  // [G][16] clock64 breakdown or nullptr
+};
+
+// Kernel variant: warp roles and per-thread register tiles.
+struct Variant {
+  int dtype;  // 0 f32, 1 f64
+  int nd;     // dot warps
+  int nz;     // column-accumulator (z) warps
+  int zv;     // 16-byte vectors per z thread per row
+};
+
+// Shared-memory carve-up (byte offsets from the dynamic smem base).
+struct Layout {
+  size_t stage, res, ctl, red, yrow, tws, uws, cnt, negf, ready, zseg, sb, total;
+};
+
+inline __host__ __device__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+
+inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_rows, int ds, int rows_max,
+                                              int Q, int zl, int cw, int sw) {
+  Layout L;
+  const size_t slots = static_cast<size_t>(stages + res_rows);
+  size_t o = 0;
+  L.stage = o;
+  o += static_cast<size_t>(stages) * rowB;
+  L.res = o;
+  o += static_cast<size_t>(res_rows) * rowB;
+  L.ctl = o;
+  o += align16(sizeof(Ctl));
+  L.red = o;
+  o += align16(slots * ds * 8);
+  L.yrow = o;
+  o += align16(static_cast<size_t>(rows_max) * 8);
+  L.tws = o;
+  o += align16(static_cast<size_t>(Q) * 4);
+  L.uws = o;
+  o += align16(static_cast<size_t>(Q) * 4);
+  L.cnt = o;
+  o += align16(slots * 4);
+  L.negf = o;
+  o += align16(slots * 4);
+  L.ready = o;
+  o += align16(slots * 8);
+  L.zseg = o;
+  o += static_cast<size_t>(zl) * cw * 32 * 8;
+  L.sb = o;
+  o += align16(static_cast<size_t>(3) * sw * 4);
+  L.total = o;
+  return L;
+}
+
+// Returns 0 on success.
+int pick_variant(int dtype, long long pitch, Variant* v);
+cudaError_t set_smem_limit(const Variant& v, size_t bytes);
+cudaError_t launch_sweep(const Variant& v, const KParams& p, size_t smem_bytes, cudaStream_t st);
+
+}  // namespace scb
