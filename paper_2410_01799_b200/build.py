@@ -18,6 +18,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-cudart", "static",
          "-Xptxas", "-v" if os.environ.get("SCB_PTXAS_VERBOSE") else "-O3"]
+if os.environ.get("SCB_PROFILE"):  # clock64 phase breakdown compiled in (tuning builds only)
+    FLAGS += ["-DSCB_PROFILE=1"]
 
 
 def _stale() -> bool:

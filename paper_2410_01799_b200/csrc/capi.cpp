@@ -260,18 +260,13 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   const int sw = (rows_max + 31) / 32;
   const int zl = std::max(1, std::min(4, (Q + G - 1) / G));
   const size_t rowB = static_cast<size_t>(pitch) * es;
-  const int CW = var.nd + var.nz;
-  // dot warps sharing a row: wide rows are split across warps so fewer rows
-  // need to sit in the ring at once (more shared memory stays resident)
-  int ds = static_cast<int>(env_size("SCB_DS", rowB >= 8192 ? 2 : 1));
-  if (ds < 1 || var.nd % ds != 0) ds = 1;
   auto smem_for = [&](int st_, int res_) {
-    return scb::make_layout(rowB, st_, res_, ds, rows_max, Q, zl, CW, sw).total;
+    return scb::make_layout(rowB, st_, res_, var.rg, var.nw, rows_max, Q, zl, sw).total;
   };
   const size_t cap = ctx->smem_optin;
   int stages = 0, res_rows = rows_max;
   if (smem_for(0, rows_max) > cap) {
-    stages = static_cast<int>(env_size("SCB_STAGES", static_cast<size_t>(var.nd / ds + 4)));
+    stages = static_cast<int>(env_size("SCB_STAGES", static_cast<size_t>(2 * var.rg + 4)));
     stages = std::max(2, std::min(stages, scb::kMaxStages));
     while (stages > 2 && smem_for(stages, 0) > cap) --stages;
     if (smem_for(stages, 0) > cap)
@@ -359,7 +354,6 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   kp.rows_base = rows_base;
   kp.rows_rem = rows_rem;
   kp.res_rows = res_rows;
-  kp.ds = ds;
   kp.rows_max = rows_max;
   kp.stages = stages;
   kp.Q = Q;
@@ -420,9 +414,9 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
     for (int g = 0; g < G; ++g)
       for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(hp[g * 16 + i]) / G;
     std::fprintf(stderr,
-                 "[scb prof] G=%d res_rows=%d stages=%d ds=%d nd=%d nz=%d zv=%d smem=%zu | cycles/CTA: "
-                 "fullwait=%.0f chunks=%.0f passend+bar=%.0f decision=%.0f reduce+bar=%.0f | z: readywait=%.0f loop=%.0f | prod emptywait=%.0f  (per pass: chunks %.0f) passes=%llu\n",
-                 G, res_rows, stages, ds, var.nd, var.nz, var.zv, smem, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7],
+                 "[scb prof] G=%d res_rows=%d stages=%d nw=%d vpt=%d rg=%d smem=%zu | cycles/CTA: "
+                 "fullwait=%.0f chunks=%.0f passend+bar=%.0f decision=%.0f reduce+bar=%.0f | staging=%.0f ringwait=%.0f | prod emptywait=%.0f  (per pass: chunks %.0f) passes=%llu\n",
+                 G, res_rows, stages, var.nw, var.vpt, var.rg, smem, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7],
                  acc[1] / std::max<double>(1.0, static_cast<double>(h_stats[1])),
                  static_cast<unsigned long long>(h_stats[1]));
   }

@@ -11,18 +11,17 @@
 // the rest are streamed every pass, one row per stage, by a TMA bulk-copy
 // producer thread (cp.async.bulk + mbarrier ring).
 //
-// Warp roles inside a CTA (no block-wide barrier inside the row loop):
-//   * dot warps: `ds` of them share a row, each summing its column segment
-//     of y_i = sum_j t_j R_ij (matvec_signed, inc/kernels.hpp:61-71) in f64;
-//     the last segment to finish (shared-memory counter) adds the segment
-//     partials in a fixed order, records y_i, s'_i = [y_i < 0] (sgn_vector,
-//     sign_vector.hpp:107-114) and signals the row ready.  In the first pass
-//     of a term they also apply the previous term's rank-1 deflation
-//     R -= alpha s t^T (flush_pending with one term, decompose.hpp:200-214)
-//     in place and accumulate ||R||_F^2.
-//   * z warps: take rows in sequence order and accumulate z += s'_i R_i
-//     (matvec_signed_t, inc/kernels.hpp:74-88) into f64 registers, then hand
-//     the stage back to the producer.
+// Consumer warps (no block-wide barrier inside the row loop): every warp owns
+// a column segment of every row.  Rows are taken in groups; for group g each
+// warp loads its segment from shared memory ONCE into registers, (in the first
+// pass of a term) applies the previous term's rank-1 deflation
+// R -= alpha s t^T in place (flush_pending with one term, decompose.hpp:200-214),
+// sums its part of y_i = sum_j t_j R_ij (matvec_signed, inc/kernels.hpp:61-71)
+// in f64 and publishes it through an mbarrier ring; it then takes the combined
+// y of group g-1 (fixed warp order), records s'_i = [y_i < 0] (sgn_vector,
+// sign_vector.hpp:107-114) and adds s'_i R_i of group g-1 -- still in its
+// registers -- into its f64 column accumulators (matvec_signed_t,
+// inc/kernels.hpp:74-88).  The lag hides the cross-warp combine latency.
 //
 // Cross-CTA exchange per pass (no float atomics, deterministic):
 //   * every CTA stores its column partials and its c / ||R||^2 partials
@@ -58,15 +57,31 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t b
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
 }
+#ifndef SCB_WAIT_HINT_NS
+#define SCB_WAIT_HINT_NS 0
+#endif
+__device__ __forceinline__ void mbar_arrive_cnt(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(unsigned long long* b, uint32_t parity) {
   uint32_t ok;
+#if SCB_WAIT_HINT_NS > 0
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(saddr(b)), "r"(parity), "r"(0x989680u)
+      : "r"(saddr(b)), "r"(parity), "r"(SCB_WAIT_HINT_NS)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(saddr(b)), "r"(parity)
+      : "memory");
+#endif
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
@@ -145,13 +160,248 @@ __device__ __forceinline__ uint32_t vec_bits(const uint32_t* words, int v) {
 }
 __device__ __forceinline__ uint32_t bitmask(uint32_t bits, int e) { return (bits << (31 - e)) & 0x80000000u; }
 
-// ---------------------------------------------------------------------------
-template <typename E, int ND, int NZ, int ZV>
-__global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KParams p) {
+
+// Sum RG per-lane partials over the warp with a transposed butterfly: the first
+// log2(RG) levels exchange whole rows (each lane keeps half of its rows), the
+// remaining levels reduce one value.  Row r's total ends up in lane
+// holder_lane<RG>(r); the addition order is fixed, so results are reproducible.
+template <int RG>
+__device__ __forceinline__ double warp_reduce_rows(double (&p)[RG], int lane) {
+  if constexpr (RG == 1) {
+    double v = p[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  } else if constexpr (RG == 2) {
+    const bool up = lane & 16;
+    const double keep = up ? p[1] : p[0], send = up ? p[0] : p[1];
+    double v = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  } else {
+    static_assert(RG == 4, "RG must be 1, 2 or 4");
+    const bool up = lane & 16;
+    const double k0 = up ? p[2] : p[0], k1 = up ? p[3] : p[1];
+    const double s0 = up ? p[0] : p[2], s1 = up ? p[1] : p[3];
+    const double q0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+    const double q1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+    const bool b3 = lane & 8;
+    double v = (b3 ? q1 : q0) + __shfl_xor_sync(0xffffffffu, b3 ? q0 : q1, 8);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  }
+}
+template <int RG>
+__device__ __forceinline__ int holder_lane(int r) {
+  return RG == 1 ? 0 : (RG == 2 ? r * 16 : (r >> 1) * 16 + (r & 1) * 8);
+}
+
+
+// Arguments of one dot pass (kept small: only hot-loop state is live inside).
+// Shared-memory regions are passed as 32-bit offsets from the dynamic smem base
+// so the callee addresses them with LDS/STS.
+struct DotArgs {
+  unsigned res, stage, full, empty, ring, rred, yrow, s_nxt, tws;
+  double* zrow;
+  unsigned* errp;
+  unsigned rowB;
+  int rows_g, nres, D, NV, sslot, sph, P;
+  unsigned gcount;
+};
+
+template <typename E, int NW, int VPT, int RG>
+__device__ __noinline__ void dot_pass(const DotArgs a) {
   constexpr int EPV = Vec<E>::N;
-  constexpr int CW = ND + NZ;  // consumer warps
+  constexpr int NE = VPT * EPV;
+  using VT = typename Vec<E>::T;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows_g = a.rows_g, nres = a.nres, D = a.D, NV = a.NV, P = a.P;
+  const unsigned gcount = a.gcount;
+  const size_t rowB = a.rowB;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const unsigned char* res_base = smem + a.res;
+  const unsigned char* stage_base = smem + a.stage;
+  double* rred = reinterpret_cast<double*>(smem + a.rred);
+  unsigned long long* ring = reinterpret_cast<unsigned long long*>(smem + a.ring);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + a.full);
+  unsigned long long* empty = reinterpret_cast<unsigned long long*>(smem + a.empty);
+  double* yrow = reinterpret_cast<double*>(smem + a.yrow);
+  uint32_t* s_nxt = reinterpret_cast<uint32_t*>(smem + a.s_nxt);
+  const uint32_t* tws = reinterpret_cast<const uint32_t*>(smem + a.tws);
+  int sslot = a.sslot, sph = a.sph;
+  int vidx[VPT];
+  bool vok[VPT];
+  bool all_ok = true;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int v = (k * NW + warp) * 32 + lane;
+    vok[k] = v < NV;
+    vidx[k] = vok[k] ? v : 0;
+    all_ok = all_ok && vok[k];
+  }
+  all_ok = __all_sync(0xffffffffu, all_ok);
+  double zacc[NE];
+#pragma unroll
+  for (int i = 0; i < NE; ++i) zacc[i] = 0.0;
+  constexpr unsigned long long* prof = nullptr;
+  long long pacc[8];
+      // ======================= dot pass (the hot loop) =======================
+      // per-thread t sign bits of the owned elements (bit i = element i)
+      uint32_t tbits = 0;
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        const int col0 = ((k * NW + warp) * 32 + lane) * EPV;
+        if (vok[k]) tbits |= ((tws[col0 >> 5] >> (col0 & 31)) & ((1u << EPV) - 1u)) << (k * EPV);
+      }
+      const int ngroups = (rows_g + RG - 1) / RG;
+      // A(grp): wait for the group's rows, load this thread's segment, dot
+      // partials, transposed warp reduction, publish to the ring, free stages
+      auto step_a = [&](E (&x)[RG][NE], int grp) {
+        int sl[RG];
+        const VT* rp[RG];
+#pragma unroll
+        for (int r = 0; r < RG; ++r) {
+          const int jr = grp * RG + r;
+          const int j = jr < rows_g ? jr : rows_g - 1;  // past-the-end rows alias the last row
+          sl[r] = -1;
+          if (j < nres) {
+            rp[r] = reinterpret_cast<const VT*>(res_base + static_cast<size_t>(j) * rowB);
+          } else if (jr < rows_g) {
+            if (prof && tid == 0) {
+              const long long tw0 = clock64();
+              mbar_wait(&full[sslot], static_cast<uint32_t>(sph));
+              pacc[0] += clock64() - tw0;
+            } else {
+              mbar_wait(&full[sslot], static_cast<uint32_t>(sph));
+            }
+            rp[r] = reinterpret_cast<const VT*>(stage_base + static_cast<size_t>(sslot) * rowB);
+            sl[r] = sslot;
+            if (++sslot == D) {
+              sslot = 0;
+              sph ^= 1;
+            }
+          } else {
+            rp[r] = rp[r > 0 ? r - 1 : 0];
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < RG; ++r)
+#pragma unroll
+          for (int k = 0; k < VPT; ++k) Vec<E>::split(rp[r][vidx[k]], &x[r][k * EPV]);
+        if (!all_ok || grp * RG + RG > rows_g) {  // rare: ragged row tail / past-the-end rows
+#pragma unroll
+          for (int r = 0; r < RG; ++r) {
+            const bool rok = grp * RG + r < rows_g;
+#pragma unroll
+            for (int k = 0; k < VPT; ++k)
+              if (!(vok[k] && rok)) {
+#pragma unroll
+                for (int e = 0; e < EPV; ++e) x[r][k * EPV + e] = E(0);
+              }
+          }
+        }
+        double part[RG];
+        uint32_t tb = tbits;
+        asm volatile("" : "+r"(tb));  // keep the per-element masks out of the loop preheader
+#pragma unroll
+        for (int r = 0; r < RG; ++r) {
+          double ac[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int i = 0; i < NE; ++i) ac[i & 3] += flipd(static_cast<double>(x[r][i]), bitmask(tb, i));
+          part[r] = (ac[0] + ac[1]) + (ac[2] + ac[3]);
+        }
+        const double v = warp_reduce_rows<RG>(part, lane);
+        const unsigned gi = gcount + static_cast<unsigned>(grp);
+        double* pr = rred + static_cast<size_t>(gi & (kRing - 1)) * RG * NW;
+#pragma unroll
+        for (int r = 0; r < RG; ++r)
+          if (lane == holder_lane<RG>(r)) pr[r * NW + warp] = v;
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&ring[gi & (kRing - 1)]);
+#pragma unroll
+          for (int r = 0; r < RG; ++r)
+            if (sl[r] >= 0) mbar_arrive(&empty[sl[r]]);
+        }
+      };
+      // B(grp): combined y of the group (fixed warp order), s' bits, z update
+      auto step_b = [&](const E (&x)[RG][NE], int grp) {
+        const unsigned gi = gcount + static_cast<unsigned>(grp);
+        if (prof && tid == 0) {
+          const long long tw0 = clock64();
+          mbar_wait(&ring[gi & (kRing - 1)], (gi / kRing) & 1u);
+          pacc[6] += clock64() - tw0;
+        } else {
+          mbar_wait(&ring[gi & (kRing - 1)], (gi / kRing) & 1u);
+        }
+        const double* pr = rred + static_cast<size_t>(gi & (kRing - 1)) * RG * NW;
+        double y = 0.0;
+        if (lane < RG) {
+#pragma unroll
+          for (int w = 0; w < NW; ++w) y += pr[lane * NW + w];
+        }
+        const unsigned negb = __ballot_sync(0xffffffffu, lane < RG && y < 0.0);
+        if (warp == 0 && lane < RG) {
+          const int j = grp * RG + lane;
+          if (j < rows_g) {
+            yrow[j] = y;
+            if (!isfinite(y)) atomicMin(a.errp + ERR_Y, static_cast<unsigned>(P));
+            if (y < 0.0) atomicOr(&s_nxt[j >> 5], 1u << (j & 31));
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < RG; ++r) {
+          if ((negb >> r) & 1u) {
+#pragma unroll
+            for (int i = 0; i < NE; ++i) zacc[i] -= static_cast<double>(x[r][i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NE; ++i) zacc[i] += static_cast<double>(x[r][i]);
+          }
+        }
+      };
+      E xa[RG][NE], xb[RG][NE];
+      // software pipeline: A(g) runs ahead of B(g-1) by one group
+      step_a(xa, 0);
+      int gI = 1;
+      for (; gI + 1 < ngroups; gI += 2) {
+        step_a(xb, gI);
+        step_b(xa, gI - 1);
+        step_a(xa, gI + 1);
+        step_b(xb, gI);
+      }
+      if (gI < ngroups) {
+        step_a(xb, gI);
+        step_b(xa, gI - 1);
+        step_b(xb, gI);
+      } else {
+        step_b(xa, gI - 1);
+      }
+
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    if (vok[k]) {
+#pragma unroll
+      for (int e = 0; e < EPV; e += 2)
+        __stcg(reinterpret_cast<double2*>(a.zrow + vidx[k] * EPV + e), make_double2(zacc[k * EPV + e], zacc[k * EPV + e + 1]));
+    }
+  }
+  (void)pacc;
+}
+
+// ---------------------------------------------------------------------------
+// Column ownership: consumer thread (warp w, lane l) owns the 16-byte vectors
+// v_k = (k * NW + w) * 32 + l, k < VPT, of every row (coalesced LDS.128), i.e.
+// NE = VPT * EPV elements per row, and the matching NE f64 column accumulators.
+template <typename E, int NW, int VPT, int RG, bool KEEP>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p) {
+  constexpr int EPV = Vec<E>::N;
+  constexpr int CW = NW;       // consumer warps
   constexpr int CT = CW * 32;  // consumer threads
-  constexpr int ZE = ZV * EPV; // f64 column accumulators per z thread
+  constexpr int NE = VPT * EPV;
+  static_assert(NE <= 32, "sign bits of a thread's elements must fit one word");
   static_assert(CW <= 32, "controller arrays hold 32 warps");
   using VT = typename Vec<E>::T;
 
@@ -169,31 +419,28 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
   const int nres = min(rows_g, p.res_rows);
   const int nstream = rows_g - nres;
   const int D = p.stages;
-  const int DS = p.ds;
 
-  const Layout L = make_layout(rowB, D, p.res_rows, DS, p.rows_max, p.Q, p.zl, CW, p.sw);
+  const Layout L = make_layout(rowB, D, p.res_rows, RG, NW, p.rows_max, p.Q, p.zl, p.sw);
   unsigned char* stage_base = smem + L.stage;
   unsigned char* res_base = smem + L.res;
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + L.ctl);
-  volatile double* red = reinterpret_cast<volatile double*>(smem + L.red);  // [slot][ds]
-  double* yrow = reinterpret_cast<double*>(smem + L.yrow);                  // [rows_max]
-  uint32_t* tws = reinterpret_cast<uint32_t*>(smem + L.tws);                // [Q] t of this pass
-  uint32_t* uws = reinterpret_cast<uint32_t*>(smem + L.uws);                // [Q] t of the update
-  int* cnt = reinterpret_cast<int*>(smem + L.cnt);                          // [slot]
-  volatile int* negf = reinterpret_cast<volatile int*>(smem + L.negf);      // [slot]
-  unsigned long long* ready = reinterpret_cast<unsigned long long*>(smem + L.ready);  // [slot]
-  double* zseg = reinterpret_cast<double*>(smem + L.zseg);                  // [zl][CW][32]
-  uint32_t* sb = reinterpret_cast<uint32_t*>(smem + L.sb);                  // [3][sw]
+  unsigned long long* ring = reinterpret_cast<unsigned long long*>(smem + L.ring);  // [kRing] mbarriers
+  double* rred = reinterpret_cast<double*>(smem + L.rred);                 // [kRing][RG][NW] dot partials
+  double* yrow = reinterpret_cast<double*>(smem + L.yrow);                 // [rows_max]
+  uint32_t* tws = reinterpret_cast<uint32_t*>(smem + L.tws);               // [Q] t of this pass
+  uint32_t* uws = reinterpret_cast<uint32_t*>(smem + L.uws);               // [Q] t of the update
+  double* zseg = reinterpret_cast<double*>(smem + L.zseg);                 // [zl][CW][32]
+  uint32_t* sb = reinterpret_cast<uint32_t*>(smem + L.sb);                 // [3][sw]
   E* R = static_cast<E*>(p.R);
 
   if (tid == 0) {
     for (int s = 0; s < D; ++s) {
       mbar_init(&ctl->full[s], 1);
-      mbar_init(&ctl->empty[s], NZ);
+      mbar_init(&ctl->empty[s], NW);
     }
-    for (int s = 0; s < D + p.res_rows; ++s) mbar_init(&ready[s], 1);
+    for (int s = 0; s < kRing; ++s) mbar_init(&ring[s], NW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const int k0 = p.width == 0 ? (F_NORM | F_WB | F_CHECK) : (F_DOT | F_NORM | F_CHECK);
+    const int k0 = p.width == 0 ? (F_NORM | F_WB | F_CHECK) : (F_NORM | F_CHECK);
     ctl->kind = k0;
     ctl->kind_ring[0] = k0;
     ctl->decided = 1;
@@ -217,7 +464,6 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
     ctl->first_value = 0.0;
   }
   for (int i = tid; i < 3 * p.sw; i += blockDim.x) sb[i] = 0u;
-  for (int i = tid; i < D + p.res_rows; i += blockDim.x) cnt[i] = 0;
   // resident rows: loaded once for the whole decomposition
   for (int l = 0; l < nres; ++l) {
     const VT* src = reinterpret_cast<const VT*>(R + static_cast<size_t>(r0 + l) * pitch);
@@ -272,16 +518,24 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
   }
 
   // ========================= consumers (CT threads) ========================
-  unsigned long long* prof = p.prof;  // optional clock64 breakdown (SCB_PROF=1)
+#ifdef SCB_PROFILE
+  unsigned long long* prof = p.prof;  // clock64 breakdown (build with SCB_PROFILE=1, run with SCB_PROF=1)
+#else
+  constexpr unsigned long long* prof = nullptr;
+#endif
   long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const unsigned* errp = p.err_pass;
-  const bool is_dot = warp < ND;
-  const int nrf = ND / DS;                    // rows in flight in the dot stage
-  const int rgrp = warp / DS, part = warp % DS;
-  const int vb = (part * NV) / DS, ve = ((part + 1) * NV) / DS;
-  const int zt = tid - ND * 32;               // z thread index (z warps)
-  int qs = 0, qph = 0;                        // stage / phase of this pass's first streamed row
-  unsigned epoch = 0;                         // grid barriers passed (thread 0)
+  int qs = 0, qph = 0;     // stage / phase of this pass's first streamed row
+  unsigned gcount = 0;     // dot-partial groups published in earlier passes
+  unsigned epoch = 0;      // grid barriers passed (thread 0)
+  int vidx[VPT];           // owned vectors (clamped to a valid address when out of range)
+  bool vok[VPT];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int v = (k * NW + warp) * 32 + lane;
+    vok[k] = v < NV;
+    vidx[k] = vok[k] ? v : 0;
+  }
 
   for (int P = 0;; ++P) {
     const int kind = ctl->kind;
@@ -300,7 +554,7 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
             p.t0 + (static_cast<size_t>(ctl->term) * p.restarts + ctl->restart) * p.t0_stride;
         for (int i = tid; i < p.Q; i += CT) tws[i] = __ldg(tw + i);
       } else {
-        // t words tagged with the pass index: poll the data itself
+        // t words were published before the last grid barrier, tagged with this pass
         const unsigned long long* tw = p.tb64 + static_cast<size_t>(ctl->tsel) * p.Q;
         for (int i = tid; i < p.Q; i += CT) {
           unsigned long long x;
@@ -319,181 +573,80 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
                                  : static_cast<uint32_t>(__ldcg(p.tb64 + static_cast<size_t>(ctl->utsel) * p.Q + i));
     }
     consumer_sync(CT);
+    if (prof && tid == 0) pacc[5] += clock64() - t_pass0;
 
-    double zacc[ZE];
-#pragma unroll
-    for (int i = 0; i < ZE; ++i) zacc[i] = 0.0;
     double nacc = 0.0;
     bool bad = false;
+    int sslot = qs, sph = qph;  // streamed-row cursor (identical in all consumer threads)
 
-    if (is_dot) {
-      // ========================= dot warps =========================
-      // streamed row k of this pass lives in stage (qs + k) % D, phase qph ^ ...
-      int js = rgrp < nres ? rgrp : rgrp;  // first row of this group
-      int sslot = 0, sph = 0;               // stage / phase of this group's next streamed row
-      {
-        int j0 = rgrp;
-        while (j0 < nres) j0 += nrf;
-        const int t = qs + (j0 - nres);
-        sslot = t % (D > 0 ? D : 1);
-        sph = qph ^ ((t / (D > 0 ? D : 1)) & 1);
-      }
-      for (int j = js; j < rows_g; j += nrf) {
-        const bool streamed = j >= nres;
-        int slot;
-        unsigned char* rowp;
-        if (!streamed) {
-          slot = D + j;
-          rowp = res_base + static_cast<size_t>(j) * rowB;
-        } else {
-          slot = sslot;
-          if (prof && tid == 0) {
-            const long long tw0 = clock64();
-            mbar_wait(&ctl->full[slot], static_cast<uint32_t>(sph));
-            pacc[0] += clock64() - tw0;
-          } else {
-            mbar_wait(&ctl->full[slot], static_cast<uint32_t>(sph));
-          }
-          rowp = stage_base + static_cast<size_t>(slot) * rowB;
-          sslot += nrf;
-          while (sslot >= D) {
-            sslot -= D;
-            sph ^= 1;
-          }
-        }
-        VT* rv = reinterpret_cast<VT*>(rowp);
-        if (kind & (F_UPD | F_WB)) {
-          const uint32_t sneg = ((s_upd[j >> 5] >> (j & 31)) & 1u) << 31;
-          VT* grow = reinterpret_cast<VT*>(R + static_cast<size_t>(r0 + j) * pitch);
-          for (int v = vb + lane; v < ve; v += 32) {
-            E x[EPV];
-            Vec<E>::split(rv[v], x);
-            if (kind & F_UPD) {
-              const uint32_t ub = vec_bits<EPV>(uws, v);
-#pragma unroll
-              for (int e = 0; e < EPV; ++e)
-                if (v * EPV + e < p.n)  // flush_pending with one term: data += flip(-alpha, s_i ^ t_j)
-                  x[e] = Vec<E>::narrow(static_cast<double>(x[e]) + flipd(-alpha, sneg ^ bitmask(ub, e)));
-              rv[v] = Vec<E>::join(x);
-            }
-            if (streamed || (kind & F_WB)) grow[v] = Vec<E>::join(x);
-          }
-        }
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        if (kind == F_DOT) {
-          // hot loop: 4 vectors in flight per lane, one f64 chain per vector slot
-          int v = vb + lane;
-          for (; v + 96 < ve; v += 128) {
-            E x[4][EPV];
-            uint32_t bb[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) Vec<E>::split(rv[v + 32 * u], x[u]);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) bb[u] = vec_bits<EPV>(tws, v + 32 * u);
-#pragma unroll
-            for (int e = 0; e < EPV; ++e) {
-              a0 += flipd(static_cast<double>(x[0][e]), bitmask(bb[0], e));
-              a1 += flipd(static_cast<double>(x[1][e]), bitmask(bb[1], e));
-              a2 += flipd(static_cast<double>(x[2][e]), bitmask(bb[2], e));
-              a3 += flipd(static_cast<double>(x[3][e]), bitmask(bb[3], e));
-            }
-          }
-          for (; v < ve; v += 32) {
-            E x[EPV];
-            Vec<E>::split(rv[v], x);
-            const uint32_t b = vec_bits<EPV>(tws, v);
-#pragma unroll
-            for (int e = 0; e < EPV; ++e) a0 += flipd(static_cast<double>(x[e]), bitmask(b, e));
-          }
-        } else if (kind & (F_DOT | F_NORM)) {
-          for (int v = vb + lane; v < ve; v += 32) {
-            E x[EPV];
-            Vec<E>::split(rv[v], x);
-            const uint32_t b = (kind & F_DOT) ? vec_bits<EPV>(tws, v) : 0u;
-#pragma unroll
-            for (int e = 0; e < EPV; ++e) {
-              const double d = static_cast<double>(x[e]);
-              if (kind & F_NORM) {
-                nacc += d * d;
-                if (kind & F_CHECK) bad |= !isfinite(d);
-              }
-              const double f = flipd(d, bitmask(b, e));
-              if (e & 1) a1 += f; else a0 += f;
-            }
-          }
-        }
-        const double part_y = warp_sum((a0 + a1) + (a2 + a3));
-        if (lane == 0) {
-          red[slot * DS + part] = part_y;
-          __threadfence_block();
-          if (atomicAdd(&cnt[slot], 1) == DS - 1) {
-            __threadfence_block();
-            double y = 0.0;
-            for (int q = 0; q < DS; ++q) y += red[slot * DS + q];
-            cnt[slot] = 0;
-            if (kind & F_DOT) {
-              yrow[j] = y;
-              negf[slot] = y < 0.0 ? 1 : 0;
-              if (!isfinite(y)) atomicMin(const_cast<unsigned*>(errp) + ERR_Y, static_cast<unsigned>(P));
-              if (y < 0.0) atomicOr(&s_nxt[j >> 5], 1u << (j & 31));
-            }
-            __threadfence_block();
-            mbar_arrive(&ready[slot]);
-          }
-        }
-      }
+    if (kind & F_DOT) {
+      // ======================= dot pass (the hot loop) =======================
+      DotArgs da;
+      da.res = static_cast<unsigned>(L.res);
+      da.stage = static_cast<unsigned>(L.stage);
+      da.full = static_cast<unsigned>(reinterpret_cast<unsigned char*>(ctl->full) - smem);
+      da.empty = static_cast<unsigned>(reinterpret_cast<unsigned char*>(ctl->empty) - smem);
+      da.ring = static_cast<unsigned>(L.ring);
+      da.rred = static_cast<unsigned>(L.rred);
+      da.yrow = static_cast<unsigned>(L.yrow);
+      da.s_nxt = static_cast<unsigned>(reinterpret_cast<unsigned char*>(s_nxt) - smem);
+      da.tws = static_cast<unsigned>(L.tws);
+      da.zrow = p.zpart + static_cast<size_t>(g) * pitch;
+      da.errp = const_cast<unsigned*>(errp);
+      da.rowB = static_cast<unsigned>(rowB);
+      da.rows_g = rows_g;
+      da.nres = nres;
+      da.D = D;
+      da.NV = NV;
+      da.sslot = sslot;
+      da.sph = sph;
+      da.P = P;
+      da.gcount = gcount;
+      dot_pass<E, NW, VPT, RG>(da);
+      const int ngroups = (rows_g + RG - 1) / RG;
+      gcount += static_cast<unsigned>(ngroups);
     } else {
-      // ========================== z warps ==========================
-      int sslot = qs, sph = qph;
-      bool zvalid[ZV];
-      int zv_idx[ZV];
-#pragma unroll
-      for (int k = 0; k < ZV; ++k) {
-        const int v = zt + k * NZ * 32;
-        zvalid[k] = v < NV;
-        zv_idx[k] = v < NV ? v : 0;  // always a valid address; contribution masked
-      }
+      // ============ maintenance pass: update / norm / check / write-back ============
+      // (rank-1 deflation R -= alpha s t^T of the previous term, flush_pending with
+      // one term, decompose.hpp:200-214; ||R||_F^2; final write-back of resident rows).
+      // All warps walk the rows in order (each takes a column segment), so the
+      // stage ring is consumed in order and its phase parity is unambiguous.
       for (int j = 0; j < rows_g; ++j) {
-        const bool streamed = j >= nres;
-        int slot;
-        uint32_t par;
-        const VT* rv;
-        if (!streamed) {
-          slot = D + j;
-          par = static_cast<uint32_t>(P & 1);
-          rv = reinterpret_cast<const VT*>(res_base + static_cast<size_t>(j) * rowB);
+        VT* rv;
+        int slot = -1;
+        if (j < nres) {
+          rv = reinterpret_cast<VT*>(res_base + static_cast<size_t>(j) * rowB);
         } else {
           slot = sslot;
-          par = static_cast<uint32_t>(sph);
-          rv = reinterpret_cast<const VT*>(stage_base + static_cast<size_t>(slot) * rowB);
+          mbar_wait(&ctl->full[slot], static_cast<uint32_t>(sph));
+          rv = reinterpret_cast<VT*>(stage_base + static_cast<size_t>(slot) * rowB);
           if (++sslot == D) {
             sslot = 0;
             sph ^= 1;
           }
         }
-        if (prof && zt == 0) {
-          const long long tw0 = clock64();
-          mbar_wait(&ready[slot], par);
-          pacc[5] += clock64() - tw0;
-        } else {
-          mbar_wait(&ready[slot], par);
-        }
-        if (kind & F_DOT) {
-          const uint32_t negm = negf[slot] ? 0x80000000u : 0u;
-          constexpr int ZH = ZV > 4 ? 4 : ZV;  // loads in flight per group (register budget)
+        const uint32_t sneg = ((s_upd[j >> 5] >> (j & 31)) & 1u) << 31;
+        VT* grow = reinterpret_cast<VT*>(R + static_cast<size_t>(r0 + j) * pitch);
+        for (int v = tid; v < NV; v += CT) {
+          E x[EPV];
+          Vec<E>::split(rv[v], x);
+          if (kind & F_UPD) {
+            const uint32_t ub = (uws[(v * EPV) >> 5] >> ((v * EPV) & 31)) & ((1u << EPV) - 1u);
 #pragma unroll
-          for (int k0 = 0; k0 < ZV; k0 += ZH) {
-            E x[ZH][EPV];
+            for (int e = 0; e < EPV; ++e)
+              if (v * EPV + e < p.n)  // flush_pending with one term: data += flip(-alpha, s_i ^ t_j)
+                x[e] = Vec<E>::narrow(static_cast<double>(x[e]) + flipd(-alpha, sneg ^ bitmask(ub, e)));
+            if (j < nres) rv[v] = Vec<E>::join(x);
+          }
+          if ((j >= nres && (kind & F_UPD)) || (kind & F_WB)) grow[v] = Vec<E>::join(x);
 #pragma unroll
-            for (int k = 0; k < ZH; ++k) Vec<E>::split(rv[zv_idx[k0 + k]], x[k]);
-#pragma unroll
-            for (int k = 0; k < ZH; ++k)
-#pragma unroll
-              for (int e = 0; e < EPV; ++e)
-                if (zvalid[k0 + k]) zacc[(k0 + k) * EPV + e] += flipd(static_cast<double>(x[k][e]), negm);
+          for (int e = 0; e < EPV; ++e) {
+            const double d = static_cast<double>(x[e]);
+            nacc += d * d;
+            if (kind & F_CHECK) bad |= !isfinite(d);
           }
         }
-        if (streamed) {
+        if (slot >= 0) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&ctl->empty[slot]);
         }
@@ -504,7 +657,6 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
       qph ^= (t / D) & 1;
       qs = t % D;
     }
-    if (prof && zt == 0) pacc[6] += clock64() - t_pass0;
 
     // ------------------------------ pass end ------------------------------
     if (prof && tid == 0) {
@@ -516,20 +668,7 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
       asm volatile("fence.proxy.async.global;" ::: "memory");
       __threadfence();
     }
-    if (!is_dot && (kind & F_DOT)) {
-      double* zrow = p.zpart + static_cast<size_t>(g) * pitch;
-#pragma unroll
-      for (int k = 0; k < ZV; ++k) {
-        const int v = zt + k * NZ * 32;
-        if (v < NV) {
-#pragma unroll
-          for (int e = 0; e < EPV; e += 2)
-            __stcg(reinterpret_cast<double2*>(zrow + v * EPV + e),
-                   make_double2(zacc[k * EPV + e], zacc[k * EPV + e + 1]));
-        }
-      }
-    }
-    if (is_dot && (kind & F_NORM)) {
+    if (kind & F_NORM) {
       const double ws = warp_sum(nacc);
       if (lane == 0) ctl->nred[warp] = ws;
       if (bad) atomicMin(const_cast<unsigned*>(errp) + ERR_INPUT, static_cast<unsigned>(P));
@@ -549,7 +688,7 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
         }
         double nsum = 0.0;
         if (kind & F_NORM)
-          for (int w = 0; w < ND; ++w) nsum += ctl->nred[w];
+          for (int w = 0; w < CW; ++w) nsum += ctl->nred[w];
         Slot* my = p.slots + g;
         __stcg(&my->c[P & 1], cl);
         __stcg(&my->n[P & 1], nsum);
@@ -596,8 +735,10 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
         next = K_TERM;
       } else {
         if ((kind & F_NORM) && g == 0) p.norm2_out[ctl->norm_idx] = ns;
-        if (!(kind & F_DOT)) {
-          next = K_TERM;
+        if (kind & F_WB) {
+          next = K_TERM;  // final write-back done
+        } else if (!(kind & F_DOT)) {
+          next = F_DOT;   // maintenance pass (initial norm / rank-1 update) -> search
         } else if (pp == 0) {
           const int t = ctl->cur;  // s_1 (just computed) becomes current
           ctl->cur = ctl->nxt;
@@ -677,7 +818,7 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
                 if (term + 1 >= p.width) {
                   next = F_UPD | F_NORM | F_WB;
                 } else {
-                  next = F_DOT | F_UPD | F_NORM;
+                  next = F_UPD | F_NORM;  // deflate, then search the next term
                   ctl->pp = 0;
                   ctl->restart = 0;
                   ctl->tsel = -1;
@@ -748,35 +889,31 @@ __global__ void __launch_bounds__((ND + NZ + 1) * 32, 1) sweep_kernel(const KPar
   }
   if (tid == 0) ctl->abort = 1;  // release a producer still waiting on an unconsumed stage
   if (prof && tid == 0)
-    for (int i = 0; i < 5; ++i) prof[g * 16 + i] = static_cast<unsigned long long>(pacc[i]);
-  if (prof && zt == 0)
-    for (int i = 5; i < 7; ++i) prof[g * 16 + i] = static_cast<unsigned long long>(pacc[i]);
+    for (int i = 0; i < 7; ++i) prof[g * 16 + i] = static_cast<unsigned long long>(pacc[i]);
 }
 
-template <typename E, int ND, int NZ, int ZV>
+template <typename E, int NW, int VPT, int RG, bool KEEP>
 struct Kern {
-  static void* fn() { return reinterpret_cast<void*>(&sweep_kernel<E, ND, NZ, ZV>); }
+  static void* fn() { return reinterpret_cast<void*>(&sweep_kernel<E, NW, VPT, RG, KEEP>); }
 };
 
 void* kernel_for(const Variant& v) {
-#define SCB_K(E, ND, NZ, ZV) \
-  if (v.nd == ND && v.nz == NZ && v.zv == ZV) return Kern<E, ND, NZ, ZV>::fn();
+#define SCB_K(E, NW, VPT, RG) \
+  if (v.nw == NW && v.vpt == VPT && v.rg == RG && v.keep == 1) return Kern<E, NW, VPT, RG, true>::fn();
   if (v.dtype == 0) {
-    SCB_K(float, 4, 1, 1)
-    SCB_K(float, 4, 1, 4)
-    SCB_K(float, 8, 2, 4)
-    SCB_K(float, 8, 4, 4)
-    SCB_K(float, 8, 4, 8)
-    SCB_K(float, 8, 8, 4)
-    SCB_K(float, 8, 8, 8)
+    SCB_K(float, 8, 1, 4)
+    SCB_K(float, 8, 2, 2)
+    SCB_K(float, 8, 4, 2)
+    SCB_K(float, 8, 4, 1)
+    SCB_K(float, 16, 2, 2)
+    SCB_K(float, 16, 2, 1)
+    SCB_K(float, 8, 8, 1)
   } else {
-    SCB_K(double, 4, 1, 1)
-    SCB_K(double, 4, 1, 4)
-    SCB_K(double, 8, 2, 4)
-    SCB_K(double, 8, 4, 4)
-    SCB_K(double, 8, 4, 8)
-    SCB_K(double, 8, 8, 8)
-    SCB_K(double, 8, 8, 16)
+    SCB_K(double, 8, 1, 4)
+    SCB_K(double, 8, 2, 2)
+    SCB_K(double, 8, 4, 2)
+    SCB_K(double, 8, 8, 1)
+    SCB_K(double, 16, 4, 1)
   }
 #undef SCB_K
   return nullptr;
@@ -785,32 +922,28 @@ void* kernel_for(const Variant& v) {
 }  // namespace
 
 int pick_variant(int dtype, long long pitch, Variant* v) {
-  // nd dot warps + nz z warps (+ 1 producer warp); a z thread owns zv 16-byte
-  // column vectors (zv * elements-per-vector f64 accumulators in registers).
+  // nw consumer warps (+1 producer warp); a thread owns vpt 16-byte vectors of
+  // every row and keeps two groups of rg rows in registers (current + lagged).
   const int epv = dtype == 0 ? 4 : 2;
   const long long nv = pitch / epv;
   v->dtype = dtype;
-  struct C { int nd, nz, zv; };
-  static const C table[] = {{4, 1, 1}, {4, 1, 4}, {8, 2, 4}, {8, 4, 4}, {8, 4, 8}, {8, 8, 8}};
-  bool found = false;
-  for (const C& c : table) {
-    if (static_cast<long long>(c.nz) * 32 * c.zv >= nv) {
-      v->nd = c.nd; v->nz = c.nz; v->zv = c.zv;
-      found = true;
-      break;
-    }
+  v->keep = 1;
+  v->nw = 8;
+  if (nv <= 256) {
+    v->vpt = 1; v->rg = 4;
+  } else if (nv <= 512) {
+    v->vpt = 2; v->rg = 2;
+  } else if (nv <= 1024) {
+    v->vpt = 4; v->rg = dtype == 0 ? 1 : 2;
+  } else if (nv <= 2048) {
+    v->vpt = 8; v->rg = 1;
+  } else {
+    return 1;
   }
-  if (!found) {
-    if (dtype == 1 && nv <= 8 * 32 * 16) {
-      v->nd = 8; v->nz = 8; v->zv = 16;
-    } else {
-      return 1;
-    }
-  }
-  if (const char* e = std::getenv("SCB_VARIANT")) {  // tuning override "nd,nz,zv"
+  if (const char* e = std::getenv("SCB_VARIANT")) {  // tuning override "nw,vpt,rg"
     Variant t = *v;
-    if (std::sscanf(e, "%d,%d,%d", &t.nd, &t.nz, &t.zv) == 3 && kernel_for(t) != nullptr &&
-        static_cast<long long>(t.nz) * 32 * t.zv >= nv)
+    if (std::sscanf(e, "%d,%d,%d", &t.nw, &t.vpt, &t.rg) == 3 && kernel_for(t) != nullptr &&
+        static_cast<long long>(t.nw) * 32 * t.vpt >= nv)
       *v = t;
   }
   return 0;
@@ -827,7 +960,7 @@ cudaError_t launch_sweep(const Variant& v, const KParams& p, size_t smem_bytes, 
   if (!f) return cudaErrorInvalidValue;
   KParams copy = p;
   void* args[] = {&copy};
-  return cudaLaunchCooperativeKernel(f, dim3(p.G), dim3((v.nd + v.nz + 1) * 32), args, smem_bytes, st);
+  return cudaLaunchCooperativeKernel(f, dim3(p.G), dim3((v.nw + 1) * 32), args, smem_bytes, st);
 }
 
 }  // namespace scb

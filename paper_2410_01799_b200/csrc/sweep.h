@@ -53,7 +53,6 @@ struct KParams {
   int G;               // CTAs (one per SM)
   int rows_base, rows_rem;
   int res_rows;        // rows per CTA kept resident in shared memory
-  int ds;              // dot warps sharing one row (column segments)
   int stages;          // TMA ring depth (one row per stage)
   int Q;               // 32-column slices = pitch / 32
   int sw;              // u32 words of per-CTA sign bits
@@ -81,25 +80,27 @@ struct KParams {
   unsigned long long* prof;  // [G][16] clock64 breakdown or nullptr
 };
 
-// Kernel variant: warp roles and per-thread register tiles.
+// Kernel variant: consumer warps and per-thread register tiles.
 struct Variant {
   int dtype;  // 0 f32, 1 f64
-  int nd;     // dot warps
-  int nz;     // column-accumulator (z) warps
-  int zv;     // 16-byte vectors per z thread per row
+  int nw;     // consumer warps (each owns a column segment of every row)
+  int vpt;    // 16-byte vectors per thread per row
+  int rg;     // rows per group (one dot-partial publication per group)
+  int keep;   // 1: lagged group kept in registers; 0: re-read from shared memory
 };
+
+constexpr int kRing = 4;  // dot-partial ring depth (groups)
 
 // Shared-memory carve-up (byte offsets from the dynamic smem base).
 struct Layout {
-  size_t stage, res, ctl, red, yrow, tws, uws, cnt, negf, ready, zseg, sb, total;
+  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, total;
 };
 
 inline __host__ __device__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
-inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_rows, int ds, int rows_max,
-                                              int Q, int zl, int cw, int sw) {
+inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_rows, int rg, int nw, int rows_max,
+                                              int Q, int zl, int sw) {
   Layout L;
-  const size_t slots = static_cast<size_t>(stages + res_rows);
   size_t o = 0;
   L.stage = o;
   o += static_cast<size_t>(stages) * rowB;
@@ -107,22 +108,18 @@ inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_r
   o += static_cast<size_t>(res_rows) * rowB;
   L.ctl = o;
   o += align16(sizeof(Ctl));
-  L.red = o;
-  o += align16(slots * ds * 8);
+  L.ring = o;
+  o += align16(static_cast<size_t>(kRing) * 8);
+  L.rred = o;
+  o += align16(static_cast<size_t>(kRing) * rg * nw * 8);
   L.yrow = o;
   o += align16(static_cast<size_t>(rows_max) * 8);
   L.tws = o;
   o += align16(static_cast<size_t>(Q) * 4);
   L.uws = o;
   o += align16(static_cast<size_t>(Q) * 4);
-  L.cnt = o;
-  o += align16(slots * 4);
-  L.negf = o;
-  o += align16(slots * 4);
-  L.ready = o;
-  o += align16(slots * 8);
   L.zseg = o;
-  o += static_cast<size_t>(zl) * cw * 32 * 8;
+  o += static_cast<size_t>(zl) * nw * 32 * 8;
   L.sb = o;
   o += align16(static_cast<size_t>(3) * sw * 4);
   L.total = o;

@@ -4,7 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2410_01799_b200 as sc
 eng = sc.Engine(0)
-m = n = int(os.environ.get("TUNE_N", 4096))
+n = int(os.environ.get("TUNE_N", 4096))
+m = int(os.environ.get("TUNE_M", n))
 dt = os.environ.get("TUNE_DTYPE", "f32")
 a = sc.fill_normal(1, m * n, np.float32 if dt == "f32" else np.float64).reshape(m, n)
 w = int(os.environ.get("TUNE_W", 16))
