@@ -380,6 +380,7 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   kp.max_sweeps = static_cast<long long>(std::min<uint64_t>(p->max_sweeps, 1ull << 40));
   kp.min_frac = p->min_value_fraction;
   kp.numel_d = static_cast<double>(m * n);
+  kp.widen_mul = 1 << 29;
 
   const bool prof = std::getenv("SCB_PROF") != nullptr;
   unsigned long long* dprof = nullptr;

@@ -38,6 +38,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "sweep.h"
 
@@ -159,6 +160,32 @@ __device__ __forceinline__ uint32_t vec_bits(const uint32_t* words, int v) {
   return (words[col0 >> 5] >> (col0 & 31)) & ((1u << EPV) - 1u);
 }
 __device__ __forceinline__ uint32_t bitmask(uint32_t bits, int e) { return (bits << (31 - e)) & 0x80000000u; }
+// Exact f32 -> f64 widening without F2F (which issues on the quarter-rate XU
+// pipe): the f32 bits shifted right by 3 (arithmetic, so the sign lands in bit
+// 31 after masking bits 28-30) form a double whose exponent field is the f32
+// exponent; scaling by 2^(1023-127) in the accumulating DFMA restores the
+// value exactly (f32 subnormals become f64 subnormals, which the FP64 pipe
+// handles at full precision; zero stays zero).  The t sign flip folds into the
+// same LOP3.  Per element: IMAD.HI + LOP3 + SHF/IMAD + DFMA, no XU.
+constexpr double kRebias = 0x1p896;
+template <typename E>
+struct Wide;
+template <>
+struct Wide<float> {
+  __device__ static double prep(float x, uint32_t m, int wmul) {
+    const long long w = static_cast<long long>(static_cast<int>(__float_as_uint(x))) * static_cast<long long>(wmul);
+    const uint32_t hi = (static_cast<uint32_t>(static_cast<unsigned long long>(w) >> 32) & 0x8fffffffu) ^ m;
+    return __hiloint2double(static_cast<int>(hi), static_cast<int>(static_cast<uint32_t>(w)));
+  }
+  __device__ static double dot(double acc, double w) { return fma(w, kRebias, acc); }
+  __device__ static double zscale(double sg) { return sg * kRebias; }
+};
+template <>
+struct Wide<double> {
+  __device__ static double prep(double x, uint32_t m, int) { return flipd(x, m); }
+  __device__ static double dot(double acc, double w) { return acc + w; }
+  __device__ static double zscale(double sg) { return sg; }
+};
 
 
 // Sum RG per-lane partials over the warp with a transposed butterfly: the first
@@ -209,6 +236,10 @@ struct DotArgs {
   unsigned rowB;
   int rows_g, nres, D, NV, sslot, sph, P;
   unsigned gcount;
+  int wmul;  // 1 << 29 (run-time value)
+#ifdef SCB_TIMING
+  unsigned long long* tprof;  // [blocks][warps][8] section cycle sums (dotbench only)
+#endif
 };
 
 template <typename E, int NW, int VPT, int RG>
@@ -242,144 +273,285 @@ __device__ __noinline__ void dot_pass(const DotArgs a) {
     all_ok = all_ok && vok[k];
   }
   all_ok = __all_sync(0xffffffffu, all_ok);
+  const unsigned toff = static_cast<unsigned>((warp * 32 + lane) * sizeof(VT));
   double zacc[NE];
 #pragma unroll
   for (int i = 0; i < NE; ++i) zacc[i] = 0.0;
-  constexpr unsigned long long* prof = nullptr;
-  long long pacc[8];
-      // ======================= dot pass (the hot loop) =======================
-      // per-thread t sign bits of the owned elements (bit i = element i)
-      uint32_t tbits = 0;
+  // per-thread t sign bits of the owned elements (bit i = element i) and the
+  // matching sign-flip masks, loop-invariant for the whole pass
+  uint32_t tbits = 0;
 #pragma unroll
-      for (int k = 0; k < VPT; ++k) {
-        const int col0 = ((k * NW + warp) * 32 + lane) * EPV;
-        if (vok[k]) tbits |= ((tws[col0 >> 5] >> (col0 & 31)) & ((1u << EPV) - 1u)) << (k * EPV);
-      }
-      const int ngroups = (rows_g + RG - 1) / RG;
-      // A(grp): wait for the group's rows, load this thread's segment, dot
-      // partials, transposed warp reduction, publish to the ring, free stages
-      auto step_a = [&](E (&x)[RG][NE], int grp) {
-        int sl[RG];
-        const VT* rp[RG];
+  for (int k = 0; k < VPT; ++k) {
+    const int col0 = ((k * NW + warp) * 32 + lane) * EPV;
+    if (vok[k]) tbits |= ((tws[col0 >> 5] >> (col0 & 31)) & ((1u << EPV) - 1u)) << (k * EPV);
+  }
+  uint32_t fm[NE];
 #pragma unroll
-        for (int r = 0; r < RG; ++r) {
-          const int jr = grp * RG + r;
-          const int j = jr < rows_g ? jr : rows_g - 1;  // past-the-end rows alias the last row
-          sl[r] = -1;
-          if (j < nres) {
-            rp[r] = reinterpret_cast<const VT*>(res_base + static_cast<size_t>(j) * rowB);
-          } else if (jr < rows_g) {
-            if (prof && tid == 0) {
-              const long long tw0 = clock64();
-              mbar_wait(&full[sslot], static_cast<uint32_t>(sph));
-              pacc[0] += clock64() - tw0;
-            } else {
-              mbar_wait(&full[sslot], static_cast<uint32_t>(sph));
-            }
-            rp[r] = reinterpret_cast<const VT*>(stage_base + static_cast<size_t>(sslot) * rowB);
-            sl[r] = sslot;
-            if (++sslot == D) {
-              sslot = 0;
-              sph ^= 1;
-            }
-          } else {
-            rp[r] = rp[r > 0 ? r - 1 : 0];
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < RG; ++r)
-#pragma unroll
-          for (int k = 0; k < VPT; ++k) Vec<E>::split(rp[r][vidx[k]], &x[r][k * EPV]);
-        if (!all_ok || grp * RG + RG > rows_g) {  // rare: ragged row tail / past-the-end rows
-#pragma unroll
-          for (int r = 0; r < RG; ++r) {
-            const bool rok = grp * RG + r < rows_g;
-#pragma unroll
-            for (int k = 0; k < VPT; ++k)
-              if (!(vok[k] && rok)) {
-#pragma unroll
-                for (int e = 0; e < EPV; ++e) x[r][k * EPV + e] = E(0);
-              }
-          }
-        }
-        double part[RG];
-        uint32_t tb = tbits;
-        asm volatile("" : "+r"(tb));  // keep the per-element masks out of the loop preheader
-#pragma unroll
-        for (int r = 0; r < RG; ++r) {
-          double ac[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-          for (int i = 0; i < NE; ++i) ac[i & 3] += flipd(static_cast<double>(x[r][i]), bitmask(tb, i));
-          part[r] = (ac[0] + ac[1]) + (ac[2] + ac[3]);
-        }
-        const double v = warp_reduce_rows<RG>(part, lane);
-        const unsigned gi = gcount + static_cast<unsigned>(grp);
-        double* pr = rred + static_cast<size_t>(gi & (kRing - 1)) * RG * NW;
-#pragma unroll
-        for (int r = 0; r < RG; ++r)
-          if (lane == holder_lane<RG>(r)) pr[r * NW + warp] = v;
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&ring[gi & (kRing - 1)]);
-#pragma unroll
-          for (int r = 0; r < RG; ++r)
-            if (sl[r] >= 0) mbar_arrive(&empty[sl[r]]);
-        }
-      };
-      // B(grp): combined y of the group (fixed warp order), s' bits, z update
-      auto step_b = [&](const E (&x)[RG][NE], int grp) {
-        const unsigned gi = gcount + static_cast<unsigned>(grp);
-        if (prof && tid == 0) {
-          const long long tw0 = clock64();
-          mbar_wait(&ring[gi & (kRing - 1)], (gi / kRing) & 1u);
-          pacc[6] += clock64() - tw0;
-        } else {
-          mbar_wait(&ring[gi & (kRing - 1)], (gi / kRing) & 1u);
-        }
-        const double* pr = rred + static_cast<size_t>(gi & (kRing - 1)) * RG * NW;
-        double y = 0.0;
-        if (lane < RG) {
-#pragma unroll
-          for (int w = 0; w < NW; ++w) y += pr[lane * NW + w];
-        }
-        const unsigned negb = __ballot_sync(0xffffffffu, lane < RG && y < 0.0);
-        if (warp == 0 && lane < RG) {
-          const int j = grp * RG + lane;
-          if (j < rows_g) {
-            yrow[j] = y;
-            if (!isfinite(y)) atomicMin(a.errp + ERR_Y, static_cast<unsigned>(P));
-            if (y < 0.0) atomicOr(&s_nxt[j >> 5], 1u << (j & 31));
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < RG; ++r) {
-          if ((negb >> r) & 1u) {
-#pragma unroll
-            for (int i = 0; i < NE; ++i) zacc[i] -= static_cast<double>(x[r][i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < NE; ++i) zacc[i] += static_cast<double>(x[r][i]);
-          }
-        }
-      };
-      E xa[RG][NE], xb[RG][NE];
-      // software pipeline: A(g) runs ahead of B(g-1) by one group
-      step_a(xa, 0);
-      int gI = 1;
-      for (; gI + 1 < ngroups; gI += 2) {
-        step_a(xb, gI);
-        step_b(xa, gI - 1);
-        step_a(xa, gI + 1);
-        step_b(xb, gI);
-      }
-      if (gI < ngroups) {
-        step_a(xb, gI);
-        step_b(xa, gI - 1);
-        step_b(xb, gI);
-      } else {
-        step_b(xa, gI - 1);
-      }
+  for (int i = 0; i < NE; ++i) fm[i] = bitmask(tbits, i);
+  const int ngroups = (rows_g + RG - 1) / RG;
+#ifdef SCB_TIMING
+  long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+  // Lag buffers: RG == 1 keeps the widened, t-flipped pairs (z is then one
+  // DFMA per element); RG >= 2 keeps the raw elements (register budget) and
+  // re-widens them in the z update (IMAD.WIDE + LOP3, no XU).
+  constexpr bool KW = RG == 1;
+  using LB = typename std::conditional<KW, double, E>::type;
+  const int wmul = a.wmul;
 
+  // rows_of(grp): row pointers of the group; streamed rows wait for their stage
+  auto rows_of = [&](int grp, const VT* (&rp)[RG], int (&sl)[RG]) {
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+      const int jr = grp * RG + r;
+      const int j = jr < rows_g ? jr : rows_g - 1;  // past-the-end rows alias the last row
+      sl[r] = -1;
+      if (j < nres) {
+        rp[r] = reinterpret_cast<const VT*>(res_base + static_cast<size_t>(j) * rowB);
+      } else if (jr < rows_g) {
+        mbar_wait(&full[sslot], static_cast<uint32_t>(sph));
+        rp[r] = reinterpret_cast<const VT*>(stage_base + static_cast<size_t>(sslot) * rowB);
+        sl[r] = sslot;
+        if (++sslot == D) {
+          sslot = 0;
+          sph ^= 1;
+        }
+      } else {
+        rp[r] = rp[r > 0 ? r - 1 : 0];
+      }
+    }
+  };
+  // ldrows: this thread's segment of the group's rows into registers
+  auto ldrows = [&](E (&x)[RG][NE], const VT* const (&rp)[RG], int grp) {
+    if (all_ok) {  // warp-uniform: full rows, compile-time vector strides
+#pragma unroll
+      for (int r = 0; r < RG; ++r)
+#pragma unroll
+        for (int k = 0; k < VPT; ++k)
+          Vec<E>::split(*reinterpret_cast<const VT*>(reinterpret_cast<const unsigned char*>(rp[r]) + toff +
+                                                      k * (NW * 32 * sizeof(VT))),
+                        &x[r][k * EPV]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < RG; ++r)
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) Vec<E>::split(rp[r][vidx[k]], &x[r][k * EPV]);
+    }
+    if (!all_ok || grp * RG + RG > rows_g) {  // rare: ragged row tail / past-the-end rows
+#pragma unroll
+      for (int r = 0; r < RG; ++r) {
+        const bool rok = grp * RG + r < rows_g;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k)
+          if (!(vok[k] && rok)) {
+#pragma unroll
+            for (int e = 0; e < EPV; ++e) x[r][k * EPV + e] = E(0);
+          }
+      }
+    }
+  };
+  // stages whose rows are in registers go back to the producer (after a
+  // barrier or __syncwarp has ordered every lane's reads)
+  auto release = [&](const int (&sl)[RG]) {
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < RG; ++r)
+        if (sl[r] >= 0) mbar_arrive(&empty[sl[r]]);
+    }
+  };
+  // widen + per-row partials of <R_j, t> over this thread's columns
+  auto widen_dot = [&](const E (&x)[RG][NE], LB (&keep)[RG][NE], double (&part)[RG]) {
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+      double ac[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < NE; ++i) {
+        const double w = Wide<E>::prep(x[r][i], fm[i], wmul);
+        if constexpr (KW) keep[r][i] = w;
+        ac[i & 3] = Wide<E>::dot(ac[i & 3], w);
+      }
+      part[r] = (ac[0] + ac[1]) + (ac[2] + ac[3]);
+    }
+  };
+  // z' += s'_j (t o R_j) for the group's rows (exact: the product with +-1 is
+  // exact); z = t o z' is applied when the pass ends
+  auto zupd = [&](const LB (&pw)[RG][NE], unsigned negb) {
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+      const double sg = Wide<E>::zscale(((negb >> r) & 1u) ? -1.0 : 1.0);
+#pragma unroll
+      for (int i = 0; i < NE; ++i) {
+        if constexpr (KW)
+          zacc[i] = fma(pw[r][i], sg, zacc[i]);
+        else
+          zacc[i] = fma(Wide<E>::prep(pw[r][i], fm[i], wmul), sg, zacc[i]);
+      }
+    }
+  };
+  auto slot = [&](int grp) {
+    return rred + static_cast<size_t>((gcount + static_cast<unsigned>(grp)) & (kRing - 1)) * RG * NW;
+  };
+  // y of the group's rows (lane r < RG holds row r) in fixed warp order, two
+  // interleaved chains, branch-free (every lane reads; only lanes < RG matter)
+  auto combine = [&](int grp) -> double {
+    static_assert(NW % 2 == 0, "two combine chains");
+    const double* pr = slot(grp) + (lane < RG ? lane : 0) * NW;
+    double y0 = pr[0], y1 = pr[1];
+#pragma unroll
+    for (int w = 2; w < NW; w += 2) {
+      y0 += pr[w];
+      y1 += pr[w + 1];
+    }
+    return y0 + y1;
+  };
+  // warp 0 records y; every warp tracks the s' word, warp 0 stores it
+  uint32_t sword = 0;
+  auto record = [&](int grp, double y, unsigned negb) {
+    const int j0 = grp * RG, jend = j0 + RG;
+    sword |= negb << (j0 & 31);
+    if (warp == 0) {
+      if (lane < RG && j0 + lane < rows_g) {
+        yrow[j0 + lane] = y;
+        if (!isfinite(y)) atomicMin(a.errp + ERR_Y, static_cast<unsigned>(P));
+      }
+      if (lane == 0 && ((jend & 31) == 0 || jend >= rows_g)) s_nxt[j0 >> 5] = sword;
+    }
+    if ((jend & 31) == 0) sword = 0;
+  };
+  // One iteration per group g, one CTA barrier: [stage wait for g+1] then a
+  // single barrier-free block (y and z update of g-1, widen + dot + reduction
+  // of g, the loads of g+1) the scheduler interleaves, then the partials of g
+  // are published and the barrier makes them visible.
+  //   dx: raw rows of g;  kc: widened keep buffer of g (KW);  kl: lag buffer of g-1
+  auto iter = [&](auto wz, auto hn, int grp, const E (&dx)[RG][NE], LB (&kc)[RG][NE], LB (&kl)[RG][NE],
+                  E (&ld)[RG][NE]) {
+    constexpr bool WZ = decltype(wz)::value, HN = decltype(hn)::value;
+#ifdef SCB_TIMING
+    long long tt0 = clock64();
+#define SCB_T(k) do { const long long t1_ = clock64(); tacc[k] += t1_ - tt0; tt0 = t1_; } while (0)
+#else
+#define SCB_T(k) do {} while (0)
+#endif
+    const VT* rpn[RG];
+    int sln[RG];
+    if constexpr (HN) rows_of(grp + 1, rpn, sln);
+    SCB_T(0);
+    // (a) the previous group's partials are loaded first (latency hidden by
+    // the dot arithmetic), (b) widen + dot of g, (c) y of g-1 and its signs,
+    // (d) next group's loads, (e) the reduction of g with the z update of g-1
+    // in chunks between its shuffle levels (shuffles and votes are scheduling
+    // barriers for ptxas, so the interleave is written out in source order)
+    double q[NW];
+    if constexpr (WZ) {
+      const double* pq = slot(grp - 1) + (lane < RG ? lane : 0) * NW;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) q[w] = pq[w];
+    }
+    double part[RG];
+    widen_dot(dx, kc, part);
+    SCB_T(1);
+    double y = 0.0;
+    unsigned negb = 0;
+    if constexpr (WZ) {
+      static_assert(NW % 2 == 0, "two combine chains");
+      double y0 = q[0], y1 = q[1];
+#pragma unroll
+      for (int w = 2; w < NW; w += 2) {
+        y0 += q[w];
+        y1 += q[w + 1];
+      }
+      y = y0 + y1;
+      negb = __ballot_sync(0xffffffffu, lane < RG && y < 0.0);
+    }
+    SCB_T(2);
+    if constexpr (HN && KW) ldrows(ld, rpn, grp + 1);
+    double v;
+    if constexpr (RG == 1 && WZ) {
+      const double sg = Wide<E>::zscale((negb & 1u) ? -1.0 : 1.0);
+      v = part[0];
+      constexpr int CH = (NE + 4) / 5;  // z elements per shuffle level
+#pragma unroll
+      for (int l = 0; l < 5; ++l) {
+        const double o = __shfl_xor_sync(0xffffffffu, v, 16 >> l);
+#pragma unroll
+        for (int i = l * CH; i < (l + 1) * CH && i < NE; ++i) {
+          if constexpr (KW)
+            zacc[i] = fma(kl[0][i], sg, zacc[i]);
+          else
+            zacc[i] = fma(Wide<E>::prep(kl[0][i], fm[i], wmul), sg, zacc[i]);
+        }
+        v += o;
+      }
+      SCB_T(3);
+    } else {
+      v = warp_reduce_rows<RG>(part, lane);
+      SCB_T(3);
+      if constexpr (WZ) zupd(kl, negb);
+    }
+    if constexpr (HN && !KW) ldrows(ld, rpn, grp + 1);
+    SCB_T(4);
+    double* pr = slot(grp);
+#pragma unroll
+    for (int r = 0; r < RG; ++r)
+      if (lane == holder_lane<RG>(r)) pr[r * NW + warp] = v;
+    SCB_T(5);
+    consumer_sync(NW * 32);
+    SCB_T(6);
+    if constexpr (WZ) record(grp - 1, y, negb);
+    if constexpr (HN) release(sln);
+    SCB_T(7);
+#undef SCB_T
+  };
+  using F = std::integral_constant<bool, false>;
+  using T = std::integral_constant<bool, true>;
+  // group k lives in buffer A (k even) or B (k odd)
+  E xr[KW ? RG : 1][KW ? NE : 1];  // raw staging (KW only)
+  LB A[RG][NE], B[RG][NE];
+  auto& dxA = [&]() -> auto& { if constexpr (KW) return xr; else return A; }();
+  auto& dxB = [&]() -> auto& { if constexpr (KW) return xr; else return B; }();
+  auto& ldA = dxA;  // where group k+1 is loaded while group k (in A) runs: KW -> xr, raw -> B's partner
+  {
+    const VT* rp0[RG];
+    int sl0[RG];
+    rows_of(0, rp0, sl0);
+    ldrows(dxA, rp0, 0);
+    __syncwarp();
+    release(sl0);
+  }
+  (void)ldA;
+  if (ngroups == 1) {
+    iter(F{}, F{}, 0, dxA, A, B, dxB);
+  } else {
+    iter(F{}, T{}, 0, dxA, A, B, dxB);
+    int g = 1;
+    for (; g + 2 < ngroups; g += 2) {
+      iter(T{}, T{}, g, dxB, B, A, dxA);
+      iter(T{}, T{}, g + 1, dxA, A, B, dxB);
+    }
+    if (g + 1 < ngroups) {
+      iter(T{}, T{}, g, dxB, B, A, dxA);
+      iter(T{}, F{}, g + 1, dxA, A, B, dxB);
+    } else {
+      iter(T{}, F{}, g, dxB, B, A, dxA);
+    }
+  }
+  {
+    const int last = ngroups - 1;
+    const double y = combine(last);
+    const unsigned negb = __ballot_sync(0xffffffffu, lane < RG && y < 0.0);
+    if (last & 1)
+      zupd(B, negb);
+    else
+      zupd(A, negb);
+    record(last, y, negb);
+  }
+
+#ifdef SCB_TIMING
+  if (lane == 0)
+    for (int k = 0; k < 8; ++k) a.tprof[(blockIdx.x * 32 + warp) * 8 + k] += tacc[k];
+#endif
+#pragma unroll
+  for (int i = 0; i < NE; ++i) zacc[i] = flipd(zacc[i], fm[i]);
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     if (vok[k]) {
@@ -388,7 +560,6 @@ __device__ __noinline__ void dot_pass(const DotArgs a) {
         __stcg(reinterpret_cast<double2*>(a.zrow + vidx[k] * EPV + e), make_double2(zacc[k * EPV + e], zacc[k * EPV + e + 1]));
     }
   }
-  (void)pacc;
 }
 
 // ---------------------------------------------------------------------------
@@ -602,6 +773,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
       da.sph = sph;
       da.P = P;
       da.gcount = gcount;
+      da.wmul = p.widen_mul;
       dot_pass<E, NW, VPT, RG>(da);
       const int ngroups = (rows_g + RG - 1) / RG;
       gcount += static_cast<unsigned>(ngroups);
@@ -908,12 +1080,14 @@ void* kernel_for(const Variant& v) {
     SCB_K(float, 16, 2, 2)
     SCB_K(float, 16, 2, 1)
     SCB_K(float, 8, 8, 1)
+    SCB_K(float, 16, 8, 1)
   } else {
     SCB_K(double, 8, 1, 4)
     SCB_K(double, 8, 2, 2)
     SCB_K(double, 8, 4, 2)
     SCB_K(double, 8, 8, 1)
     SCB_K(double, 16, 4, 1)
+    SCB_K(double, 16, 8, 1)
   }
 #undef SCB_K
   return nullptr;
@@ -937,6 +1111,8 @@ int pick_variant(int dtype, long long pitch, Variant* v) {
     v->vpt = 4; v->rg = dtype == 0 ? 1 : 2;
   } else if (nv <= 2048) {
     v->vpt = 8; v->rg = 1;
+  } else if (nv <= 4096) {  // wide rows: 16 consumer warps, register-capped (spills; correct, not tuned)
+    v->nw = 16; v->vpt = 8; v->rg = 1;
   } else {
     return 1;
   }

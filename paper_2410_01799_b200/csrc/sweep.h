@@ -77,6 +77,7 @@ struct KParams {
   long long width, restarts, max_sweeps;
   double min_frac;
   double numel_d;
+  int widen_mul;       // 1 << 29, passed at run time so ptxas emits IMAD.WIDE (not 3 shifts)
   unsigned long long* prof;  // [G][16] clock64 breakdown or nullptr
 };
 

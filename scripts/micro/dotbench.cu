@@ -4,7 +4,7 @@
 #include <vector>
 namespace scb {
 template <int NW, int VPT, int RG>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) dotbench(int rows, int n, int passes, long long* cyc, double* zout) {
+__global__ void __launch_bounds__((NW + 1) * 32, 1) dotbench(int rows, int n, int passes, long long* cyc, double* zout, int wmul, unsigned long long* tprof) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int pitch = (n + 31) / 32 * 32;
   const size_t rowB = pitch * 4;
@@ -31,7 +31,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) dotbench(int rows, int n, in
   unsigned gcount = 0;
   const long long t0 = clock64();
   for (int P = 0; P < passes; ++P) {
-    a.P = P; a.gcount = gcount;
+    a.P = P; a.gcount = gcount; a.wmul = wmul;
+#ifdef SCB_TIMING
+    a.tprof = tprof;
+#endif
     dot_pass<float, NW, VPT, RG>(a);
     gcount += (rows + RG - 1) / RG;
     asm volatile("bar.sync 1, %0;" :: "r"(NW * 32));
@@ -49,14 +52,23 @@ void run(int rows, int n, const char* name) {
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   long long* cyc; double* z; cudaMalloc(&cyc, 8 * 148); cudaMalloc(&z, 8 * 148 * (size_t)pitch);
   int passes = 200;
-  f<<<148, (NW + 1) * 32, L.total>>>(rows, n, passes, cyc, z);
+  unsigned long long* tp; cudaMalloc(&tp, 148 * 32 * 8 * 8); cudaMemset(tp, 0, 148 * 32 * 8 * 8);
+  f<<<148, (NW + 1) * 32, L.total>>>(rows, n, passes, cyc, z, 1 << 29, tp);
   cudaError_t e = cudaDeviceSynchronize();
   std::vector<long long> h(148); cudaMemcpy(h.data(), cyc, 8 * 148, cudaMemcpyDeviceToHost);
   double avg = 0; for (auto v : h) avg += v; avg /= 148.0 * passes;
+#ifdef SCB_TIMING
+  { std::vector<unsigned long long> t(148 * 32 * 8); cudaMemcpy(t.data(), tp, t.size() * 8, cudaMemcpyDeviceToHost);
+    const char* nm[8] = {"rows_of", "combine", "widen+dot(+ld)", "reduce", "zupd(+ld)", "sts", "barrier", "rec+rel"};
+    for (int w : {0, 4, 7}) { printf("warp %d:", w); double tot = 0;
+      for (int k = 0; k < 8; ++k) { double c = 0; for (int b = 0; b < 148; ++b) c += t[(b * 32 + w) * 8 + k]; c /= 148.0 * passes * rows; tot += c; printf(" %s=%.0f", nm[k], c); }
+      printf(" | sum=%.0f cycles/row\n", tot); } }
+#endif
   printf("%-12s rows=%3d n=%5d: %8.0f cycles/pass  %6.0f cycles/row  %.2f elem/clk/SM  (%s)\n", name, rows, n, avg, avg / rows,
          rows * (double)n / avg, cudaGetErrorString(e));
 }
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) { run<8, 4, 1>(12, 4096, "8,4,1"); run<8, 4, 2>(12, 4096, "8,4,2"); return 0; }
   run<8, 4, 1>(7, 4096, "8,4,1");
   run<8, 4, 1>(12, 4096, "8,4,1");
   run<8, 1, 4>(7, 1024, "8,1,4");
