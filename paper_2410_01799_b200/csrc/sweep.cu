@@ -61,9 +61,6 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
 #ifndef SCB_WAIT_HINT_NS
 #define SCB_WAIT_HINT_NS 0
 #endif
-__device__ __forceinline__ void mbar_arrive_cnt(unsigned long long* b, uint32_t count) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
-}
 __device__ __forceinline__ bool mbar_try_wait(unsigned long long* b, uint32_t parity) {
   uint32_t ok;
 #if SCB_WAIT_HINT_NS > 0
@@ -242,6 +239,14 @@ struct DotArgs {
 #endif
 };
 
+template <bool C, typename X, typename Y>
+__device__ __forceinline__ typename std::conditional<C, X, Y>::type& pick(X& x, Y& y) {
+  if constexpr (C)
+    return x;
+  else
+    return y;
+}
+
 template <typename E, int NW, int VPT, int RG>
 __device__ __noinline__ void dot_pass(const DotArgs a) {
   constexpr int EPV = Vec<E>::N;
@@ -255,7 +260,6 @@ __device__ __noinline__ void dot_pass(const DotArgs a) {
   const unsigned char* res_base = smem + a.res;
   const unsigned char* stage_base = smem + a.stage;
   double* rred = reinterpret_cast<double*>(smem + a.rred);
-  unsigned long long* ring = reinterpret_cast<unsigned long long*>(smem + a.ring);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + a.full);
   unsigned long long* empty = reinterpret_cast<unsigned long long*>(smem + a.empty);
   double* yrow = reinterpret_cast<double*>(smem + a.yrow);
@@ -507,9 +511,9 @@ __device__ __noinline__ void dot_pass(const DotArgs a) {
   // group k lives in buffer A (k even) or B (k odd)
   E xr[KW ? RG : 1][KW ? NE : 1];  // raw staging (KW only)
   LB A[RG][NE], B[RG][NE];
-  auto& dxA = [&]() -> auto& { if constexpr (KW) return xr; else return A; }();
-  auto& dxB = [&]() -> auto& { if constexpr (KW) return xr; else return B; }();
-  auto& ldA = dxA;  // where group k+1 is loaded while group k (in A) runs: KW -> xr, raw -> B's partner
+  // raw rows of a group in A / B: the staging buffer (KW) or the buffer itself
+  auto& dxA = pick<KW>(xr, A);
+  auto& dxB = pick<KW>(xr, B);
   {
     const VT* rp0[RG];
     int sl0[RG];
@@ -518,7 +522,6 @@ __device__ __noinline__ void dot_pass(const DotArgs a) {
     __syncwarp();
     release(sl0);
   }
-  (void)ldA;
   if (ngroups == 1) {
     iter(F{}, F{}, 0, dxA, A, B, dxB);
   } else {
@@ -596,7 +599,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
   unsigned char* res_base = smem + L.res;
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + L.ctl);
   unsigned long long* ring = reinterpret_cast<unsigned long long*>(smem + L.ring);  // [kRing] mbarriers
-  double* rred = reinterpret_cast<double*>(smem + L.rred);                 // [kRing][RG][NW] dot partials
   double* yrow = reinterpret_cast<double*>(smem + L.yrow);                 // [rows_max]
   uint32_t* tws = reinterpret_cast<uint32_t*>(smem + L.tws);               // [Q] t of this pass
   uint32_t* uws = reinterpret_cast<uint32_t*>(smem + L.uws);               // [Q] t of the update
