@@ -20,7 +20,7 @@ if [ $rc -eq 0 ]; then
     > $OUT/ncu_launch_$TAG.log 2>&1
   echo "ncu launches rc=$?"
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:sweep_kernel -c 1 \
-    -o $OUT/sweep_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline --width 16 \
+    -o $OUT/sweep_$TAG python bench.py --steps 1 --warmup 0 --no-cpu-baseline \
     > $OUT/ncu_full_$TAG.log 2>&1
   echo "ncu full rc=$?"
 fi

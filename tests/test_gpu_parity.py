@@ -7,6 +7,8 @@ Tolerances (BASELINE.json north_star): packed sign words bit-exact except at
 ties; c_j and ||R_w||/||A|| within 1e-10 relative for f64 storage and 1e-4 for
 f32 storage; sweep counts equal, except the reference's cache-refresh artefact
 (oracle sweeps = gpu + 1 when gpu is a multiple of 16)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -14,6 +16,7 @@ import paper_2410_01799_b200 as sc
 from golden_cases import cut_names, dec_input, dec_names, load
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 F64_TOL = 1e-10
 F32_TOL = 1e-4
@@ -232,3 +235,18 @@ def test_full_size_properties_4096_f32(engine, ref):
     od = ref.greedy_decompose(a.astype(np.float64), 2, seed=1)
     assert all((dec.factors[i][:2] == od.signs[i]).all() for i in range(2))
     assert sweeps_ok(rep.sweeps[:2], od.iterations)
+
+
+# ------------------------------------------------------------ C++ drop-in shim
+@pytest.mark.gpu
+def test_cpp_shim_matches_reference():
+    """include/sigcut_b200.hpp against the reference's own greedy_decompose /
+    greedy_signed_cut (headers compiled unchanged into tests/shim/_bin/shim_check):
+    identical SignMatrix factors, coefficients and curve, same exception types."""
+    import subprocess
+
+    exe = os.path.join(ROOT, "tests", "shim", "_bin", "shim_check")
+    if not os.path.exists(exe):
+        pytest.skip("shim_check not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "SHIM OK" in r.stdout, r.stdout + r.stderr

@@ -152,3 +152,21 @@ def test_host_path_rejects_bad_input_before_device():
     # validation errors surface as the reference's invalid_argument even without a device
     with pytest.raises((sc.InvalidArgument, sc.DeviceError)):
         sc.greedy_decompose(np.zeros((4, 0)), sc.DecomposeConfig(width=1))
+
+
+def test_cpp_shim_compiles_against_reference_headers(tmp_path):
+    """include/sigcut_b200.hpp type-checks against the reference's unchanged
+    headers (the drop-in a maintainer would include); skipped where the
+    reference tree is absent (the GPU box)."""
+    import subprocess
+
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc):
+        pytest.skip("reference headers absent")
+    src = tmp_path / "t.cpp"
+    src.write_text('#include <sigcut/sigcut.hpp>\n#include "sigcut_b200.hpp"\n'
+                   "int main() { sigcut::DenseTensor a({2, 2}, {1, 2, 3, 4}); sigcut::DecomposeConfig c; c.width = 1;\n"
+                   "  auto r = sigcut::b200::greedy_decompose(a, c); return (int)r.first.width(); }\n")
+    r = subprocess.run(["g++", "-std=gnu++20", "-fsyntax-only", f"-I{ref_inc}", f"-I{ROOT}/include", str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
