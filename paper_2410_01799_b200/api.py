@@ -260,9 +260,9 @@ class Engine:
         return dec, rep
 
     def greedy_signed_cut(self, a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None) -> CutResult:
+        """One cut searched with cfg.seed itself: order 2 is greedy_signed_cut
+        (search.hpp:259-263), any other order axial_greedy_cut (:269-272)."""
         cfg = cfg or SearchConfig()
-        if np.ndim(a) != 2 and not (hasattr(a, "dim") and a.dim() == 2):
-            raise InvalidArgument("greedy_signed_cut: matrix required")
         dc = DecomposeConfig(width=1, search=cfg)
         dec, rep, _ = self.run(a, dc, dtype=dtype, seed_mode=N.SC_SEED_DIRECT)
         return CutResult(float(rep._cut_values[0]), [f[0] for f in dec.factors], int(rep.sweeps[0]))
@@ -294,7 +294,8 @@ def greedy_signed_cut(a, cfg: Optional[SearchConfig] = None, dtype: Optional[str
 
 
 def axial_greedy_cut(a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None) -> CutResult:
-    """Order 2 routes to greedy_signed_cut exactly as the reference does (search.hpp:269-272)."""
+    """Order-k cut (axial_run, search.hpp:191-213); order 2 routes to the matrix
+    alternation exactly as the reference does (search.hpp:247, :269-272)."""
     return greedy_signed_cut(a, cfg, dtype=dtype)
 
 

@@ -236,13 +236,32 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   if (res == nullptr) return set_err(ctx, SC_INVALID_ARGUMENT, "sc_result: null");
   std::string msg;
   if (validate(p, &msg) != SC_OK) return set_err(ctx, SC_INVALID_ARGUMENT, "%s", msg.c_str());
-  if (p->order != 2)
-    return set_err(ctx, SC_NOT_SUPPORTED, "order-%d tensors are not supported by this build", p->order);
-  if (res->sign_words[0] == nullptr || res->sign_words[1] == nullptr || res->cut_value == nullptr)
-    return set_err(ctx, SC_INVALID_ARGUMENT, "sc_result: sign_words and cut_value are required");
+  for (int i = 0; i < p->order; ++i)
+    if (res->sign_words[i] == nullptr)
+      return set_err(ctx, SC_INVALID_ARGUMENT, "sc_result: sign_words of every axis are required");
+  if (res->cut_value == nullptr) return set_err(ctx, SC_INVALID_ARGUMENT, "sc_result: cut_value is required");
   SC_CUDA(ctx, cudaSetDevice(ctx->device));
 
-  const uint64_t m = p->shape[0], n = p->shape[1];
+  // Order 2: the matrix itself.  Order k (1 or >= 3; axial_run, search.hpp:191-213):
+  // the matrix view M = n_0 x (n_1 ... n_{k-1}) with the Kronecker sign of the
+  // trailing axes as t; the trailing axes are updated on the device from M^T s_0.
+  const bool tensor = p->order != 2;
+  const int kax = p->order - 1;
+  const uint64_t m = p->shape[0];
+  uint64_t n = 1;
+  for (int i = 1; i < p->order; ++i) {
+    if (p->shape[i] > INT32_MAX / 2 || n > (INT32_MAX / 2) / p->shape[i])
+      return set_err(ctx, SC_NOT_SUPPORTED, "tensor trailing size too large for this build");
+    n *= p->shape[i];
+  }
+  uint64_t axw64 = 0;  // u64 words of the trailing axes' signs
+  int ax_off[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int i = 1; i < p->order; ++i) {
+    ax_off[i - 1] = static_cast<int>(2 * axw64);
+    axw64 += words64(p->shape[i]);
+  }
+  if (!tensor) axw64 = 0;
+  const int axw = static_cast<int>(2 * axw64);
   if (m > INT32_MAX / 2 || n > INT32_MAX / 2)
     return set_err(ctx, SC_NOT_SUPPORTED, "matrix dimension too large for this build");
   const int dt = p->dtype;
@@ -261,7 +280,7 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   const int zl = std::max(1, std::min(4, (Q + G - 1) / G));
   const size_t rowB = static_cast<size_t>(pitch) * es;
   auto smem_for = [&](int st_, int res_) {
-    return scb::make_layout(rowB, st_, res_, var.rg, var.nw, rows_max, Q, zl, sw).total;
+    return scb::make_layout(rowB, st_, res_, var.rg, var.nw, rows_max, Q, zl, sw, axw).total;
   };
   const size_t cap = ctx->smem_optin;
   int stages = 0, res_rows = rows_max;
@@ -291,7 +310,10 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
                       ((nstart * wn * 8 + 255) & ~size_t(255)) +
                       ((std::max<uint64_t>(w, 1) * (wm + wn) * 8 + 511) & ~size_t(255)) +
                       ((std::max<uint64_t>(w, 1) * 8 + 255) & ~size_t(255)) * 2 +
-                      (((w + 1) * 8 + 255) & ~size_t(255)) + 8 * 256 + 4096;
+                      (((w + 1) * 8 + 255) & ~size_t(255)) + 8 * 256 + 4096 +
+                      ((nstart * axw64 * 8 + 255) & ~size_t(255)) +
+                      ((std::max<uint64_t>(w, 1) * axw64 * 8 + 255) & ~size_t(255)) +
+                      ((static_cast<size_t>(pitch) * 8 + 255) & ~size_t(255));
   if (need > ctx->arena_bytes) {
     if (ctx->arena) cudaFree(ctx->arena);
     ctx->arena = nullptr;
@@ -313,19 +335,47 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   double* c_out = carve<double>(cur, std::max<uint64_t>(w, 1));
   uint32_t* sweeps_out = carve<uint32_t>(cur, std::max<uint64_t>(w, 1) * 2);
   double* norm2 = carve<double>(cur, w + 1);
+  uint64_t* ax0 = carve<uint64_t>(cur, std::max<uint64_t>(nstart * axw64, 1));
+  uint64_t* AX_out = carve<uint64_t>(cur, std::max<uint64_t>(std::max<uint64_t>(w, 1) * axw64, 1));
+  double* zfull = carve<double>(cur, static_cast<size_t>(pitch));
 
   // ---- host staging (pinned) for the start vectors ----
-  const size_t t0_bytes = nstart * wn * 8;
-  if (t0_bytes > ctx->pinned_bytes) {
+  const size_t t0_bytes = nstart * wn * 8, ax0_bytes = nstart * axw64 * 8;
+  if (t0_bytes + ax0_bytes > ctx->pinned_bytes) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     ctx->pinned = nullptr;
     ctx->pinned_bytes = 0;
-    SC_CUDA(ctx, cudaMallocHost(&ctx->pinned, t0_bytes));
-    ctx->pinned_bytes = t0_bytes;
+    SC_CUDA(ctx, cudaMallocHost(&ctx->pinned, t0_bytes + ax0_bytes));
+    ctx->pinned_bytes = t0_bytes + ax0_bytes;
   }
   uint64_t* ht0 = static_cast<uint64_t*>(ctx->pinned);
-  for (uint64_t term = 0; term < w; ++term)
-    for (uint64_t r = 0; r < p->restarts; ++r) start_vectors(p, term, r, ht0 + (term * p->restarts + r) * wn);
+  uint64_t* hax0 = ht0 + nstart * wn;
+  if (!tensor) {
+    for (uint64_t term = 0; term < w; ++term)
+      for (uint64_t r = 0; r < p->restarts; ++r) start_vectors(p, term, r, ht0 + (term * p->restarts + r) * wn);
+  } else {
+    // all k axes drawn in axis order (search.hpp:197); s_0 is recomputed first,
+    // the trailing axes seed the axial step and form the first t = kron(s_1..s_{k-1})
+    std::vector<uint64_t> buf(words64(m) + axw64);
+    for (uint64_t term = 0; term < w; ++term)
+      for (uint64_t r = 0; r < p->restarts; ++r) {
+        start_vectors(p, term, r, buf.data());
+        const uint64_t* axs = buf.data() + words64(m);
+        uint64_t* rec = hax0 + (term * p->restarts + r) * axw64;
+        std::copy(axs, axs + axw64, rec);
+        uint64_t* tw = ht0 + (term * p->restarts + r) * wn;
+        std::fill(tw, tw + wn, uint64_t{0});
+        for (uint64_t col = 0; col < n; ++col) {
+          uint64_t c = col, xb = 0;
+          for (int i = kax - 1; i >= 0; --i) {
+            const uint64_t ni = p->shape[i + 1], idx = c % ni;
+            c /= ni;
+            xb ^= (axs[ax_off[i] / 2 + idx / 64] >> (idx % 64)) & 1u;
+          }
+          tw[col / 64] |= xb << (col % 64);
+        }
+      }
+  }
 
   cudaStream_t st = ctx->stream;
   uint64_t h2d = 0, d2h = 0;
@@ -336,6 +386,10 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   if (w > 0) {
     SC_CUDA(ctx, cudaMemcpyAsync(t0, ht0, t0_bytes, cudaMemcpyHostToDevice, st));
     h2d += t0_bytes;
+    if (ax0_bytes) {
+      SC_CUDA(ctx, cudaMemcpyAsync(ax0, hax0, ax0_bytes, cudaMemcpyHostToDevice, st));
+      h2d += ax0_bytes;
+    }
   }
   SC_CUDA(ctx, cudaMemsetAsync(ctr, 0, 4, st));
   SC_CUDA(ctx, cudaMemsetAsync(ctr + 1, 0xff, 12, st));
@@ -381,6 +435,16 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   kp.min_frac = p->min_value_fraction;
   kp.numel_d = static_cast<double>(m * n);
   kp.widen_mul = 1 << 29;
+  kp.tensor = tensor ? 1 : 0;
+  kp.kax = tensor ? kax : 0;
+  for (int i = 0; i < 7; ++i) {
+    kp.ax_n[i] = (tensor && i < kax) ? static_cast<int>(p->shape[i + 1]) : 1;
+    kp.ax_off[i] = ax_off[i];
+  }
+  kp.axw = axw;
+  kp.ax0 = reinterpret_cast<const uint32_t*>(ax0);
+  kp.AX_out = reinterpret_cast<uint32_t*>(AX_out);
+  kp.zfull = zfull;
 
   const bool prof = std::getenv("SCB_PROF") != nullptr;
   unsigned long long* dprof = nullptr;
@@ -430,9 +494,18 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   res->passes = h_stats[1];
   if (wd > 0) {
     SC_CUDA(ctx, cudaMemcpyAsync(res->sign_words[0], S_out, wd * wm * 8, cudaMemcpyDeviceToHost, st));
-    SC_CUDA(ctx, cudaMemcpyAsync(res->sign_words[1], T_out, wd * wn * 8, cudaMemcpyDeviceToHost, st));
+    if (!tensor) {
+      SC_CUDA(ctx, cudaMemcpyAsync(res->sign_words[1], T_out, wd * wn * 8, cudaMemcpyDeviceToHost, st));
+      d2h += wd * wn * 8;
+    } else if (axw64) {  // split the per-term axis records into the per-axis outputs
+      for (int i = 0; i < kax; ++i)
+        SC_CUDA(ctx, cudaMemcpy2DAsync(res->sign_words[i + 1], words64(p->shape[i + 1]) * 8,
+                                       AX_out + ax_off[i] / 2, axw64 * 8, words64(p->shape[i + 1]) * 8, wd,
+                                       cudaMemcpyDeviceToHost, st));
+      d2h += wd * axw64 * 8;
+    }
     SC_CUDA(ctx, cudaMemcpyAsync(res->cut_value, c_out, wd * 8, cudaMemcpyDeviceToHost, st));
-    d2h += wd * (wm + wn + 1) * 8;
+    d2h += wd * (wm + 1) * 8;
     if (res->sweeps) {
       SC_CUDA(ctx, cudaMemcpyAsync(res->sweeps, sweeps_out, wd * 4, cudaMemcpyDeviceToHost, st));
       d2h += wd * 4;

@@ -566,6 +566,108 @@ __device__ __noinline__ void dot_pass(const DotArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Order-k tensors (axial_run, search.hpp:191-213) on the matrix view
+// M = n_0 x N', N' = n_1 ... n_{k-1} (row-major, last axis fastest).  Axis 0 of
+// a sweep is the dot pass (y = M kron(s_1..s_{k-1}), s_0 = sgn(y)); its column
+// reduction gives Z = M^T s_0, from which the trailing axes are updated in
+// order (Gauss-Seidel: axis i uses the new s_j, j < i, and the old s_j, j > i):
+//   v_i[q] = sum over Z entries with index_i = q of Z * prod_{j != i} s_j,
+//   s_i = sgn(v_i), and c = <s_{k-1}, v_{k-1}> = sum_q |v_{k-1}[q]|.
+// Every CTA runs this redundantly on the same data in the same order, so all
+// CTAs hold identical signs and c (deterministic fixed-order sums).
+__device__ __forceinline__ uint32_t axbit(const KParams& p, const uint32_t* sax, int j, int idx) {
+  return (sax[p.ax_off[j] + (idx >> 5)] >> (idx & 31)) & 1u;
+}
+// t word q of kron(s_1, ..., s_{k-1}) over the N' columns
+__device__ uint32_t kron_word(const KParams& p, const uint32_t* sax, int q) {
+  uint32_t word = 0;
+  for (int b = 0; b < 32; ++b) {
+    long long col = static_cast<long long>(q) * 32 + b;
+    if (col >= p.n) break;
+    uint32_t xb = 0;
+    for (int j = p.kax - 1; j >= 0; --j) {
+      const int nj = p.ax_n[j];
+      xb ^= axbit(p, sax, j, static_cast<int>(col % nj));
+      col /= nj;
+    }
+    word |= xb << b;
+  }
+  return word;
+}
+
+template <int CW>
+__device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_t* tws, Ctl* ctl, int P) {
+  constexpr int CT = CW * 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kax = p.kax;
+  const double* Z = p.zfull;
+  unsigned* errp = p.err_pass;
+  double csum = 0.0;
+  if (kax == 0 && tid == 0) csum = __ldcg(Z);  // order 1: c = <s_0, a> = Z[0]
+  for (int i = 0; i < kax; ++i) {
+    const int ni = p.ax_n[i];
+    long long inner = 1;
+    for (int j = i + 1; j < kax; ++j) inner *= p.ax_n[j];
+    const long long other = static_cast<long long>(p.n) / ni;
+    uint32_t* wi = sax + p.ax_off[i];
+    const int nwi = (ni + 31) / 32;
+    // Z entry (index_i = q, r-th combination of the other axes, last fastest), signed
+    auto term = [&](int q, long long r) -> double {
+      long long flat = static_cast<long long>(q) * inner, stride = 1;
+      uint32_t xb = 0;
+      for (int j = kax - 1; j >= 0; --j) {
+        const int nj = p.ax_n[j];
+        if (j != i) {
+          const int ij = static_cast<int>(r % nj);
+          r /= nj;
+          flat += ij * stride;
+          xb ^= axbit(p, sax, j, ij);
+        }
+        stride *= nj;
+      }
+      return flipd(__ldcg(Z + flat), xb << 31);
+    };
+    if (other <= 64) {  // one output per thread, r ascending
+      for (int base = 0; base < ni; base += CT) {
+        const int q = base + tid;
+        const bool ok = q < ni;
+        double v = 0.0;
+        if (ok)
+          for (long long r = 0; r < other; ++r) v += term(q, r);
+        if (ok && !isfinite(v)) atomicMin(errp + ERR_Z, static_cast<unsigned>(P));
+        const unsigned word = __ballot_sync(0xffffffffu, ok && v < 0.0);
+        const int wq = (base >> 5) + warp;
+        if (lane == 0 && wq < nwi) wi[wq] = word;
+        if (i == kax - 1 && ok) csum += fabs(v);
+      }
+    } else {  // one output per warp, lanes stride r, fixed butterfly
+      for (int wq = tid; wq < nwi; wq += CT) wi[wq] = 0u;
+      consumer_sync(CT);
+      for (int q = warp; q < ni; q += CW) {
+        double v = 0.0;
+        for (long long r = lane; r < other; r += 32) v += term(q, r);
+        v = warp_sum(v);
+        if (lane == 0) {
+          if (!isfinite(v)) atomicMin(errp + ERR_Z, static_cast<unsigned>(P));
+          if (v < 0.0) atomicOr(&wi[q >> 5], 1u << (q & 31));
+          if (i == kax - 1) csum += fabs(v);
+        }
+      }
+    }
+    consumer_sync(CT);
+  }
+  csum = warp_sum(csum);
+  if (lane == 0) ctl->cred[warp] = csum;
+  for (int q = tid; q < p.Q; q += CT) tws[q] = kron_word(p, sax, q);
+  consumer_sync(CT);
+  if (tid == 0) {
+    double c = 0.0;
+    for (int w = 0; w < CW; ++w) c += ctl->cred[w];
+    ctl->ax_c = c;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Column ownership: consumer thread (warp w, lane l) owns the 16-byte vectors
 // v_k = (k * NW + w) * 32 + l, k < VPT, of every row (coalesced LDS.128), i.e.
 // NE = VPT * EPV elements per row, and the matching NE f64 column accumulators.
@@ -594,7 +696,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
   const int nstream = rows_g - nres;
   const int D = p.stages;
 
-  const Layout L = make_layout(rowB, D, p.res_rows, RG, NW, p.rows_max, p.Q, p.zl, p.sw);
+  const Layout L = make_layout(rowB, D, p.res_rows, RG, NW, p.rows_max, p.Q, p.zl, p.sw, p.axw);
   unsigned char* stage_base = smem + L.stage;
   unsigned char* res_base = smem + L.res;
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + L.ctl);
@@ -604,6 +706,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
   uint32_t* uws = reinterpret_cast<uint32_t*>(smem + L.uws);               // [Q] t of the update
   double* zseg = reinterpret_cast<double*>(smem + L.zseg);                 // [zl][CW][32]
   uint32_t* sb = reinterpret_cast<uint32_t*>(smem + L.sb);                 // [3][sw]
+  uint32_t* sax = reinterpret_cast<uint32_t*>(smem + L.ax);                // [axw] axes 1..k-1 (order-k)
+  uint32_t* sax_best = sax + p.axw;                                        // [axw] best restart's
   E* R = static_cast<E*>(p.R);
 
   if (tid == 0) {
@@ -619,7 +723,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
     ctl->decided = 1;
     ctl->stored = 0;
     ctl->abort = 0;
-    ctl->pp = 0;
+    ctl->pp = p.tensor ? 1 : 0;  // order-k: pp = sweep of the current pass (1-based)
+    ctl->kron_upd = 0;
     ctl->term = 0;
     ctl->restart = 0;
     ctl->tsel = -1;
@@ -710,6 +815,51 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
     vidx[k] = vok[k] ? v : 0;
   }
 
+  // Owner CTAs sum the G column partials of their 32-column words in a fixed
+  // order; matrix mode publishes sgn(z) as tagged t words, order-k mode stores
+  // z itself.  Ends with a grid barrier.
+  auto col_reduce = [&](bool zmode, int P) {
+    unsigned long long* tout = p.tb64 + static_cast<size_t>(ctl->tsel & 1) * p.Q;
+    const unsigned long long tag = static_cast<unsigned long long>(P + 1) << 32;
+    const int gs = (warp * G) / CW, ge = ((warp + 1) * G) / CW;
+    for (int q0 = g; q0 < p.Q; q0 += G * p.zl) {
+      int nls = 0;
+      for (int j = 0; j < p.zl && q0 + j * G < p.Q; ++j) nls = j + 1;
+      for (int j = 0; j < nls; ++j) {
+        const int col = (q0 + j * G) * 32 + lane;
+        const double* zp = p.zpart + col;
+        double a = 0.0;
+        for (int g0 = gs; g0 < ge; g0 += 16) {  // 16 independent L2 loads in flight
+          double v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = (g0 + u < ge) ? __ldcg(zp + static_cast<size_t>(g0 + u) * pitch) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) a += v[u];
+        }
+        zseg[(j * CW + warp) * 32 + lane] = a;
+      }
+      consumer_sync(CT);
+      for (int j = warp; j < nls; j += CW) {
+        const int qq = q0 + j * G;
+        const int col = qq * 32 + lane;
+        double z = 0.0;
+#pragma unroll
+        for (int w = 0; w < CW; ++w) z += zseg[(j * CW + w) * 32 + lane];
+        const bool valid = col < p.n;
+        if (valid && !isfinite(z)) atomicMin(const_cast<unsigned*>(errp) + ERR_Z, static_cast<unsigned>(P));
+        if (zmode) {  // order-k: Z = M^T s_0 for the axial step
+          if (valid) __stcg(p.zfull + col, z);
+        } else {
+          const unsigned word = __ballot_sync(0xffffffffu, valid && z < 0.0);
+          if (lane == 0) st_relaxed64(tout + qq, tag | word);
+        }
+      }
+      consumer_sync(CT);
+    }
+    if (tid == 0) grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
+    consumer_sync(CT);
+  };
+
   for (int P = 0;; ++P) {
     const int kind = ctl->kind;
     if (kind & K_TERM) break;
@@ -726,7 +876,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
         const uint32_t* tw =
             p.t0 + (static_cast<size_t>(ctl->term) * p.restarts + ctl->restart) * p.t0_stride;
         for (int i = tid; i < p.Q; i += CT) tws[i] = __ldg(tw + i);
-      } else {
+        if (p.tensor) {  // drawn start signs of axes 1..k-1 (search.hpp:197)
+          const uint32_t* aw = p.ax0 + (static_cast<size_t>(ctl->term) * p.restarts + ctl->restart) * p.axw;
+          for (int i = tid; i < p.axw; i += CT) sax[i] = __ldg(aw + i);
+        }
+      } else if (!p.tensor) {  // order-k: tws was rebuilt by the previous pass's axial step
         // t words were published before the last grid barrier, tagged with this pass
         const unsigned long long* tw = p.tb64 + static_cast<size_t>(ctl->tsel) * p.Q;
         for (int i = tid; i < p.Q; i += CT) {
@@ -740,7 +894,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
       if (tid == 0)
         for (int i = 0; i < p.sw; ++i) s_nxt[i] = 0u;
     }
-    if (kind & F_UPD) {
+    if ((kind & F_UPD) && !p.tensor) {  // order-k: uws = kron(best axes), built at term accept
       for (int i = tid; i < p.Q; i += CT)
         uws[i] = ctl->utsel == 2 ? __ldcg(p.tbest + i)
                                  : static_cast<uint32_t>(__ldcg(p.tb64 + static_cast<size_t>(ctl->utsel) * p.Q + i));
@@ -851,7 +1005,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
     if (warp == 0) {
       // this CTA's c partial: sum_i s_i y_i in row order (lane-strided, fixed tree)
       double cl = 0.0;
-      if ((kind & F_DOT) && pp >= 1)
+      if ((kind & F_DOT) && pp >= 1 && !p.tensor)
         for (int j = lane; j < rows_g; j += 32)
           cl += flipd(yrow[j], ((s_cur[j >> 5] >> (j & 31)) & 1u) << 31);
       cl = warp_sum(cl);
@@ -893,9 +1047,67 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
       pacc[2] += t - t_pass0;
       t_pass0 = t;
     }
+    if (p.tensor && (kind & F_DOT)) {  // order-k: Z = M^T s_0, then axes 1..k-1 and c
+      col_reduce(true, P);
+      axial_step<CW>(p, sax, tws, ctl, P);
+    }
 
     // ------------------------------ decision ------------------------------
     if (tid == 0) {
+      // restart loop done: accept or reject the best restart's term (decompose.hpp:329-343)
+      auto accept_term = [&]() -> int {
+        const long long term = ctl->term;
+        const double bc = ctl->best_c;
+        const bool accept = (term == 0) || !(bc < p.min_frac * ctl->first_value);
+        if (accept) {
+          if (term == 0) ctl->first_value = bc;
+          // record term (CutDecomposition::append_term, decompose.hpp:341)
+          const uint32_t* sbest = sb + ctl->best * p.sw;
+          uint32_t* srow = p.S_out + static_cast<size_t>(term) * p.s_stride;
+          for (int l = 0; l < rows_g; ++l)
+            if ((sbest[l >> 5] >> (l & 31)) & 1u) {
+              const int i = r0 + l;
+              atomicOr(srow + (i >> 5), 1u << (i & 31));
+            }
+          if (g == 0 && p.tensor) {  // axes 1..k-1 of the accepted term
+            for (int i = 0; i < p.axw; ++i) p.AX_out[static_cast<size_t>(term) * p.axw + i] = sax_best[i];
+          }
+          if (g == 0) {
+            uint32_t* trow = p.T_out + static_cast<size_t>(term) * p.t_stride;
+            const int nw = min(p.t_stride, p.Q);  // words past Q are pad (zero)
+            if (p.tensor) {
+              for (int i = 0; i < nw; ++i) trow[i] = 0u;  // order-k: per-axis words are in AX_out
+            } else if (ctl->best_tsel == 2) {
+              for (int i = 0; i < nw; ++i) trow[i] = __ldcg(p.tbest + i);
+            } else {
+              const unsigned long long* src = p.tb64 + static_cast<size_t>(ctl->best_tsel) * p.Q;
+              for (int i = 0; i < nw; ++i) trow[i] = static_cast<uint32_t>(__ldcg(src + i));
+            }
+            for (int i = nw; i < p.t_stride; ++i) trow[i] = 0u;
+            p.c_out[term] = bc;
+            p.sweeps_out[term] = static_cast<uint32_t>(ctl->best_sweeps);
+            p.stats[0] = static_cast<unsigned long long>(term + 1);
+          }
+          ctl->alpha = bc / p.numel_d;  // alpha = c / numel (decompose.hpp:340)
+          ctl->utsel = ctl->best_tsel;
+          ctl->kron_upd = p.tensor;  // order-k: uws = kron(best axes) after the decision
+          ctl->term = static_cast<int>(term + 1);
+          ctl->norm_idx = static_cast<int>(term + 1);
+          if (term + 1 >= p.width) {
+            return F_UPD | F_NORM | F_WB;
+          } else {
+            ctl->pp = p.tensor ? 1 : 0;
+            ctl->restart = 0;
+            ctl->tsel = -1;
+            ctl->c_prev = -INFINITY;
+            return F_UPD | F_NORM;  // deflate, then search the next term
+          }
+        } else {
+          // min_value_fraction stop (decompose.hpp:337-338): nothing appended
+          ctl->norm_idx = static_cast<int>(term);
+          return F_NORM | F_WB;
+        }
+      };
       double cs = 0.0, ns = 0.0;
       for (int w = 0; w < CW; ++w) {
         cs += ctl->cred[w];
@@ -913,7 +1125,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
           next = K_TERM;  // final write-back done
         } else if (!(kind & F_DOT)) {
           next = F_DOT;   // maintenance pass (initial norm / rank-1 update) -> search
-        } else if (pp == 0) {
+        } else if (!p.tensor && pp == 0) {
           const int t = ctl->cur;  // s_1 (just computed) becomes current
           ctl->cur = ctl->nxt;
           ctl->nxt = t;
@@ -922,17 +1134,41 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
           need_reduce = 1;
           next = F_DOT;
         } else {
-          const double c = cs;
+          // matrix: c = <s_pp, R t_pp> from this pass's y; order-k: c of this sweep's axial step
+          const double c = p.tensor ? ctl->ax_c : cs;
           const bool stop = (c <= ctl->c_prev) || (pp >= p.max_sweeps);
           if (!stop) {
             ctl->c_prev = c;
-            const int t = ctl->cur;
-            ctl->cur = ctl->nxt;
-            ctl->nxt = t;
             ctl->pp = pp + 1;
-            ctl->tsel = (pp + 1) & 1;
-            need_reduce = 1;
+            if (p.tensor) {
+              ctl->tsel = 0;  // next t = kron(new axes), already in tws
+            } else {
+              const int t = ctl->cur;
+              ctl->cur = ctl->nxt;
+              ctl->nxt = t;
+              ctl->tsel = (pp + 1) & 1;
+              need_reduce = 1;
+            }
             next = F_DOT;
+          } else if (p.tensor) {
+            // axial_run returns the current sweep's (c, signs) (search.hpp:206, :210)
+            const bool better = (ctl->restart == 0) || (c > ctl->best_c);
+            if (better) {
+              ctl->best_c = c;
+              ctl->best_sweeps = pp;
+              uint32_t* sbest = sb + ctl->best * p.sw;
+              for (int i = 0; i < p.sw; ++i) sbest[i] = s_nxt[i];
+              for (int i = 0; i < p.axw; ++i) sax_best[i] = sax[i];
+            }
+            ctl->restart += 1;
+            if (ctl->restart < p.restarts) {
+              ctl->pp = 1;
+              ctl->tsel = -1;
+              ctl->c_prev = -INFINITY;
+              next = F_DOT;
+            } else {
+              next = accept_term();
+            }
           } else {
             // restart result (c, s_pp, t_pp, pp): search.hpp:178-180 / :185
             const bool better = (ctl->restart == 0) || (c > ctl->best_c);
@@ -958,51 +1194,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
               ctl->c_prev = -INFINITY;
               next = F_DOT;
             } else {
-              const long long term = ctl->term;
-              const double bc = ctl->best_c;
-              const bool accept = (term == 0) || !(bc < p.min_frac * ctl->first_value);
-              if (accept) {
-                if (term == 0) ctl->first_value = bc;
-                // record term (CutDecomposition::append_term, decompose.hpp:341)
-                const uint32_t* sbest = sb + ctl->best * p.sw;
-                uint32_t* srow = p.S_out + static_cast<size_t>(term) * p.s_stride;
-                for (int l = 0; l < rows_g; ++l)
-                  if ((sbest[l >> 5] >> (l & 31)) & 1u) {
-                    const int i = r0 + l;
-                    atomicOr(srow + (i >> 5), 1u << (i & 31));
-                  }
-                if (g == 0) {
-                  uint32_t* trow = p.T_out + static_cast<size_t>(term) * p.t_stride;
-                  const int nw = min(p.t_stride, p.Q);  // words past Q are pad (zero)
-                  if (ctl->best_tsel == 2) {
-                    for (int i = 0; i < nw; ++i) trow[i] = __ldcg(p.tbest + i);
-                  } else {
-                    const unsigned long long* src = p.tb64 + static_cast<size_t>(ctl->best_tsel) * p.Q;
-                    for (int i = 0; i < nw; ++i) trow[i] = static_cast<uint32_t>(__ldcg(src + i));
-                  }
-                  for (int i = nw; i < p.t_stride; ++i) trow[i] = 0u;
-                  p.c_out[term] = bc;
-                  p.sweeps_out[term] = static_cast<uint32_t>(ctl->best_sweeps);
-                  p.stats[0] = static_cast<unsigned long long>(term + 1);
-                }
-                ctl->alpha = bc / p.numel_d;  // alpha = c / numel (decompose.hpp:340)
-                ctl->utsel = ctl->best_tsel;
-                ctl->term = static_cast<int>(term + 1);
-                ctl->norm_idx = static_cast<int>(term + 1);
-                if (term + 1 >= p.width) {
-                  next = F_UPD | F_NORM | F_WB;
-                } else {
-                  next = F_UPD | F_NORM;  // deflate, then search the next term
-                  ctl->pp = 0;
-                  ctl->restart = 0;
-                  ctl->tsel = -1;
-                  ctl->c_prev = -INFINITY;
-                }
-              } else {
-                // min_value_fraction stop (decompose.hpp:337-338): nothing appended
-                ctl->norm_idx = static_cast<int>(term);
-                next = F_NORM | F_WB;
-              }
+              next = accept_term();
             }
           }
         }
@@ -1020,46 +1212,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
       pacc[3] += t - t_pass0;
       t_pass0 = t;
     }
+    if (p.tensor && ctl->kron_upd) {  // order-k: t of the rank-1 update = kron(best axes)
+      for (int q = tid; q < p.Q; q += CT) uws[q] = kron_word(p, sax_best, q);
+      consumer_sync(CT);
+      if (tid == 0) ctl->kron_upd = 0;
+    }
 
     // --------------------- column reduction: t' = sgn(z) ---------------------
-    if (ctl->need_reduce) {
-      unsigned long long* tout = p.tb64 + static_cast<size_t>(ctl->tsel & 1) * p.Q;
-      const unsigned long long tag = static_cast<unsigned long long>(P + 1) << 32;
-      const int gs = (warp * G) / CW, ge = ((warp + 1) * G) / CW;
-      for (int q0 = g; q0 < p.Q; q0 += G * p.zl) {
-        int nls = 0;
-        for (int j = 0; j < p.zl && q0 + j * G < p.Q; ++j) nls = j + 1;
-        for (int j = 0; j < nls; ++j) {
-          const int col = (q0 + j * G) * 32 + lane;
-          const double* zp = p.zpart + col;
-          double a = 0.0;
-          for (int g0 = gs; g0 < ge; g0 += 16) {  // 16 independent L2 loads in flight
-            double v[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) v[u] = (g0 + u < ge) ? __ldcg(zp + static_cast<size_t>(g0 + u) * pitch) : 0.0;
-#pragma unroll
-            for (int u = 0; u < 16; ++u) a += v[u];
-          }
-          zseg[(j * CW + warp) * 32 + lane] = a;
-        }
-        consumer_sync(CT);
-        for (int j = warp; j < nls; j += CW) {
-          const int qq = q0 + j * G;
-          const int col = qq * 32 + lane;
-          double z = 0.0;
-#pragma unroll
-          for (int w = 0; w < CW; ++w) z += zseg[(j * CW + w) * 32 + lane];
-          const bool valid = col < p.n;
-          if (valid && !isfinite(z)) atomicMin(const_cast<unsigned*>(errp) + ERR_Z, static_cast<unsigned>(P));
-          const unsigned word = __ballot_sync(0xffffffffu, valid && z < 0.0);
-          if (lane == 0) st_relaxed64(tout + qq, tag | word);
-        }
-        consumer_sync(CT);
-      }
-      if (tid == 0) grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
-      consumer_sync(CT);
-      if (prof && tid == 0) pacc[4] += clock64() - t_pass0;
-    }
+    if (!p.tensor && ctl->need_reduce) col_reduce(false, P);
   }
   if (tid == 0) ctl->abort = 1;  // release a producer still waiting on an unconsumed stage
   if (prof && tid == 0)

@@ -40,8 +40,9 @@ struct Ctl {
   volatile int kind_ring[4];
   // controller state (thread 0 writes, consumers read after a named barrier)
   int kind, pp, term, restart, tsel, utsel, best_tsel, best_sweeps;
-  int cur, nxt, best, need_reduce, norm_idx, pad0;
+  int cur, nxt, best, need_reduce, norm_idx, kron_upd;
   double alpha, c_prev, best_c, first_value;
+  double ax_c;  // order-k mode: c = <s_{k-1}, v_{k-1}> of the axial step
   double cred[32];
   double nred[32];
 };
@@ -78,6 +79,17 @@ struct KParams {
   double min_frac;
   double numel_d;
   int widen_mul;       // 1 << 29, passed at run time so ptxas emits IMAD.WIDE (not 3 shifts)
+  // order-k tensors (k == 1 or k >= 3; axial_run, search.hpp:191-213): the kernel
+  // runs on the matrix view M = n_0 x (n_1 ... n_{k-1}); axes 1..k-1 are updated
+  // from Z = M^T s_0 by every CTA after the column reduction.
+  int tensor;          // 1: order-k axial mode
+  int kax;             // trailing axes (k - 1)
+  int ax_n[7];         // n_1 .. n_{k-1}
+  int ax_off[7];       // u32 word offset of axis i+1 within an axis-word record
+  int axw;             // u32 words per axis-word record (even)
+  const uint32_t* ax0; // [width][restarts][axw] start words of axes 1..k-1
+  uint32_t* AX_out;    // [width][axw] accepted axis words
+  double* zfull;       // [pitch] reduced z (order-k mode)
   unsigned long long* prof;  // [G][16] clock64 breakdown or nullptr
 };
 
@@ -94,13 +106,13 @@ constexpr int kRing = 4;  // dot-partial ring depth (groups)
 
 // Shared-memory carve-up (byte offsets from the dynamic smem base).
 struct Layout {
-  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, total;
+  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, total;
 };
 
 inline __host__ __device__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
 inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_rows, int rg, int nw, int rows_max,
-                                              int Q, int zl, int sw) {
+                                              int Q, int zl, int sw, int axw = 0) {
   Layout L;
   size_t o = 0;
   L.stage = o;
@@ -123,6 +135,8 @@ inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_r
   o += static_cast<size_t>(zl) * nw * 32 * 8;
   L.sb = o;
   o += align16(static_cast<size_t>(3) * sw * 4);
+  L.ax = o;  // [2][axw]: current / best axis words (order-k mode)
+  o += align16(static_cast<size_t>(2) * axw * 4);
   L.total = o;
   return L;
 }
