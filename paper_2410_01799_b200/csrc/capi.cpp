@@ -26,6 +26,7 @@ struct sc_ctx {
   int device = 0;
   int num_sms = 0;
   size_t smem_optin = 0;
+  size_t smem_per_sm = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::string err;
@@ -152,6 +153,7 @@ sc_status sc_create(sc_ctx** out, int device) {
   }
   ctx->num_sms = prop.multiProcessorCount;
   ctx->smem_optin = prop.sharedMemPerBlockOptin;
+  ctx->smem_per_sm = prop.sharedMemPerMultiprocessor;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
     delete ctx;
@@ -272,7 +274,7 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
     return set_err(ctx, SC_NOT_SUPPORTED, "row length %llu exceeds the fused-kernel envelope",
                    static_cast<unsigned long long>(n));
 
-  const int G = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(ctx->num_sms), m));
+  const int G = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(ctx->num_sms) * var.cps, m));
   const int rows_base = static_cast<int>(m / G), rows_rem = static_cast<int>(m % G);
   const int rows_max = rows_base + (rows_rem ? 1 : 0);
   const int Q = static_cast<int>(pitch / 32);
@@ -282,7 +284,9 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   auto smem_for = [&](int st_, int res_) {
     return scb::make_layout(rowB, st_, res_, var.rg, var.nw, rows_max, Q, zl, sw, axw).total;
   };
-  const size_t cap = ctx->smem_optin;
+  // per-CTA shared memory: the opt-in maximum, or an even split of the SM's
+  // 228 KB (minus the 1 KB the runtime reserves per CTA) when two CTAs share an SM
+  const size_t cap = var.cps == 1 ? ctx->smem_optin : std::min(ctx->smem_optin, (ctx->smem_per_sm / var.cps) - 1024);
   int stages = 0, res_rows = rows_max;
   if (smem_for(0, rows_max) > cap) {
     stages = static_cast<int>(env_size("SCB_STAGES", static_cast<size_t>(2 * var.rg + 4)));
@@ -295,7 +299,12 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
     res_rows = static_cast<int>(std::min<size_t>(env_size("SCB_RES_ROWS", static_cast<size_t>(res_rows)),
                                                  static_cast<size_t>(res_rows)));
   }
+  // the cooperative launch needs every CTA co-resident: trim resident rows until
+  // the occupancy API confirms var.cps CTAs per SM at this footprint
+  while (var.cps > 1 && res_rows > 0 && scb::blocks_per_sm(var, smem_for(stages, res_rows)) < var.cps) --res_rows;
   const size_t smem = smem_for(stages, res_rows);
+  if (scb::blocks_per_sm(var, smem) < var.cps)
+    return set_err(ctx, SC_NOT_SUPPORTED, "%d CTAs per SM do not fit (%zu bytes of shared memory each)", var.cps, smem);
 
   const uint64_t w = p->width;
   const uint64_t wm = words64(m), wn = words64(n);
@@ -304,7 +313,7 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   const uint64_t nstart = std::max<uint64_t>(w, 1) * p->restarts;
 
   // ---- device arena ----
-  const size_t need = ((m * rowB + 255) & ~size_t(255)) + ((G * rowB * 8 / es + 255) & ~size_t(255)) +
+  const size_t need = ((m * rowB + 255) & ~size_t(255)) + ((2 * G * rowB * 8 / es + 255) & ~size_t(255)) +
                       ((G * sizeof(scb::Slot) + 255) & ~size_t(255)) + 4 * 256 +
                       3 * ((tw32 * 8 + 255) & ~size_t(255)) +
                       ((nstart * wn * 8 + 255) & ~size_t(255)) +
@@ -323,7 +332,7 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   }
   char* cur = static_cast<char*>(ctx->arena);
   void* dR = carve<char>(cur, m * rowB);
-  double* zpart = carve<double>(cur, static_cast<size_t>(G) * pitch);
+  double* zpart = carve<double>(cur, 2 * static_cast<size_t>(G) * pitch);  // [2][G][pitch] by pass parity
   scb::Slot* slots = carve<scb::Slot>(cur, G);
   unsigned* ctr = carve<unsigned>(cur, 8);  // [1..3] err_pass
   unsigned long long* stats = carve<unsigned long long>(cur, 4);
@@ -445,6 +454,7 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   kp.ax0 = reinterpret_cast<const uint32_t*>(ax0);
   kp.AX_out = reinterpret_cast<uint32_t*>(AX_out);
   kp.zfull = zfull;
+  kp.two_phase = static_cast<int>(env_size("SCB_2PH", 1));  // SCB_2PH=0: fused single-read pass
 
   const bool prof = std::getenv("SCB_PROF") != nullptr;
   unsigned long long* dprof = nullptr;
@@ -475,9 +485,14 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
     std::vector<unsigned long long> hp(static_cast<size_t>(G) * 16);
     cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost);
     cudaFree(dprof);
-    double acc[8] = {0};
+    double acc[12] = {0};
     for (int g = 0; g < G; ++g)
-      for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(hp[g * 16 + i]) / G;
+      for (int i = 0; i < 12; ++i) acc[i] += static_cast<double>(hp[g * 16 + i]) / G;
+    std::fprintf(stderr, "[scb prof2] per pass: stagewait=%.0f A=%.0f B=%.0f C=%.0f\n",
+                 acc[8] / std::max<double>(1.0, static_cast<double>(h_stats[1])),
+                 acc[9] / std::max<double>(1.0, static_cast<double>(h_stats[1])),
+                 acc[10] / std::max<double>(1.0, static_cast<double>(h_stats[1])),
+                 acc[11] / std::max<double>(1.0, static_cast<double>(h_stats[1])));
     std::fprintf(stderr,
                  "[scb prof] G=%d res_rows=%d stages=%d nw=%d vpt=%d rg=%d smem=%zu | cycles/CTA: "
                  "fullwait=%.0f chunks=%.0f passend+bar=%.0f decision=%.0f reduce+bar=%.0f | staging=%.0f ringwait=%.0f | prod emptywait=%.0f  (per pass: chunks %.0f) passes=%llu\n",

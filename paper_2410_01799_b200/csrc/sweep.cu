@@ -165,6 +165,15 @@ __device__ __forceinline__ uint32_t bitmask(uint32_t bits, int e) { return (bits
 // handles at full precision; zero stays zero).  The t sign flip folds into the
 // same LOP3.  Per element: IMAD.HI + LOP3 + SHF/IMAD + DFMA, no XU.
 constexpr double kRebias = 0x1p896;
+// Same exact widening with 32-bit shifts (SHF + LOP3 + SHL on the full-rate
+// ALU / FMA pipes instead of the quarter-rate IMAD.WIDE).
+__device__ __forceinline__ double widen_shf(float x, uint32_t m) {
+  const uint32_t u = __float_as_uint(x);
+  const uint32_t hi = (static_cast<uint32_t>(static_cast<int>(u) >> 3) & 0x8fffffffu) ^ m;
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
+}
+__device__ __forceinline__ double widen_shf(double x, uint32_t m) { return flipd(x, m); }
+
 template <typename E>
 struct Wide;
 template <>
@@ -227,13 +236,14 @@ __device__ __forceinline__ int holder_lane(int r) {
 // Shared-memory regions are passed as 32-bit offsets from the dynamic smem base
 // so the callee addresses them with LDS/STS.
 struct DotArgs {
-  unsigned res, stage, full, empty, ring, rred, yrow, s_nxt, tws;
+  unsigned res, stage, full, empty, ring, rred, yrow, s_nxt, tws, ypart;
   double* zrow;
   unsigned* errp;
   unsigned rowB;
   int rows_g, nres, D, NV, sslot, sph, P;
   unsigned gcount;
   int wmul;  // 1 << 29 (run-time value)
+  unsigned long long* prof;  // [4] thread-0 cycle sums (SCB_PROFILE builds): stage waits, A, B, C
 #ifdef SCB_TIMING
   unsigned long long* tprof;  // [blocks][warps][8] section cycle sums (dotbench only)
 #endif
@@ -247,7 +257,7 @@ __device__ __forceinline__ typename std::conditional<C, X, Y>::type& pick(X& x, 
     return y;
 }
 
-template <typename E, int NW, int VPT, int RG>
+template <typename E, int NW, int VPT, int RG, int CPS = 1>
 __device__ __noinline__ void dot_pass(const DotArgs a) {
   constexpr int EPV = Vec<E>::N;
   constexpr int NE = VPT * EPV;
@@ -299,7 +309,7 @@ __device__ __noinline__ void dot_pass(const DotArgs a) {
   // Lag buffers: RG == 1 keeps the widened, t-flipped pairs (z is then one
   // DFMA per element); RG >= 2 keeps the raw elements (register budget) and
   // re-widens them in the z update (IMAD.WIDE + LOP3, no XU).
-  constexpr bool KW = RG == 1;
+  constexpr bool KW = RG == 1 && CPS == 1;
   using LB = typename std::conditional<KW, double, E>::type;
   const int wmul = a.wmul;
 
@@ -566,6 +576,229 @@ __device__ __noinline__ void dot_pass(const DotArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Two-phase dot pass.  (A) every warp forms the partial <R_j, t> of its column
+// segment for each row and reduces it within the warp only (no CTA barrier per
+// row; two rows per step for ILP); (B) after ONE barrier the CTA combines the
+// per-warp partials of all its rows in fixed warp order (y, s' = sgn(y)); then
+// (C) z = R^T s' streams the rows again (SMEM-resident ones from SMEM, the rest
+// re-streamed by the producer) as a pure accumulate.  Rows are read twice, but
+// they live in SMEM / L2; what this removes is the per-row serial chain.
+template <typename E, int NW, int VPT, bool FULL>
+__device__ __forceinline__ void dot_pass_2ph_impl(const DotArgs& a) {
+  constexpr int EPV = Vec<E>::N;
+  constexpr int NE = VPT * EPV;
+  using VT = typename Vec<E>::T;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows_g = a.rows_g, nres = a.nres, D = a.D, NV = a.NV, P = a.P;
+  const size_t rowB = a.rowB;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const unsigned char* res_base = smem + a.res;
+  const unsigned char* stage_base = smem + a.stage;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + a.full);
+  unsigned long long* empty = reinterpret_cast<unsigned long long*>(smem + a.empty);
+  double* yrow = reinterpret_cast<double*>(smem + a.yrow);
+  double* ypart = reinterpret_cast<double*>(smem + a.ypart);
+  uint32_t* s_nxt = reinterpret_cast<uint32_t*>(smem + a.s_nxt);
+  const uint32_t* tws = reinterpret_cast<const uint32_t*>(smem + a.tws);
+  int sslot = a.sslot, sph = a.sph;
+  int vidx[VPT];
+  bool vok[VPT];
+  bool all_ok = true;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int v = (k * NW + warp) * 32 + lane;
+    vok[k] = v < NV;
+    vidx[k] = vok[k] ? v : 0;
+    all_ok = all_ok && vok[k];
+  }
+  (void)all_ok;
+  const unsigned toff = static_cast<unsigned>((warp * 32 + lane) * sizeof(VT));
+  uint32_t tbits = 0;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int col0 = ((k * NW + warp) * 32 + lane) * EPV;
+    if (vok[k]) tbits |= ((tws[col0 >> 5] >> (col0 & 31)) & ((1u << EPV) - 1u)) << (k * EPV);
+  }
+  uint32_t fm[NE];
+#pragma unroll
+  for (int i = 0; i < NE; ++i) fm[i] = bitmask(tbits, i);
+
+  long long twait = 0;
+  auto rowptr = [&](int j, int& sl) -> const VT* {
+    if (j < nres) {
+      sl = -1;
+      return reinterpret_cast<const VT*>(res_base + static_cast<size_t>(j) * rowB);
+    }
+#ifdef SCB_PROFILE
+    const long long tw0 = clock64();
+    mbar_wait(&full[sslot], static_cast<uint32_t>(sph));
+    twait += clock64() - tw0;
+#else
+    mbar_wait(&full[sslot], static_cast<uint32_t>(sph));
+#endif
+    sl = sslot;
+    if (++sslot == D) {
+      sslot = 0;
+      sph ^= 1;
+    }
+    return reinterpret_cast<const VT*>(stage_base + static_cast<size_t>(sl) * rowB);
+  };
+  // FULL: the warp's vectors are all inside the row (warp-uniform; the loops are
+  // instantiated per case because ptxas does not unswitch the loop-invariant test)
+  auto ld = [&](const VT* rp, E (&x)[NE]) {
+    if constexpr (FULL) {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k)
+        Vec<E>::split(*reinterpret_cast<const VT*>(reinterpret_cast<const unsigned char*>(rp) + toff +
+                                                    k * (NW * 32 * sizeof(VT))),
+                      &x[k * EPV]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        Vec<E>::split(rp[vidx[k]], &x[k * EPV]);
+        if (!vok[k]) {
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) x[k * EPV + e] = E(0);
+        }
+      }
+    }
+  };
+  auto release = [&](int sl) {
+    if (sl >= 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sl]);
+    }
+  };
+  auto partial = [&](const E (&x)[NE]) -> double {
+    double ac[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < NE; ++i) ac[i & 3] = fma(widen_shf(x[i], fm[i]), Wide<E>::zscale(1.0), ac[i & 3]);
+    return (ac[0] + ac[1]) + (ac[2] + ac[3]);
+  };
+
+  // ---- (A) per-warp row partials ----
+  const long long tA = clock64();
+  int j = 0;
+  for (; j + 1 < rows_g; j += 2) {
+    int s0, s1;
+    const VT* p0 = rowptr(j, s0);
+    const VT* p1 = rowptr(j + 1, s1);
+    E x0[NE], x1[NE];
+    ld(p0, x0);
+    ld(p1, x1);
+    double v0 = partial(x0), v1 = partial(x1);
+    release(s0);
+    release(s1);
+  #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double o0 = __shfl_xor_sync(0xffffffffu, v0, o), o1 = __shfl_xor_sync(0xffffffffu, v1, o);
+      v0 += o0;
+      v1 += o1;
+    }
+    if (lane == 0) {
+      ypart[j * NW + warp] = v0;
+      ypart[(j + 1) * NW + warp] = v1;
+    }
+  }
+  if (j < rows_g) {
+    int s0;
+    const VT* p0 = rowptr(j, s0);
+    E x0[NE];
+    ld(p0, x0);
+    double v0 = partial(x0);
+    release(s0);
+    v0 = warp_sum(v0);
+    if (lane == 0) ypart[j * NW + warp] = v0;
+  }
+  const long long tB = clock64();
+  consumer_sync(NW * 32);
+  // ---- (B) y and s' of every row, fixed warp order ----
+  for (int jb = 0; jb < rows_g; jb += NW * 32) {
+    const int jj = jb + tid;
+    const bool ok = jj < rows_g;
+    double y = 0.0;
+    if (ok) {
+      const double* pr = ypart + jj * NW;
+      double y0 = pr[0], y1 = pr[1];
+  #pragma unroll
+      for (int w = 2; w < NW; w += 2) {
+        y0 += pr[w];
+        y1 += pr[w + 1];
+      }
+      y = y0 + y1;
+      yrow[jj] = y;
+      if (!isfinite(y)) atomicMin(a.errp + ERR_Y, static_cast<unsigned>(P));
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, ok && y < 0.0);
+    if (lane == 0 && jb + warp * 32 < rows_g) s_nxt[(jb >> 5) + warp] = word;
+  }
+  consumer_sync(NW * 32);
+  const long long tC = clock64();
+  // ---- (C) z = R^T s' ----
+  double zacc[NE];
+  #pragma unroll
+  for (int i = 0; i < NE; ++i) zacc[i] = 0.0;
+  auto sgn_of = [&](int r) { return Wide<E>::zscale(((s_nxt[r >> 5] >> (r & 31)) & 1u) ? -1.0 : 1.0); };
+  j = 0;
+  for (; j + 1 < rows_g; j += 2) {
+    int s0, s1;
+    const VT* p0 = rowptr(j, s0);
+    const VT* p1 = rowptr(j + 1, s1);
+    E x0[NE], x1[NE];
+    ld(p0, x0);
+    ld(p1, x1);
+    const double g0 = sgn_of(j), g1 = sgn_of(j + 1);
+  #pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      zacc[i] = fma(widen_shf(x0[i], 0u), g0, zacc[i]);
+      zacc[i] = fma(widen_shf(x1[i], 0u), g1, zacc[i]);
+    }
+    release(s0);
+    release(s1);
+  }
+  if (j < rows_g) {
+    int s0;
+    const VT* p0 = rowptr(j, s0);
+    E x0[NE];
+    ld(p0, x0);
+    const double g0 = sgn_of(j);
+  #pragma unroll
+    for (int i = 0; i < NE; ++i) zacc[i] = fma(widen_shf(x0[i], 0u), g0, zacc[i]);
+    release(s0);
+  }
+  #ifdef SCB_PROFILE
+  if (a.prof && tid == 0) {
+    a.prof[0] += twait;
+    a.prof[1] += tB - tA;
+    a.prof[2] += tC - tB;
+    a.prof[3] += clock64() - tC;
+  }
+  #else
+  (void)tA; (void)tB; (void)tC; (void)twait;
+  #endif
+  #pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    if (vok[k]) {
+  #pragma unroll
+      for (int e = 0; e < EPV; e += 2)
+        __stcg(reinterpret_cast<double2*>(a.zrow + vidx[k] * EPV + e), make_double2(zacc[k * EPV + e], zacc[k * EPV + e + 1]));
+    }
+  }
+}
+
+template <typename E, int NW, int VPT>
+__device__ __noinline__ void dot_pass_2ph(const DotArgs a) {
+  // warp-uniform: does every vector this warp owns lie inside the row?
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bool full = true;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) full = full && ((k * NW + warp) * 32 + lane) < a.NV;
+  if (__all_sync(0xffffffffu, full))
+    dot_pass_2ph_impl<E, NW, VPT, true>(a);
+  else
+    dot_pass_2ph_impl<E, NW, VPT, false>(a);
+}
+// ---------------------------------------------------------------------------
 // Order-k tensors (axial_run, search.hpp:191-213) on the matrix view
 // M = n_0 x N', N' = n_1 ... n_{k-1} (row-major, last axis fastest).  Axis 0 of
 // a sweep is the dot pass (y = M kron(s_1..s_{k-1}), s_0 = sgn(y)); its column
@@ -671,8 +904,9 @@ __device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_
 // Column ownership: consumer thread (warp w, lane l) owns the 16-byte vectors
 // v_k = (k * NW + w) * 32 + l, k < VPT, of every row (coalesced LDS.128), i.e.
 // NE = VPT * EPV elements per row, and the matching NE f64 column accumulators.
-template <typename E, int NW, int VPT, int RG, bool KEEP>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p) {
+// CPS: CTAs per SM (1, or 2 with a 112-register budget and raw lag buffers).
+template <typename E, int NW, int VPT, int RG, int CPS>
+__device__ __forceinline__ void sweep_body(const KParams& p) {
   constexpr int EPV = Vec<E>::N;
   constexpr int CW = NW;       // consumer warps
   constexpr int CT = CW * 32;  // consumer threads
@@ -771,7 +1005,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
-        for (int j = 0; j < nstream; ++j, ++q) {
+        // the two-phase dot pass reads the streamed rows twice (y, then z)
+        const int reps = ((kind & F_DOT) && p.two_phase) ? 2 : 1;
+        for (int j = 0; j < nstream * reps; ++j, ++q) {
           const int s = static_cast<int>(q % D);
           if (q >= static_cast<unsigned>(D)) {
             const uint32_t ph = ((q / D) & 1u) ^ 1u;
@@ -783,7 +1019,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
           }
           mbar_expect_tx(&ctl->full[s], static_cast<uint32_t>(rowB));
           bulk_g2s(stage_base + static_cast<size_t>(s) * rowB,
-                   R + static_cast<size_t>(r0 + nres + j) * pitch, static_cast<uint32_t>(rowB), &ctl->full[s]);
+                   R + static_cast<size_t>(r0 + nres + j % nstream) * pitch, static_cast<uint32_t>(rowB),
+                   &ctl->full[s]);
         }
         prev_kind = kind;
       }
@@ -827,7 +1064,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
       for (int j = 0; j < p.zl && q0 + j * G < p.Q; ++j) nls = j + 1;
       for (int j = 0; j < nls; ++j) {
         const int col = (q0 + j * G) * 32 + lane;
-        const double* zp = p.zpart + col;
+        const double* zp = p.zpart + static_cast<size_t>(P & 1) * G * pitch + col;  // pass-parity buffer
         double a = 0.0;
         for (int g0 = gs; g0 < ge; g0 += 16) {  // 16 independent L2 loads in flight
           double v[16];
@@ -856,8 +1093,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
       }
       consumer_sync(CT);
     }
-    if (tid == 0) grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
-    consumer_sync(CT);
+    // Order-k: every CTA reads all of Z next, so the reduction ends in a grid
+    // barrier.  Matrix mode needs none: the next pass polls the pass-tagged t
+    // words, and zpart / slots / tb64 are reused only two passes later, i.e.
+    // after the next pass's grid barrier, which every CTA reaches only after
+    // finishing this reduction.
+    if (zmode) {
+      if (tid == 0) grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
+      consumer_sync(CT);
+    }
   };
 
   for (int P = 0;; ++P) {
@@ -918,7 +1162,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
       da.yrow = static_cast<unsigned>(L.yrow);
       da.s_nxt = static_cast<unsigned>(reinterpret_cast<unsigned char*>(s_nxt) - smem);
       da.tws = static_cast<unsigned>(L.tws);
-      da.zrow = p.zpart + static_cast<size_t>(g) * pitch;
+      da.zrow = p.zpart + (static_cast<size_t>(P & 1) * G + g) * pitch;
       da.errp = const_cast<unsigned*>(errp);
       da.rowB = static_cast<unsigned>(rowB);
       da.rows_g = rows_g;
@@ -930,7 +1174,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
       da.P = P;
       da.gcount = gcount;
       da.wmul = p.widen_mul;
-      dot_pass<E, NW, VPT, RG>(da);
+      da.ypart = static_cast<unsigned>(L.ypart);
+      da.prof = prof ? prof + g * 16 + 8 : nullptr;
+      if (p.two_phase)
+        dot_pass_2ph<E, NW, VPT>(da);
+      else
+        dot_pass<E, NW, VPT, RG, CPS>(da);
       const int ngroups = (rows_g + RG - 1) / RG;
       gcount += static_cast<unsigned>(ngroups);
     } else {
@@ -981,7 +1230,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
       }
     }
     if (D > 0) {  // advance the stage ring past this pass's streamed rows
-      const int t = qs + nstream;
+      const int t = qs + nstream * (((kind & F_DOT) && p.two_phase) ? 2 : 1);
       qph ^= (t / D) & 1;
       qs = t % D;
     }
@@ -1226,14 +1475,30 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p
     for (int i = 0; i < 7; ++i) prof[g * 16 + i] = static_cast<unsigned long long>(pacc[i]);
 }
 
-template <typename E, int NW, int VPT, int RG, bool KEEP>
+template <typename E, int NW, int VPT, int RG>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p) {
+  sweep_body<E, NW, VPT, RG, 1>(p);
+}
+template <typename E, int NW, int VPT, int RG>
+__global__ void __maxnreg__(112) sweep_kernel2(const KParams p) {
+  sweep_body<E, NW, VPT, RG, 2>(p);
+}
+
+template <typename E, int NW, int VPT, int RG, int CPS>
 struct Kern {
-  static void* fn() { return reinterpret_cast<void*>(&sweep_kernel<E, NW, VPT, RG, KEEP>); }
+  static void* fn() {
+    if constexpr (CPS == 1)
+      return reinterpret_cast<void*>(&sweep_kernel<E, NW, VPT, RG>);
+    else
+      return reinterpret_cast<void*>(&sweep_kernel2<E, NW, VPT, RG>);
+  }
 };
 
 void* kernel_for(const Variant& v) {
 #define SCB_K(E, NW, VPT, RG) \
-  if (v.nw == NW && v.vpt == VPT && v.rg == RG && v.keep == 1) return Kern<E, NW, VPT, RG, true>::fn();
+  if (v.nw == NW && v.vpt == VPT && v.rg == RG && v.cps == 1) return Kern<E, NW, VPT, RG, 1>::fn();
+#define SCB_K2(E, NW, VPT, RG) \
+  if (v.nw == NW && v.vpt == VPT && v.rg == RG && v.cps == 2) return Kern<E, NW, VPT, RG, 2>::fn();
   if (v.dtype == 0) {
     SCB_K(float, 8, 1, 4)
     SCB_K(float, 8, 2, 2)
@@ -1243,6 +1508,8 @@ void* kernel_for(const Variant& v) {
     SCB_K(float, 16, 2, 1)
     SCB_K(float, 8, 8, 1)
     SCB_K(float, 16, 8, 1)
+    SCB_K2(float, 8, 4, 1)
+    SCB_K2(float, 8, 2, 2)
   } else {
     SCB_K(double, 8, 1, 4)
     SCB_K(double, 8, 2, 2)
@@ -1252,6 +1519,7 @@ void* kernel_for(const Variant& v) {
     SCB_K(double, 16, 8, 1)
   }
 #undef SCB_K
+#undef SCB_K2
   return nullptr;
 }
 
@@ -1263,7 +1531,7 @@ int pick_variant(int dtype, long long pitch, Variant* v) {
   const int epv = dtype == 0 ? 4 : 2;
   const long long nv = pitch / epv;
   v->dtype = dtype;
-  v->keep = 1;
+  v->cps = 1;
   v->nw = 8;
   if (nv <= 256) {
     v->vpt = 1; v->rg = 4;
@@ -1278,9 +1546,9 @@ int pick_variant(int dtype, long long pitch, Variant* v) {
   } else {
     return 1;
   }
-  if (const char* e = std::getenv("SCB_VARIANT")) {  // tuning override "nw,vpt,rg"
+  if (const char* e = std::getenv("SCB_VARIANT")) {  // tuning override "nw,vpt,rg[,cps]"
     Variant t = *v;
-    if (std::sscanf(e, "%d,%d,%d", &t.nw, &t.vpt, &t.rg) == 3 && kernel_for(t) != nullptr &&
+    if (std::sscanf(e, "%d,%d,%d,%d", &t.nw, &t.vpt, &t.rg, &t.cps) >= 3 && kernel_for(t) != nullptr &&
         static_cast<long long>(t.nw) * 32 * t.vpt >= nv)
       *v = t;
   }
@@ -1290,7 +1558,20 @@ int pick_variant(int dtype, long long pitch, Variant* v) {
 cudaError_t set_smem_limit(const Variant& v, size_t bytes) {
   void* f = kernel_for(v);
   if (!f) return cudaErrorInvalidValue;
-  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e != cudaSuccess) return e;
+  // all of the unified L1/shared array as shared memory (the kernel streams R
+  // through TMA, not L1), so co-residency is decided by the real 228 KB
+  return cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+
+int blocks_per_sm(const Variant& v, size_t smem_bytes) {
+  void* f = kernel_for(v);
+  int nb = 0;
+  if (!f || set_smem_limit(v, smem_bytes) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, (v.nw + 1) * 32, smem_bytes) != cudaSuccess)
+    return 0;
+  return nb;
 }
 
 cudaError_t launch_sweep(const Variant& v, const KParams& p, size_t smem_bytes, cudaStream_t st) {

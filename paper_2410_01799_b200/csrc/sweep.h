@@ -63,7 +63,7 @@ struct KParams {
   int t0_stride;       // u32 words per start vector (= 2 * ceil(n/64))
   unsigned long long* tb64;  // [2][Q] t words tagged with the consuming pass: (P << 32) | word
   uint32_t* tbest;     // [Q] t of the best restart so far (restarts > 1)
-  double* zpart;       // [G][pitch] per-CTA column partials
+  double* zpart;       // [2][G][pitch] per-CTA column partials, by pass parity
   Slot* slots;         // [G] c / ||R||^2 partials
   unsigned* bar;       // grid barrier counter
   unsigned* err_pass;  // [3] first pass index that saw an error (UINT_MAX = none)
@@ -90,6 +90,7 @@ struct KParams {
   const uint32_t* ax0; // [width][restarts][axw] start words of axes 1..k-1
   uint32_t* AX_out;    // [width][axw] accepted axis words
   double* zfull;       // [pitch] reduced z (order-k mode)
+  int two_phase;       // 1: dot pass as (A) y = R t, (B) z = R^T s' (rows streamed twice)
   unsigned long long* prof;  // [G][16] clock64 breakdown or nullptr
 };
 
@@ -99,14 +100,14 @@ struct Variant {
   int nw;     // consumer warps (each owns a column segment of every row)
   int vpt;    // 16-byte vectors per thread per row
   int rg;     // rows per group (one dot-partial publication per group)
-  int keep;   // 1: lagged group kept in registers; 0: re-read from shared memory
+  int cps;    // CTAs per SM (2: 113-register budget, raw lag buffers)
 };
 
 constexpr int kRing = 4;  // dot-partial ring depth (groups)
 
 // Shared-memory carve-up (byte offsets from the dynamic smem base).
 struct Layout {
-  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, total;
+  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, ypart, total;
 };
 
 inline __host__ __device__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
@@ -137,6 +138,8 @@ inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_r
   o += align16(static_cast<size_t>(3) * sw * 4);
   L.ax = o;  // [2][axw]: current / best axis words (order-k mode)
   o += align16(static_cast<size_t>(2) * axw * 4);
+  L.ypart = o;  // [rows_max][nw]: per-warp row partials of the two-phase dot pass
+  o += align16(static_cast<size_t>(rows_max) * nw * 8);
   L.total = o;
   return L;
 }
@@ -144,6 +147,7 @@ inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_r
 // Returns 0 on success.
 int pick_variant(int dtype, long long pitch, Variant* v);
 cudaError_t set_smem_limit(const Variant& v, size_t bytes);
+int blocks_per_sm(const Variant& v, size_t smem_bytes);  // co-resident CTAs at this smem
 cudaError_t launch_sweep(const Variant& v, const KParams& p, size_t smem_bytes, cudaStream_t st);
 
 }  // namespace scb

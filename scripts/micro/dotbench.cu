@@ -3,7 +3,7 @@
 #include <cstdio>
 #include <vector>
 namespace scb {
-template <int NW, int VPT, int RG>
+template <int NW, int VPT, int RG, int TWO>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) dotbench(int rows, int n, int passes, long long* cyc, double* zout, int wmul, unsigned long long* tprof) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int pitch = (n + 31) / 32 * 32;
@@ -31,24 +31,24 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) dotbench(int rows, int n, in
   unsigned gcount = 0;
   const long long t0 = clock64();
   for (int P = 0; P < passes; ++P) {
-    a.P = P; a.gcount = gcount; a.wmul = wmul;
+    a.P = P; a.gcount = gcount; a.wmul = wmul; a.ypart = L.ypart; a.prof = nullptr;
 #ifdef SCB_TIMING
     a.tprof = tprof;
 #endif
-    dot_pass<float, NW, VPT, RG>(a);
+    if (TWO) dot_pass_2ph<float, NW, VPT>(a); else dot_pass<float, NW, VPT, RG>(a);
     gcount += (rows + RG - 1) / RG;
     asm volatile("bar.sync 1, %0;" :: "r"(NW * 32));
   }
   if (tid == 0) cyc[blockIdx.x] = clock64() - t0;
 }
 }  // namespace scb
-template <int NW, int VPT, int RG>
+template <int NW, int VPT, int RG, int TWO = 0>
 void run(int rows, int n, const char* name) {
   using namespace scb;
   int pitch = (n + 31) / 32 * 32;
   size_t rowB = pitch * 4;
   Layout L = make_layout(rowB, 0, rows, RG, NW, rows, pitch / 32, 1, (rows + 31) / 32);
-  auto f = dotbench<NW, VPT, RG>;
+  auto f = dotbench<NW, VPT, RG, TWO>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   long long* cyc; double* z; cudaMalloc(&cyc, 8 * 148); cudaMalloc(&z, 8 * 148 * (size_t)pitch);
   int passes = 200;
@@ -68,7 +68,10 @@ void run(int rows, int n, const char* name) {
          rows * (double)n / avg, cudaGetErrorString(e));
 }
 int main(int argc, char** argv) {
-  if (argc > 1) { run<8, 4, 1>(12, 4096, "8,4,1"); run<8, 4, 2>(12, 4096, "8,4,2"); return 0; }
+  if (argc > 1) { run<8, 4, 1, 1>(12, 4096, "2ph 8,4"); return 0; }
+  run<8, 4, 1, 1>(12, 4096, "2ph 8,4");
+  run<8, 4, 1, 1>(24, 4096, "2ph 8,4");
+  run<16, 2, 1, 1>(12, 4096, "2ph 16,2");
   run<8, 4, 1>(7, 4096, "8,4,1");
   run<8, 4, 1>(12, 4096, "8,4,1");
   run<8, 1, 4>(7, 1024, "8,1,4");
