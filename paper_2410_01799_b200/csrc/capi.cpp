@@ -274,6 +274,9 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
     return set_err(ctx, SC_NOT_SUPPORTED, "row length %llu exceeds the fused-kernel envelope",
                    static_cast<unsigned long long>(n));
 
+  // wide rows: column chunks of one warp-tile pass (var.nw * 32 * var.vpt vectors)
+  const long long tile_cols = static_cast<long long>(var.nw) * 32 * var.vpt * (dt == SC_F32 ? 4 : 2);
+  const int cpr = pitch > tile_cols ? static_cast<int>((pitch + tile_cols - 1) / tile_cols) : 1;
   const int G = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(ctx->num_sms) * var.cps, m));
   const int rows_base = static_cast<int>(m / G), rows_rem = static_cast<int>(m % G);
   const int rows_max = rows_base + (rows_rem ? 1 : 0);
@@ -281,21 +284,22 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   const int sw = (rows_max + 31) / 32;
   const int zl = std::max(1, std::min(4, (Q + G - 1) / G));
   const size_t rowB = static_cast<size_t>(pitch) * es;
+  const size_t stageB = cpr > 1 ? static_cast<size_t>(tile_cols) * es : rowB;  // one row or one chunk
   auto smem_for = [&](int st_, int res_) {
-    return scb::make_layout(rowB, st_, res_, var.rg, var.nw, rows_max, Q, zl, sw, axw).total;
+    return scb::make_layout(stageB, st_, res_, var.rg, var.nw, rows_max, Q, zl, sw, axw).total;
   };
   // per-CTA shared memory: the opt-in maximum, or an even split of the SM's
   // 228 KB (minus the 1 KB the runtime reserves per CTA) when two CTAs share an SM
   const size_t cap = var.cps == 1 ? ctx->smem_optin : std::min(ctx->smem_optin, (ctx->smem_per_sm / var.cps) - 1024);
   int stages = 0, res_rows = rows_max;
-  if (smem_for(0, rows_max) > cap) {
+  if (cpr > 1 || smem_for(0, rows_max) > cap) {
     stages = static_cast<int>(env_size("SCB_STAGES", static_cast<size_t>(2 * var.rg + 4)));
     stages = std::max(2, std::min(stages, scb::kMaxStages));
     while (stages > 2 && smem_for(stages, 0) > cap) --stages;
     if (smem_for(stages, 0) > cap)
       return set_err(ctx, SC_NOT_SUPPORTED, "row of %zu bytes does not fit the shared-memory ring", rowB);
     res_rows = 0;
-    while (res_rows < rows_max && smem_for(stages, res_rows + 1) <= cap) ++res_rows;
+    while (cpr == 1 && res_rows < rows_max && smem_for(stages, res_rows + 1) <= cap) ++res_rows;
     res_rows = static_cast<int>(std::min<size_t>(env_size("SCB_RES_ROWS", static_cast<size_t>(res_rows)),
                                                  static_cast<size_t>(res_rows)));
   }
@@ -454,7 +458,9 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   kp.ax0 = reinterpret_cast<const uint32_t*>(ax0);
   kp.AX_out = reinterpret_cast<uint32_t*>(AX_out);
   kp.zfull = zfull;
-  kp.two_phase = static_cast<int>(env_size("SCB_2PH", 1));  // SCB_2PH=0: fused single-read pass
+  kp.two_phase = cpr > 1 ? 1 : static_cast<int>(env_size("SCB_2PH", 1));  // SCB_2PH=0: fused single-read pass
+  kp.cpr = cpr;
+  kp.chunk_cols = cpr > 1 ? static_cast<int>(tile_cols) : static_cast<int>(pitch);
 
   const bool prof = std::getenv("SCB_PROF") != nullptr;
   unsigned long long* dprof = nullptr;

@@ -244,6 +244,7 @@ struct DotArgs {
   unsigned gcount;
   int wmul;  // 1 << 29 (run-time value)
   unsigned long long* prof;  // [4] thread-0 cycle sums (SCB_PROFILE builds): stage waits, A, B, C
+  int cpr, chunk_cols;       // wide rows: column chunks per row (stage = one chunk)
 #ifdef SCB_TIMING
   unsigned long long* tprof;  // [blocks][warps][8] section cycle sums (dotbench only)
 #endif
@@ -799,6 +800,191 @@ __device__ __noinline__ void dot_pass_2ph(const DotArgs a) {
     dot_pass_2ph_impl<E, NW, VPT, false>(a);
 }
 // ---------------------------------------------------------------------------
+// Wide rows (cpr > 1): the two-phase pass over column chunks.  Every (row,
+// chunk) piece is one TMA stage; both phases walk the pieces chunk-major, so
+// the t-flip masks (phase A) and the z accumulators (phase C) of a chunk stay
+// in registers across all rows.  Phase A accumulates the per-warp partial of
+// row j over the chunks in ypart[j][warp] (owned by that warp; fixed chunk
+// order), then the same combine as the single-chunk pass.  No resident rows.
+template <typename E, int NW, int VPT, bool FULL>
+__device__ __forceinline__ void ld_piece(const typename Vec<E>::T* rp, unsigned toff, const int (&vloc)[VPT],
+                                         const bool (&vok)[VPT], E (&x)[VPT * Vec<E>::N]) {
+  using VT = typename Vec<E>::T;
+  constexpr int EPV = Vec<E>::N;
+  if constexpr (FULL) {
+#pragma unroll
+    for (int k = 0; k < VPT; ++k)
+      Vec<E>::split(*reinterpret_cast<const VT*>(reinterpret_cast<const unsigned char*>(rp) + toff +
+                                                  k * (NW * 32 * sizeof(VT))),
+                    &x[k * EPV]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      Vec<E>::split(rp[vok[k] ? vloc[k] : 0], &x[k * EPV]);
+      if (!vok[k]) {
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) x[k * EPV + e] = E(0);
+      }
+    }
+  }
+}
+
+struct PieceCursor {
+  int sslot, sph, D;
+  const unsigned char* stage_base;
+  unsigned long long* full;
+  unsigned long long* empty;
+  size_t stageB;
+  __device__ __forceinline__ const unsigned char* next(int& sl) {
+    mbar_wait(&full[sslot], static_cast<uint32_t>(sph));
+    sl = sslot;
+    if (++sslot == D) {
+      sslot = 0;
+      sph ^= 1;
+    }
+    return stage_base + static_cast<size_t>(sl) * stageB;
+  }
+  __device__ __forceinline__ void release(int sl) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[sl]);
+  }
+};
+
+// phase A over one chunk: every row's partial against this chunk's t, reduced in
+// the warp and accumulated into ypart[j][warp]
+template <typename E, int NW, int VPT, bool FULL>
+__device__ __forceinline__ void chunk_dot(PieceCursor& cur, int rows_g, int k, unsigned toff, const int (&vloc)[VPT],
+                                          const bool (&vok)[VPT], const uint32_t (&fm)[VPT * Vec<E>::N],
+                                          double* ypart) {
+  using VT = typename Vec<E>::T;
+  constexpr int NE = VPT * Vec<E>::N;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto partial = [&](const E (&x)[NE]) -> double {
+    double ac[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < NE; ++i) ac[i & 3] = fma(widen_shf(x[i], fm[i]), Wide<E>::zscale(1.0), ac[i & 3]);
+    return (ac[0] + ac[1]) + (ac[2] + ac[3]);
+  };
+  for (int j = 0; j < rows_g; ++j) {
+    int sl;
+    const VT* rp = reinterpret_cast<const VT*>(cur.next(sl));
+    E x[NE];
+    ld_piece<E, NW, VPT, FULL>(rp, toff, vloc, vok, x);
+    double v = partial(x);
+    cur.release(sl);
+    v = warp_sum(v);
+    if (lane == 0) ypart[j * NW + warp] = (k == 0) ? v : ypart[j * NW + warp] + v;
+  }
+}
+
+// phase C over one chunk: z of the chunk's columns accumulated over all rows
+template <typename E, int NW, int VPT, bool FULL>
+__device__ __forceinline__ void chunk_z(PieceCursor& cur, int rows_g, unsigned toff, const int (&vloc)[VPT],
+                                        const bool (&vok)[VPT], const uint32_t* s_nxt, double* zrow_chunk) {
+  using VT = typename Vec<E>::T;
+  constexpr int EPV = Vec<E>::N;
+  constexpr int NE = VPT * EPV;
+  double zacc[NE];
+#pragma unroll
+  for (int i = 0; i < NE; ++i) zacc[i] = 0.0;
+  for (int j = 0; j < rows_g; ++j) {
+    int sl;
+    const VT* rp = reinterpret_cast<const VT*>(cur.next(sl));
+    E x[NE];
+    ld_piece<E, NW, VPT, FULL>(rp, toff, vloc, vok, x);
+    const double g = Wide<E>::zscale(((s_nxt[j >> 5] >> (j & 31)) & 1u) ? -1.0 : 1.0);
+#pragma unroll
+    for (int i = 0; i < NE; ++i) zacc[i] = fma(widen_shf(x[i], 0u), g, zacc[i]);
+    cur.release(sl);
+  }
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    if (vok[k]) {
+#pragma unroll
+      for (int e = 0; e < EPV; e += 2)
+        __stcg(reinterpret_cast<double2*>(zrow_chunk + vloc[k] * EPV + e), make_double2(zacc[k * EPV + e], zacc[k * EPV + e + 1]));
+    }
+  }
+}
+
+template <typename E, int NW, int VPT>
+__device__ __noinline__ void dot_pass_chunked(const DotArgs a) {
+  constexpr int EPV = Vec<E>::N;
+  constexpr int NE = VPT * EPV;
+  constexpr int chunkV = NW * 32 * VPT;  // vectors per chunk
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows_g = a.rows_g, NV = a.NV, P = a.P, cpr = a.cpr;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* yrow = reinterpret_cast<double*>(smem + a.yrow);
+  double* ypart = reinterpret_cast<double*>(smem + a.ypart);
+  uint32_t* s_nxt = reinterpret_cast<uint32_t*>(smem + a.s_nxt);
+  const uint32_t* tws = reinterpret_cast<const uint32_t*>(smem + a.tws);
+  PieceCursor cur{a.sslot, a.sph, a.D, smem + a.stage, reinterpret_cast<unsigned long long*>(smem + a.full),
+                  reinterpret_cast<unsigned long long*>(smem + a.empty), a.rowB};
+  const unsigned toff = static_cast<unsigned>((warp * 32 + lane) * sizeof(typename Vec<E>::T));
+  int vloc[VPT];
+  bool vok[VPT];
+  auto setup = [&](int k) -> bool {  // this chunk's vectors; returns warp-uniform "all inside"
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      vloc[q] = (q * NW + warp) * 32 + lane;
+      vok[q] = k * chunkV + vloc[q] < NV;
+      ok = ok && vok[q];
+    }
+    return __all_sync(0xffffffffu, ok);
+  };
+  // ---- (A) y partials, chunk-major ----
+  for (int k = 0; k < cpr; ++k) {
+    const bool full = setup(k);
+    uint32_t tbits = 0;
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const int col0 = (k * chunkV + vloc[q]) * EPV;
+      if (vok[q]) tbits |= ((tws[col0 >> 5] >> (col0 & 31)) & ((1u << EPV) - 1u)) << (q * EPV);
+    }
+    uint32_t fm[NE];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) fm[i] = bitmask(tbits, i);
+    if (full)
+      chunk_dot<E, NW, VPT, true>(cur, rows_g, k, toff, vloc, vok, fm, ypart);
+    else
+      chunk_dot<E, NW, VPT, false>(cur, rows_g, k, toff, vloc, vok, fm, ypart);
+  }
+  consumer_sync(NW * 32);
+  // ---- (B) y and s' of every row, fixed warp order ----
+  for (int jb = 0; jb < rows_g; jb += NW * 32) {
+    const int jj = jb + tid;
+    const bool ok = jj < rows_g;
+    double y = 0.0;
+    if (ok) {
+      const double* pr = ypart + jj * NW;
+      double y0 = pr[0], y1 = pr[1];
+#pragma unroll
+      for (int w = 2; w < NW; w += 2) {
+        y0 += pr[w];
+        y1 += pr[w + 1];
+      }
+      y = y0 + y1;
+      yrow[jj] = y;
+      if (!isfinite(y)) atomicMin(a.errp + ERR_Y, static_cast<unsigned>(P));
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, ok && y < 0.0);
+    if (lane == 0 && jb + warp * 32 < rows_g) s_nxt[(jb >> 5) + warp] = word;
+  }
+  consumer_sync(NW * 32);
+  // ---- (C) z, chunk-major ----
+  for (int k = 0; k < cpr; ++k) {
+    const bool full = setup(k);
+    double* zc = a.zrow + static_cast<size_t>(k) * chunkV * EPV;
+    if (full)
+      chunk_z<E, NW, VPT, true>(cur, rows_g, toff, vloc, vok, s_nxt, zc);
+    else
+      chunk_z<E, NW, VPT, false>(cur, rows_g, toff, vloc, vok, s_nxt, zc);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Order-k tensors (axial_run, search.hpp:191-213) on the matrix view
 // M = n_0 x N', N' = n_1 ... n_{k-1} (row-major, last axis fastest).  Axis 0 of
 // a sweep is the dot pass (y = M kron(s_1..s_{k-1}), s_0 = sgn(y)); its column
@@ -930,7 +1116,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   const int nstream = rows_g - nres;
   const int D = p.stages;
 
-  const Layout L = make_layout(rowB, D, p.res_rows, RG, NW, p.rows_max, p.Q, p.zl, p.sw, p.axw);
+  // stage = one row, or one column chunk of a wide row (then no resident rows)
+  const size_t stageB = p.cpr > 1 ? static_cast<size_t>(p.chunk_cols) * sizeof(E) : rowB;
+  const int npieces = nstream * p.cpr;  // TMA pieces per streaming sweep over the band
+  const Layout L = make_layout(stageB, D, p.res_rows, RG, NW, p.rows_max, p.Q, p.zl, p.sw, p.axw);
   unsigned char* stage_base = smem + L.stage;
   unsigned char* res_base = smem + L.res;
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + L.ctl);
@@ -985,9 +1174,13 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   __syncthreads();
 
   // ======================= TMA producer (one thread) =======================
+  // Keep this loop lean: the producer warp shares SMSP 0 with two consumer
+  // warps, and every instruction it issues is taken from them (runtime integer
+  // divisions here cost ~10% of the pass; one lane per stage was slower still).
   if (warp == CW) {
     if (lane != 0 || nstream == 0) return;
     unsigned q = 0;
+    int ps = 0, pph = 0;  // stage slot of piece q and its ring phase (q / D) & 1
     int prev_kind = 0;
     long long pwait = 0;
     for (int P = 0;; ++P) {
@@ -1005,22 +1198,41 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
-        // the two-phase dot pass reads the streamed rows twice (y, then z)
-        const int reps = ((kind & F_DOT) && p.two_phase) ? 2 : 1;
-        for (int j = 0; j < nstream * reps; ++j, ++q) {
-          const int s = static_cast<int>(q % D);
-          if (q >= static_cast<unsigned>(D)) {
-            const uint32_t ph = ((q / D) & 1u) ^ 1u;
-            const long long tw0 = p.prof ? clock64() : 0;
-            while (!mbar_try_wait(&ctl->empty[s], ph)) {
-              if (ctl->abort) goto drain;
+        // the two-phase dot pass reads the streamed rows twice (y, then z); wide
+        // rows go as column chunks, chunk-major in dot passes, row-major otherwise
+        const bool dotp = (kind & F_DOT) && p.two_phase;
+        const int reps = dotp ? 2 : 1;
+        for (int rep = 0; rep < reps; ++rep) {
+          int row = 0, chunk = 0;  // piece cursor: chunk-major in dot passes, row-major otherwise
+          for (int idx = 0; idx < npieces; ++idx, ++q) {
+            const int s = ps;
+            if (q >= static_cast<unsigned>(D)) {
+              const uint32_t ph = static_cast<uint32_t>(pph) ^ 1u;
+              const long long tw0 = p.prof ? clock64() : 0;
+              while (!mbar_try_wait(&ctl->empty[s], ph)) {
+                if (ctl->abort) goto drain;
+#ifdef SCB_PRODUCER_SLEEP
+                __nanosleep(SCB_PRODUCER_SLEEP);  // yield issue slots to the consumer warps on this SMSP
+#endif
+              }
+              if (p.prof) pwait += clock64() - tw0;
             }
-            if (p.prof) pwait += clock64() - tw0;
+            const long long c0 = static_cast<long long>(chunk) * p.chunk_cols;
+            const uint32_t bytes = p.cpr == 1 ? static_cast<uint32_t>(rowB)
+                                              : static_cast<uint32_t>(min(static_cast<long long>(p.chunk_cols), pitch - c0) * sizeof(E));
+            mbar_expect_tx(&ctl->full[s], bytes);
+            bulk_g2s(stage_base + static_cast<size_t>(s) * stageB, R + static_cast<size_t>(r0 + nres + row) * pitch + c0,
+                     bytes, &ctl->full[s]);
+            if (++ps == D) {  // incremental stage / phase (no division on the refill path)
+              ps = 0;
+              pph ^= 1;
+            }
+            if (dotp) {
+              if (++row == nstream) { row = 0; ++chunk; }
+            } else {
+              if (++chunk == p.cpr) { chunk = 0; ++row; }
+            }
           }
-          mbar_expect_tx(&ctl->full[s], static_cast<uint32_t>(rowB));
-          bulk_g2s(stage_base + static_cast<size_t>(s) * rowB,
-                   R + static_cast<size_t>(r0 + nres + j % nstream) * pitch, static_cast<uint32_t>(rowB),
-                   &ctl->full[s]);
         }
         prev_kind = kind;
       }
@@ -1176,10 +1388,16 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       da.wmul = p.widen_mul;
       da.ypart = static_cast<unsigned>(L.ypart);
       da.prof = prof ? prof + g * 16 + 8 : nullptr;
-      if (p.two_phase)
+      da.cpr = p.cpr;
+      da.chunk_cols = p.chunk_cols;
+      if (p.cpr > 1) {
+        da.rowB = static_cast<unsigned>(stageB);
+        dot_pass_chunked<E, NW, VPT>(da);
+      } else if (p.two_phase) {
         dot_pass_2ph<E, NW, VPT>(da);
-      else
+      } else {
         dot_pass<E, NW, VPT, RG, CPS>(da);
+      }
       const int ngroups = (rows_g + RG - 1) / RG;
       gcount += static_cast<unsigned>(ngroups);
     } else {
@@ -1188,49 +1406,55 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       // one term, decompose.hpp:200-214; ||R||_F^2; final write-back of resident rows).
       // All warps walk the rows in order (each takes a column segment), so the
       // stage ring is consumed in order and its phase parity is unambiguous.
+      const int chunkVv = p.cpr > 1 ? p.chunk_cols / EPV : NV;  // vectors per piece
       for (int j = 0; j < rows_g; ++j) {
-        VT* rv;
-        int slot = -1;
-        if (j < nres) {
-          rv = reinterpret_cast<VT*>(res_base + static_cast<size_t>(j) * rowB);
-        } else {
-          slot = sslot;
-          mbar_wait(&ctl->full[slot], static_cast<uint32_t>(sph));
-          rv = reinterpret_cast<VT*>(stage_base + static_cast<size_t>(slot) * rowB);
-          if (++sslot == D) {
-            sslot = 0;
-            sph ^= 1;
-          }
-        }
         const uint32_t sneg = ((s_upd[j >> 5] >> (j & 31)) & 1u) << 31;
-        VT* grow = reinterpret_cast<VT*>(R + static_cast<size_t>(r0 + j) * pitch);
-        for (int v = tid; v < NV; v += CT) {
-          E x[EPV];
-          Vec<E>::split(rv[v], x);
-          if (kind & F_UPD) {
-            const uint32_t ub = (uws[(v * EPV) >> 5] >> ((v * EPV) & 31)) & ((1u << EPV) - 1u);
-#pragma unroll
-            for (int e = 0; e < EPV; ++e)
-              if (v * EPV + e < p.n)  // flush_pending with one term: data += flip(-alpha, s_i ^ t_j)
-                x[e] = Vec<E>::narrow(static_cast<double>(x[e]) + flipd(-alpha, sneg ^ bitmask(ub, e)));
-            if (j < nres) rv[v] = Vec<E>::join(x);
+        for (int k = 0; k < p.cpr; ++k) {
+          VT* rv;
+          int slot = -1;
+          if (j < nres) {
+            rv = reinterpret_cast<VT*>(res_base + static_cast<size_t>(j) * rowB);
+          } else {
+            slot = sslot;
+            mbar_wait(&ctl->full[slot], static_cast<uint32_t>(sph));
+            rv = reinterpret_cast<VT*>(stage_base + static_cast<size_t>(slot) * stageB);
+            if (++sslot == D) {
+              sslot = 0;
+              sph ^= 1;
+            }
           }
-          if ((j >= nres && (kind & F_UPD)) || (kind & F_WB)) grow[v] = Vec<E>::join(x);
+          const int v0 = k * chunkVv;  // first vector of the piece within the row
+          const int nvp = min(chunkVv, NV - v0);
+          VT* grow = reinterpret_cast<VT*>(R + static_cast<size_t>(r0 + j) * pitch) + v0;
+          for (int v = tid; v < nvp; v += CT) {
+            const int gv = v0 + v;
+            E x[EPV];
+            Vec<E>::split(rv[v], x);
+            if (kind & F_UPD) {
+              const uint32_t ub = (uws[(gv * EPV) >> 5] >> ((gv * EPV) & 31)) & ((1u << EPV) - 1u);
 #pragma unroll
-          for (int e = 0; e < EPV; ++e) {
-            const double d = static_cast<double>(x[e]);
-            nacc += d * d;
-            if (kind & F_CHECK) bad |= !isfinite(d);
+              for (int e = 0; e < EPV; ++e)
+                if (gv * EPV + e < p.n)  // flush_pending with one term: data += flip(-alpha, s_i ^ t_j)
+                  x[e] = Vec<E>::narrow(static_cast<double>(x[e]) + flipd(-alpha, sneg ^ bitmask(ub, e)));
+              if (j < nres) rv[v] = Vec<E>::join(x);
+            }
+            if ((j >= nres && (kind & F_UPD)) || (kind & F_WB)) grow[v] = Vec<E>::join(x);
+#pragma unroll
+            for (int e = 0; e < EPV; ++e) {
+              const double d = static_cast<double>(x[e]);
+              nacc += d * d;
+              if (kind & F_CHECK) bad |= !isfinite(d);
+            }
           }
-        }
-        if (slot >= 0) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl->empty[slot]);
+          if (slot >= 0) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ctl->empty[slot]);
+          }
         }
       }
     }
     if (D > 0) {  // advance the stage ring past this pass's streamed rows
-      const int t = qs + nstream * (((kind & F_DOT) && p.two_phase) ? 2 : 1);
+      const int t = qs + npieces * (((kind & F_DOT) && p.two_phase) ? 2 : 1);
       qph ^= (t / D) & 1;
       qs = t % D;
     }
@@ -1507,7 +1731,6 @@ void* kernel_for(const Variant& v) {
     SCB_K(float, 16, 2, 2)
     SCB_K(float, 16, 2, 1)
     SCB_K(float, 8, 8, 1)
-    SCB_K(float, 16, 8, 1)
     SCB_K2(float, 8, 4, 1)
     SCB_K2(float, 8, 2, 2)
   } else {
@@ -1515,8 +1738,6 @@ void* kernel_for(const Variant& v) {
     SCB_K(double, 8, 2, 2)
     SCB_K(double, 8, 4, 2)
     SCB_K(double, 8, 8, 1)
-    SCB_K(double, 16, 4, 1)
-    SCB_K(double, 16, 8, 1)
   }
 #undef SCB_K
 #undef SCB_K2
@@ -1539,12 +1760,10 @@ int pick_variant(int dtype, long long pitch, Variant* v) {
     v->vpt = 2; v->rg = 2;
   } else if (nv <= 1024) {
     v->vpt = 4; v->rg = dtype == 0 ? 1 : 2;
-  } else if (nv <= 2048) {
-    v->vpt = 8; v->rg = 1;
-  } else if (nv <= 4096) {  // wide rows: 16 consumer warps, register-capped (spills; correct, not tuned)
-    v->nw = 16; v->vpt = 8; v->rg = 1;
   } else {
-    return 1;
+    // nv <= 2048: whole rows; wider: the same tile over column chunks of 2048
+    // vectors (8192 f32 / 4096 f64 columns, one TMA stage each, two-phase pass)
+    v->vpt = 8; v->rg = 1;
   }
   if (const char* e = std::getenv("SCB_VARIANT")) {  // tuning override "nw,vpt,rg[,cps]"
     Variant t = *v;

@@ -91,6 +91,10 @@ struct KParams {
   uint32_t* AX_out;    // [width][axw] accepted axis words
   double* zfull;       // [pitch] reduced z (order-k mode)
   int two_phase;       // 1: dot pass as (A) y = R t, (B) z = R^T s' (rows streamed twice)
+  // wide rows: every row is streamed as cpr column chunks of chunk_cols
+  // elements (one stage each); cpr == 1, chunk_cols == pitch otherwise
+  int cpr;
+  int chunk_cols;
   unsigned long long* prof;  // [G][16] clock64 breakdown or nullptr
 };
 

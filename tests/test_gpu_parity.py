@@ -297,3 +297,35 @@ def test_order_k_single_cut_restarts(engine, ref):
             assert (r.signs[i] == o["signs"][i]).all()
         if restarts == 1:
             assert r.iterations == o["iterations"]
+
+
+# ------------------------------------------------------------------- wide rows
+# Rows wider than one warp-tile pass (f32 > 8192, f64 > 4096 columns) stream as
+# column chunks (one TMA stage each) through the chunked two-phase pass.
+@pytest.mark.parametrize("shape,dtype,width", [((64, 20000), "f32", 5), ((300, 8193), "f32", 4),
+                                               ((50, 9000), "f64", 5), ((3, 12345), "f64", 3),
+                                               ((256, 65536), "f32", 2)])
+def test_wide_rows_vs_reference(engine, ref, shape, dtype, width):
+    m, n = shape
+    a = ref.fill_normal(m + n, m * n).reshape(m, n)
+    a_in = a.astype(np.float32) if dtype == "f32" else a
+    dec, rep, rem = run(engine, a_in, width, seed=3, dtype=dtype, remainder=True)
+    od = ref.greedy_decompose(a_in.astype(np.float64), width, seed=3, want_remainder=True)
+    tol = F32_TOL if dtype == "f32" else F64_TOL
+    assert dec.width() == od.width
+    assert (dec.factors[0][:2] == od.signs[0][:2]).all() and (dec.factors[1][:2] == od.signs[1][:2]).all()
+    if dtype == "f64":
+        assert (dec.factors[0] == od.signs[0]).all() and (dec.factors[1] == od.signs[1]).all()
+        assert sweeps_ok(rep.sweeps, od.iterations)
+    assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= tol
+    rel_g, rel_r = rep.final_residual_norm / rep.input_norm, od.final_residual_norm / od.input_norm
+    assert abs(rel_g - rel_r) <= tol * rel_r
+
+
+def test_order3_wide_trailing_axes(engine, ref):
+    a = ref.fill_normal(91, 20 * 3000 * 3).reshape(20, 3000, 3)  # matrix view 20 x 9000 (two chunks)
+    dec, rep, _ = run(engine, a, 4, seed=9)
+    od = ref.greedy_decompose(a, 4, seed=9)
+    for i in range(3):
+        assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
+    assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F64_TOL
