@@ -141,6 +141,40 @@ uint64_t sc_width_for_compression(int coeff_bits, int source_bits, int order,
  * multi-GPU batch path (one process per GPU, no data-path collective). */
 void sc_lpt_schedule(const double* costs, uint64_t count, uint32_t bins, uint32_t* bin_of_job);
 
+/* ------------------------------------------------------------------------ */
+/* Row-sharded decomposition of ONE matrix over `world` GPUs (one process and
+ * one context per GPU).  Rank r owns the contiguous row band
+ * [row0, row0 + local rows) of the m_global x n matrix.  The persistent kernel
+ * of every rank joins one grid: per pass the z partials and the c / ||R||^2
+ * partials of all ranks' CTAs are reduced in the same fixed order through
+ * peer-mapped buffers (CUDA IPC over NVLink), owner CTAs publish the next t to
+ * every rank, and one system-scope barrier separates the passes -- the
+ * allreduce of R^T s and of the objective is fused into the kernel.
+ * Protocol (all ranks):
+ *   1. sc_shard_open(ctx, cfg, handle)   allocate + export this rank's buffers
+ *   2. all-gather the world handles      (e.g. torch.distributed)
+ *   3. sc_shard_connect(ctx, handles)    map the peers (world * 64 bytes)
+ *   4. per decomposition: sc_shard_reset on every rank, a host barrier, then
+ *      sc_greedy_decompose_sharded on every rank concurrently.
+ * Results: sign_words[0] = this rank's row signs (local rows, bit 0 = row0),
+ * sign_words[1] = t, coefficients and curve identical on all ranks. */
+#define SC_IPC_HANDLE_BYTES 64
+typedef struct sc_shard_config {
+  int32_t rank, world;
+  uint64_t m_global; /* rows of the whole matrix */
+  uint64_t row0;     /* first global row of this rank's band */
+  uint64_t n;        /* columns */
+  int32_t dtype;     /* sc_dtype */
+  int32_t ctas;      /* CTAs per rank, identical on all ranks; 0 = min(SMs, m_global / world) */
+} sc_shard_config;
+
+sc_status sc_shard_open(sc_ctx* ctx, const sc_shard_config* cfg, void* handle_out);
+sc_status sc_shard_connect(sc_ctx* ctx, const void* handles);
+sc_status sc_shard_reset(sc_ctx* ctx);
+sc_status sc_greedy_decompose_sharded(sc_ctx* ctx, const sc_problem* local, const sc_shard_config* cfg,
+                                      sc_result* result);
+void sc_shard_close(sc_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

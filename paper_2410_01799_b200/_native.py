@@ -60,6 +60,20 @@ class ScResult(C.Structure):
     ]
 
 
+class ScShardConfig(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int32),
+        ("world", C.c_int32),
+        ("m_global", u64),
+        ("row0", u64),
+        ("n", u64),
+        ("dtype", C.c_int32),
+        ("ctas", C.c_int32),
+    ]
+
+
+SC_IPC_HANDLE_BYTES = 64
+
 # every symbol the header declares, with its ctypes signature
 SIGNATURES = {
     "sc_version": (C.c_char_p, []),
@@ -74,6 +88,11 @@ SIGNATURES = {
     "sc_fill_normal_f32": (None, [u64, u64, P(C.c_float)]),
     "sc_width_for_compression": (u64, [C.c_int, C.c_int, C.c_int, P(u64), C.c_double]),
     "sc_lpt_schedule": (None, [P(C.c_double), u64, C.c_uint32, P(C.c_uint32)]),
+    "sc_shard_open": (C.c_int, [C.c_void_p, P(ScShardConfig), C.c_void_p]),
+    "sc_shard_connect": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sc_shard_reset": (C.c_int, [C.c_void_p]),
+    "sc_greedy_decompose_sharded": (C.c_int, [C.c_void_p, P(ScProblem), P(ScShardConfig), P(ScResult)]),
+    "sc_shard_close": (None, [C.c_void_p]),
 }
 
 _lib = None

@@ -173,7 +173,7 @@ class Engine:
 
     # -- core call -----------------------------------------------------------
     def run(self, a, cfg: DecomposeConfig, *, dtype: Optional[str] = None, seed_mode: int = N.SC_SEED_PER_TERM,
-            want_remainder: bool = False):
+            want_remainder: bool = False, shard=None):
         """Runs the device decomposition; returns (CutDecomposition, CutReport, remainder|None).
 
         ``a`` is a numpy array (host path) or a CUDA torch tensor (device path,
@@ -237,10 +237,13 @@ class Engine:
         res.resid_norm_exact = rne.ctypes.data_as(C.POINTER(C.c_double))
         res.sweeps = sweeps.ctypes.data_as(C.POINTER(C.c_uint32))
         res.remainder = rem.ctypes.data if rem is not None else None
-        self._check(self.lib.sc_greedy_decompose(self.handle, C.byref(prob), C.byref(res)))
+        if shard is None:
+            self._check(self.lib.sc_greedy_decompose(self.handle, C.byref(prob), C.byref(res)))
+        else:  # this rank's band of a row-sharded matrix (sharded.py)
+            self._check(self.lib.sc_greedy_decompose_sharded(self.handle, C.byref(prob), C.byref(shard), C.byref(res)))
         del keep
         wd = int(res.width_done)
-        numel = float(np.prod([float(d) for d in shape]))
+        numel = float(np.prod([float(d) for d in shape])) if shard is None else float(shard.m_global) * shape[1]
         bits_per_term = 64 + sum(int(d) for d in shape)
         steps = []
         if cfg.record_curve:

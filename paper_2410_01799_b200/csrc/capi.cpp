@@ -35,6 +35,17 @@ struct sc_ctx {
   size_t arena_bytes = 0;
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // row-sharded mode (sc_shard_*): this rank's exchange region and the peers'
+  struct Shard {
+    int world = 0, rank = 0, G = 0, dtype = 0;
+    long long pitch = 0;
+    int tw32 = 0;
+    uint64_t m_global = 0, row0 = 0, n = 0;
+    void* exch = nullptr;
+    size_t exch_bytes = 0, off_zpart = 0, off_slots = 0, off_tb64 = 0, off_ctr = 0;
+    void* peers[8] = {};
+    bool connected = false;
+  } shard;
 };
 
 namespace {
@@ -165,6 +176,7 @@ sc_status sc_create(sc_ctx** out, int device) {
 
 void sc_destroy(sc_ctx* ctx) {
   if (!ctx) return;
+  sc_shard_close(ctx);
   cudaSetDevice(ctx->device);
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -232,7 +244,16 @@ void sc_lpt_schedule(const double* costs, uint64_t count, uint32_t bins, uint32_
   }
 }
 
+namespace {
+sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc_ctx::Shard* sh);
+}
+
 sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) {
+  return run_decompose(ctx, p, res, nullptr);
+}
+
+namespace {
+sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc_ctx::Shard* sh) {
   const auto t_start = std::chrono::steady_clock::now();
   if (ctx == nullptr) return SC_INVALID_ARGUMENT;
   if (res == nullptr) return set_err(ctx, SC_INVALID_ARGUMENT, "sc_result: null");
@@ -277,7 +298,9 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   // wide rows: column chunks of one warp-tile pass (var.nw * 32 * var.vpt vectors)
   const long long tile_cols = static_cast<long long>(var.nw) * 32 * var.vpt * (dt == SC_F32 ? 4 : 2);
   const int cpr = pitch > tile_cols ? static_cast<int>((pitch + tile_cols - 1) / tile_cols) : 1;
-  const int G = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(ctx->num_sms) * var.cps, m));
+  if (sh && (tensor || var.cps != 1 || static_cast<uint64_t>(sh->G) > m))
+    return set_err(ctx, SC_NOT_SUPPORTED, "row sharding: matrices only, one CTA per SM, band >= %d rows", sh ? sh->G : 0);
+  const int G = sh ? sh->G : static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(ctx->num_sms) * var.cps, m));
   const int rows_base = static_cast<int>(m / G), rows_rem = static_cast<int>(m % G);
   const int rows_max = rows_base + (rows_rem ? 1 : 0);
   const int Q = static_cast<int>(pitch / 32);
@@ -338,9 +361,20 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   void* dR = carve<char>(cur, m * rowB);
   double* zpart = carve<double>(cur, 2 * static_cast<size_t>(G) * pitch);  // [2][G][pitch] by pass parity
   scb::Slot* slots = carve<scb::Slot>(cur, G);
-  unsigned* ctr = carve<unsigned>(cur, 8);  // [1..3] err_pass
+  unsigned* ctr = carve<unsigned>(cur, 8);  // [0] grid barrier, [1..3] err_pass
   unsigned long long* stats = carve<unsigned long long>(cur, 4);
   unsigned long long* tb64 = carve<unsigned long long>(cur, 2 * static_cast<size_t>(tw32));
+  unsigned* ctr_g = ctr;  // the grid's barrier / error words (rank 0's when sharded)
+  if (sh) {  // exchange buffers live in the peer-mapped shard region (reset by sc_shard_reset)
+    if (sh->pitch != pitch || sh->dtype != dt || sh->n != n)
+      return set_err(ctx, SC_INVALID_ARGUMENT, "sc_greedy_decompose_sharded: problem does not match the shard");
+    char* ex = static_cast<char*>(sh->exch);
+    zpart = reinterpret_cast<double*>(ex + sh->off_zpart);
+    slots = reinterpret_cast<scb::Slot*>(ex + sh->off_slots);
+    tb64 = reinterpret_cast<unsigned long long*>(ex + sh->off_tb64);
+    ctr = reinterpret_cast<unsigned*>(ex + sh->off_ctr);
+    ctr_g = reinterpret_cast<unsigned*>(static_cast<char*>(sh->peers[0]) + sh->off_ctr);
+  }
   uint32_t* tbest = carve<uint32_t>(cur, tw32);
   uint64_t* t0 = carve<uint64_t>(cur, nstart * wn);
   uint64_t* S_out = carve<uint64_t>(cur, std::max<uint64_t>(w, 1) * wm);
@@ -364,8 +398,12 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   uint64_t* ht0 = static_cast<uint64_t*>(ctx->pinned);
   uint64_t* hax0 = ht0 + nstart * wn;
   if (!tensor) {
+    // sharded: the draw of s0 skips the words of the GLOBAL row count
+    sc_problem pg = *p;
+    uint64_t gshape[2] = {sh ? sh->m_global : m, n};
+    pg.shape = gshape;
     for (uint64_t term = 0; term < w; ++term)
-      for (uint64_t r = 0; r < p->restarts; ++r) start_vectors(p, term, r, ht0 + (term * p->restarts + r) * wn);
+      for (uint64_t r = 0; r < p->restarts; ++r) start_vectors(&pg, term, r, ht0 + (term * p->restarts + r) * wn);
   } else {
     // all k axes drawn in axis order (search.hpp:197); s_0 is recomputed first,
     // the trailing axes seed the axial step and form the first t = kron(s_1..s_{k-1})
@@ -404,10 +442,12 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
       h2d += ax0_bytes;
     }
   }
-  SC_CUDA(ctx, cudaMemsetAsync(ctr, 0, 4, st));
-  SC_CUDA(ctx, cudaMemsetAsync(ctr + 1, 0xff, 12, st));
-  SC_CUDA(ctx, cudaMemsetAsync(slots, 0, static_cast<size_t>(G) * sizeof(scb::Slot), st));
-  SC_CUDA(ctx, cudaMemsetAsync(tb64, 0, 2 * static_cast<size_t>(tw32) * 8, st));
+  if (!sh) {
+    SC_CUDA(ctx, cudaMemsetAsync(ctr, 0, 4, st));
+    SC_CUDA(ctx, cudaMemsetAsync(ctr + 1, 0xff, 12, st));
+    SC_CUDA(ctx, cudaMemsetAsync(slots, 0, static_cast<size_t>(G) * sizeof(scb::Slot), st));
+    SC_CUDA(ctx, cudaMemsetAsync(tb64, 0, 2 * static_cast<size_t>(tw32) * 8, st));
+  }
   SC_CUDA(ctx, cudaMemsetAsync(tbest, 0, static_cast<size_t>(tw32) * 4, st));
   SC_CUDA(ctx, cudaMemsetAsync(stats, 0, 32, st));
   if (w > 0) SC_CUDA(ctx, cudaMemsetAsync(S_out, 0, w * wm * 8, st));
@@ -432,8 +472,8 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   kp.tbest = tbest;
   kp.zpart = zpart;
   kp.slots = slots;
-  kp.bar = ctr;
-  kp.err_pass = ctr + 1;
+  kp.bar = ctr_g;
+  kp.err_pass = ctr_g + 1;
   kp.S_out = reinterpret_cast<uint32_t*>(S_out);
   kp.s_stride = s_stride;
   kp.T_out = reinterpret_cast<uint32_t*>(T_out);
@@ -446,7 +486,7 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   kp.restarts = static_cast<long long>(p->restarts);
   kp.max_sweeps = static_cast<long long>(std::min<uint64_t>(p->max_sweeps, 1ull << 40));
   kp.min_frac = p->min_value_fraction;
-  kp.numel_d = static_cast<double>(m * n);
+  kp.numel_d = static_cast<double>((sh ? sh->m_global : m) * n);
   kp.widen_mul = 1 << 29;
   kp.tensor = tensor ? 1 : 0;
   kp.kax = tensor ? kax : 0;
@@ -460,6 +500,15 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   kp.zfull = zfull;
   kp.two_phase = cpr > 1 ? 1 : static_cast<int>(env_size("SCB_2PH", 1));  // SCB_2PH=0: fused single-read pass
   kp.cpr = cpr;
+  kp.world = sh ? sh->world : 1;
+  kp.rank = sh ? sh->rank : 0;
+  kp.GT = G * kp.world;
+  for (int r = 0; r < kp.world; ++r) {
+    char* ex = sh ? static_cast<char*>(sh->peers[r]) : nullptr;
+    kp.zpart_pe[r] = sh ? reinterpret_cast<double*>(ex + sh->off_zpart) : zpart;
+    kp.slots_pe[r] = sh ? reinterpret_cast<scb::Slot*>(ex + sh->off_slots) : slots;
+    kp.tb64_pe[r] = sh ? reinterpret_cast<unsigned long long*>(ex + sh->off_tb64) : tb64;
+  }
   kp.chunk_cols = cpr > 1 ? static_cast<int>(tile_cols) : static_cast<int>(pitch);
 
   const bool prof = std::getenv("SCB_PROF") != nullptr;
@@ -478,7 +527,7 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   unsigned h_ctr[4];
   unsigned long long h_stats[4];
   std::vector<double> h_norm2(w + 1);
-  SC_CUDA(ctx, cudaMemcpyAsync(h_ctr, ctr, 16, cudaMemcpyDeviceToHost, st));
+  SC_CUDA(ctx, cudaMemcpyAsync(h_ctr, ctr_g, 16, cudaMemcpyDeviceToHost, st));
   SC_CUDA(ctx, cudaMemcpyAsync(h_stats, stats, 32, cudaMemcpyDeviceToHost, st));
   SC_CUDA(ctx, cudaMemcpyAsync(h_norm2.data(), norm2, (w + 1) * 8, cudaMemcpyDeviceToHost, st));
   SC_CUDA(ctx, cudaStreamSynchronize(st));
@@ -558,6 +607,90 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
   res->total_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   return SC_OK;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Row-sharded decomposition of one matrix over `world` GPUs.
+sc_status sc_shard_open(sc_ctx* ctx, const sc_shard_config* cfg, void* handle_out) {
+  if (!ctx || !cfg || !handle_out) return SC_INVALID_ARGUMENT;
+  if (cfg->world < 1 || cfg->world > 8 || cfg->rank < 0 || cfg->rank >= cfg->world || cfg->n == 0 ||
+      cfg->m_global < static_cast<uint64_t>(cfg->world) || (cfg->dtype != SC_F32 && cfg->dtype != SC_F64))
+    return set_err(ctx, SC_INVALID_ARGUMENT, "sc_shard_config: bad rank/world/shape/dtype");
+  SC_CUDA(ctx, cudaSetDevice(ctx->device));
+  sc_shard_close(ctx);
+  auto& S = ctx->shard;
+  S.world = cfg->world;
+  S.rank = cfg->rank;
+  S.dtype = cfg->dtype;
+  S.m_global = cfg->m_global;
+  S.row0 = cfg->row0;
+  S.n = cfg->n;
+  S.pitch = static_cast<long long>((cfg->n + 31) / 32 * 32);
+  const uint64_t min_band = cfg->m_global / cfg->world;  // bands are floor/ceil of m/world
+  S.G = cfg->ctas > 0 ? cfg->ctas : static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(ctx->num_sms), min_band));
+  const int Q = static_cast<int>(S.pitch / 32);
+  S.tw32 = std::max(Q, static_cast<int>(2 * words64(cfg->n)));
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  S.off_zpart = 0;
+  S.off_slots = al(2 * static_cast<size_t>(S.G) * S.pitch * 8);
+  S.off_tb64 = S.off_slots + al(static_cast<size_t>(S.G) * sizeof(scb::Slot));
+  S.off_ctr = S.off_tb64 + al(2 * static_cast<size_t>(S.tw32) * 8);
+  S.exch_bytes = S.off_ctr + 256;
+  SC_CUDA(ctx, cudaMalloc(&S.exch, S.exch_bytes));
+  cudaIpcMemHandle_t h;
+  SC_CUDA(ctx, cudaIpcGetMemHandle(&h, S.exch));
+  std::memcpy(handle_out, &h, sizeof h);
+  S.peers[S.rank] = S.exch;
+  return sc_shard_reset(ctx);
+}
+
+sc_status sc_shard_connect(sc_ctx* ctx, const void* handles) {
+  if (!ctx || !handles || !ctx->shard.exch) return SC_INVALID_ARGUMENT;
+  SC_CUDA(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->shard;
+  for (int r = 0; r < S.world; ++r) {
+    if (r == S.rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + r * SC_IPC_HANDLE_BYTES, sizeof h);
+    SC_CUDA(ctx, cudaIpcOpenMemHandle(&S.peers[r], h, cudaIpcMemLazyEnablePeerAccess));
+  }
+  S.connected = true;
+  return SC_OK;
+}
+
+sc_status sc_shard_reset(sc_ctx* ctx) {
+  if (!ctx || !ctx->shard.exch) return SC_INVALID_ARGUMENT;
+  SC_CUDA(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->shard;
+  char* ex = static_cast<char*>(S.exch);
+  SC_CUDA(ctx, cudaMemset(ex + S.off_slots, 0, S.off_ctr - S.off_slots));  // slots + tagged t words
+  SC_CUDA(ctx, cudaMemset(ex + S.off_ctr, 0, 4));                          // grid barrier counter
+  SC_CUDA(ctx, cudaMemset(ex + S.off_ctr + 4, 0xff, 12));                  // no error seen
+  SC_CUDA(ctx, cudaDeviceSynchronize());
+  return SC_OK;
+}
+
+sc_status sc_greedy_decompose_sharded(sc_ctx* ctx, const sc_problem* local, const sc_shard_config* cfg,
+                                      sc_result* res) {
+  if (!ctx || !local || !cfg || !res) return SC_INVALID_ARGUMENT;
+  const auto& S = ctx->shard;
+  if (!S.exch || !(S.connected || S.world == 1))
+    return set_err(ctx, SC_INVALID_ARGUMENT, "sc_greedy_decompose_sharded: sc_shard_open/connect first");
+  if (local->order != 2 || cfg->rank != S.rank || cfg->world != S.world || cfg->m_global != S.m_global ||
+      cfg->n != S.n || local->shape[1] != S.n)
+    return set_err(ctx, SC_INVALID_ARGUMENT, "sc_greedy_decompose_sharded: problem/config do not match the shard");
+  return run_decompose(ctx, local, res, &S);
+}
+
+void sc_shard_close(sc_ctx* ctx) {
+  if (!ctx) return;
+  auto& S = ctx->shard;
+  cudaSetDevice(ctx->device);
+  for (int r = 0; r < 8; ++r)
+    if (S.peers[r] && r != S.rank) cudaIpcCloseMemHandle(S.peers[r]);
+  if (S.exch) cudaFree(S.exch);
+  S = sc_ctx::Shard{};
 }
 
 }  // extern "C"

@@ -110,10 +110,30 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   }
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
+// the same across GPUs: the counter lives on rank 0, peers reach it over NVLink
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier_sys(unsigned* bar, unsigned target) {
+  asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+  while (static_cast<int>(ld_relaxed_sys(bar) - target) < 0) {
+  }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
 __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed64_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -1270,26 +1290,33 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   auto col_reduce = [&](bool zmode, int P) {
     unsigned long long* tout = p.tb64 + static_cast<size_t>(ctl->tsel & 1) * p.Q;
     const unsigned long long tag = static_cast<unsigned long long>(P + 1) << 32;
-    const int gs = (warp * G) / CW, ge = ((warp + 1) * G) / CW;
-    for (int q0 = g; q0 < p.Q; q0 += G * p.zl) {
+    // owners by global CTA index: the CTAs of all ranks share the column words
+    const int GT = p.GT, gg = p.rank * G + g;
+    const int gs = (warp * GT) / CW, ge = ((warp + 1) * GT) / CW;
+    for (int q0 = gg; q0 < p.Q; q0 += GT * p.zl) {
       int nls = 0;
-      for (int j = 0; j < p.zl && q0 + j * G < p.Q; ++j) nls = j + 1;
+      for (int j = 0; j < p.zl && q0 + j * GT < p.Q; ++j) nls = j + 1;
       for (int j = 0; j < nls; ++j) {
-        const int col = (q0 + j * G) * 32 + lane;
-        const double* zp = p.zpart + static_cast<size_t>(P & 1) * G * pitch + col;  // pass-parity buffer
+        const int col = (q0 + j * GT) * 32 + lane;
+        const size_t par = static_cast<size_t>(P & 1) * G * pitch + col;  // pass-parity buffer
         double a = 0.0;
-        for (int g0 = gs; g0 < ge; g0 += 16) {  // 16 independent L2 loads in flight
-          double v[16];
+        for (int g0 = gs; g0 < ge; g0 += 32) {  // one round of up to 32 L2 loads in flight
+          double v[32];
 #pragma unroll
-          for (int u = 0; u < 16; ++u) v[u] = (g0 + u < ge) ? __ldcg(zp + static_cast<size_t>(g0 + u) * pitch) : 0.0;
+          for (int u = 0; u < 32; ++u) {
+            const int gp = g0 + u;
+            const double* zp = p.world > 1 ? p.zpart_pe[gp / G] + static_cast<size_t>(gp % G) * pitch
+                                           : p.zpart + static_cast<size_t>(gp) * pitch;
+            v[u] = (gp < ge) ? __ldcg(zp + par) : 0.0;
+          }
 #pragma unroll
-          for (int u = 0; u < 16; ++u) a += v[u];
+          for (int u = 0; u < 32; ++u) a += v[u];
         }
         zseg[(j * CW + warp) * 32 + lane] = a;
       }
       consumer_sync(CT);
       for (int j = warp; j < nls; j += CW) {
-        const int qq = q0 + j * G;
+        const int qq = q0 + j * GT;
         const int col = qq * 32 + lane;
         double z = 0.0;
 #pragma unroll
@@ -1300,16 +1327,21 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           if (valid) __stcg(p.zfull + col, z);
         } else {
           const unsigned word = __ballot_sync(0xffffffffu, valid && z < 0.0);
-          if (lane == 0) st_relaxed64(tout + qq, tag | word);
+          if (p.world > 1) {  // every rank stages t from its own copy
+            if (lane < p.world)
+              st_relaxed64_sys(p.tb64_pe[lane] + static_cast<size_t>(ctl->tsel & 1) * p.Q + qq, tag | word);
+          } else if (lane == 0) {
+            st_relaxed64(tout + qq, tag | word);
+          }
         }
       }
       consumer_sync(CT);
     }
-    // Order-k: every CTA reads all of Z next, so the reduction ends in a grid
-    // barrier.  Matrix mode needs none: the next pass polls the pass-tagged t
-    // words, and zpart / slots / tb64 are reused only two passes later, i.e.
-    // after the next pass's grid barrier, which every CTA reaches only after
-    // finishing this reduction.
+    // Order-k (single GPU): every CTA reads all of Z next, so the reduction ends
+    // in a grid barrier.  Matrix mode needs none: the next pass polls the
+    // pass-tagged t words, and zpart / slots / tb64 are reused only two passes
+    // later, i.e. after the next pass's grid barrier, which every CTA reaches
+    // only after finishing this reduction.
     if (zmode) {
       if (tid == 0) grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
       consumer_sync(CT);
@@ -1342,7 +1374,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         for (int i = tid; i < p.Q; i += CT) {
           unsigned long long x;
           do {
-            x = ld_relaxed64(tw + i);
+            x = p.world > 1 ? ld_relaxed64_sys(tw + i) : ld_relaxed64(tw + i);
           } while (static_cast<int>(static_cast<unsigned>(x >> 32) - static_cast<unsigned>(P)) < 0);
           tws[i] = static_cast<uint32_t>(x);
         }
@@ -1496,18 +1528,28 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       }
     }
     consumer_sync(CT);
-    if (tid == 0) grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
+    if (tid == 0) {
+      if (p.world > 1)
+        grid_barrier_sys(p.bar, ++epoch * static_cast<unsigned>(p.GT));
+      else
+        grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
+    }
     consumer_sync(CT);
     {
-      // every CTA reduces the G partials in the same fixed order
+      // every CTA (of every rank) reduces the GT partials in the same fixed order
       double cs = 0.0, ns = 0.0;
-      for (int i = tid; i < G; i += CT) {
-        const Slot* s = p.slots + i;
+      for (int i = tid; i < p.GT; i += CT) {
+        const Slot* s = p.world > 1 ? p.slots_pe[i / G] + (i % G) : p.slots + i;
         cs += __ldcg(&s->c[P & 1]);
         ns += __ldcg(&s->n[P & 1]);
       }
       cs = warp_sum(cs);
       ns = warp_sum(ns);
+      if (tid == 32) {  // error flags for the decision, off thread 0's serial path
+        ctl->err_pre[0] = __ldcg(errp + ERR_Y);
+        ctl->err_pre[1] = __ldcg(errp + ERR_INPUT);
+        ctl->err_pre[2] = __ldcg(errp + ERR_Z);
+      }
       consumer_sync(CT);  // thread 0 is done reading ctl->nred of the norm step
       if (lane == 0) {
         ctl->cred[warp] = cs;
@@ -1588,7 +1630,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       }
       int next;
       int need_reduce = 0;
-      const unsigned ey = __ldcg(errp + ERR_Y), ei = __ldcg(errp + ERR_INPUT), ez = __ldcg(errp + ERR_Z);
+      const unsigned ey = ctl->err_pre[0], ei = ctl->err_pre[1], ez = ctl->err_pre[2];
       if (ey <= static_cast<unsigned>(P) || ei <= static_cast<unsigned>(P) ||
           ez < static_cast<unsigned>(P)) {
         next = K_TERM;

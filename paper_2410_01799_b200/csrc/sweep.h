@@ -43,6 +43,7 @@ struct Ctl {
   int cur, nxt, best, need_reduce, norm_idx, kron_upd;
   double alpha, c_prev, best_c, first_value;
   double ax_c;  // order-k mode: c = <s_{k-1}, v_{k-1}> of the axial step
+  unsigned err_pre[4];  // error flags prefetched after the pass's grid barrier
   double cred[32];
   double nred[32];
 };
@@ -95,6 +96,14 @@ struct KParams {
   // elements (one stage each); cpr == 1, chunk_cols == pitch otherwise
   int cpr;
   int chunk_cols;
+  // Row-sharded multi-GPU (one process per GPU): every rank runs this
+  // kernel on its row band with the same G; the exchange buffers of all ranks are
+  // peer-mapped (CUDA IPC over NVLink) and the CTAs of all ranks form one grid:
+  // global CTA gg = rank * G + g, GT = world * G.  world == 1: the local buffers.
+  int world, rank, GT;
+  double* zpart_pe[8];               // per-rank [2][G][pitch] column partials
+  Slot* slots_pe[8];                 // per-rank [G] slots
+  unsigned long long* tb64_pe[8];    // per-rank [2][Q] tagged t words (owners write all)
   unsigned long long* prof;  // [G][16] clock64 breakdown or nullptr
 };
 

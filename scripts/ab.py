@@ -10,8 +10,12 @@ libs = [os.environ.get("SCB_LIB_A", N.LIB_PATH)] + os.environ["SCB_LIB_B"].split
 a = sc.fill_normal(1, 4096 * 4096, np.float32).reshape(4096, 4096)
 cfg = sc.DecomposeConfig(width=int(os.environ.get("AB_W", 64)), search=sc.SearchConfig(seed=1))
 res = {}
+ALL_SIGS = dict(N.SIGNATURES)
 for rnd in range(int(os.environ.get("AB_ROUNDS", 3))):
     for path in libs:
+        import ctypes
+        probe = ctypes.CDLL(path)
+        N.SIGNATURES = {k: v for k, v in ALL_SIGS.items() if hasattr(probe, k)}  # older builds: fewer symbols
         N._lib = None
         N.LIB_PATH = path
         eng = sc.Engine(0)

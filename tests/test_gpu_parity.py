@@ -329,3 +329,27 @@ def test_order3_wide_trailing_axes(engine, ref):
     for i in range(3):
         assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
     assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F64_TOL
+
+
+# ------------------------------------------------------------ row sharding
+@pytest.mark.parametrize("shape,dtype", [((512, 1000), "f32"), ((300, 777), "f64"), ((200, 9000), "f32")])
+def test_sharded_world1_equals_engine(engine, ref, shape, dtype):
+    """sc_greedy_decompose_sharded with one rank: the peer-memory exchange path
+    (system-scope barrier off, peer tables of size 1) gives bit-identical results."""
+    from paper_2410_01799_b200 import sharded
+
+    m, n = shape
+    a = ref.fill_normal(m * 7 + n, m * n).reshape(m, n)
+    a = a.astype(np.float32) if dtype == "f32" else a
+    cfg = sc.DecomposeConfig(width=6, record_curve=True, search=sc.SearchConfig(seed=5))
+    dec, rep, _ = engine.run(a, cfg, dtype=dtype)
+    se = sharded.ShardedEngine(m, n, dtype, 0, 1, device=0)
+    try:
+        sdec, srep, _ = se.decompose(a, cfg)
+        S = se.gather_signs(sdec)
+    finally:
+        se.close()
+    assert (S == dec.factors[0]).all() and (sdec.factors[1] == dec.factors[1]).all()
+    assert np.array_equal(srep._cut_values, rep._cut_values)
+    assert np.array_equal(srep.sweeps, rep.sweeps)
+    assert srep.final_residual_norm == rep.final_residual_norm
