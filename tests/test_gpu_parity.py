@@ -353,3 +353,27 @@ def test_sharded_world1_equals_engine(engine, ref, shape, dtype):
     assert np.array_equal(srep._cut_values, rep._cut_values)
     assert np.array_equal(srep.sweeps, rep.sweeps)
     assert srep.final_residual_norm == rep.final_residual_norm
+
+
+# ------------------------------------------------- both dot-pass forms stay exact
+@pytest.mark.parametrize("two_phase", ["0", "1"])
+def test_dot_pass_forms_f32_1024_trajectory(engine, ref, monkeypatch, two_phase):
+    """The fused single-read pass (default once R exceeds L2) and the two-phase
+    pass (default while R is L2-resident), forced on the same C1-shaped input."""
+    monkeypatch.setenv("SCB_2PH", two_phase)
+    a = ref.fill_normal(0, 1024 * 1024).reshape(1024, 1024).astype(np.float32)
+    dec, rep, _ = run(engine, a, 48, seed=0, dtype="f32")
+    od = ref.greedy_decompose(a.astype(np.float64), 48, seed=0)
+    assert (dec.factors[0] == od.signs[0]).all() and (dec.factors[1] == od.signs[1]).all()
+    assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F32_TOL
+    assert sweeps_ok(rep.sweeps, od.iterations)
+
+
+def test_fused_pass_default_beyond_l2(engine, ref):
+    """A matrix larger than the L2 budget takes the fused pass by default."""
+    m, n = 6200, 4096  # 101 MB f32
+    a = (ref.fill_normal(5, m * n).reshape(m, n)).astype(np.float32)
+    dec, rep, _ = run(engine, a, 3, seed=2, dtype="f32")
+    od = ref.greedy_decompose(a.astype(np.float64), 3, seed=2)
+    assert (dec.factors[0] == od.signs[0]).all() and (dec.factors[1] == od.signs[1]).all()
+    assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F32_TOL
