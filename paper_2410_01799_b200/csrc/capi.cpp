@@ -349,7 +349,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
                       (((w + 1) * 8 + 255) & ~size_t(255)) + 8 * 256 + 4096 +
                       ((nstart * axw64 * 8 + 255) & ~size_t(255)) +
                       ((std::max<uint64_t>(w, 1) * axw64 * 8 + 255) & ~size_t(255)) +
-                      ((static_cast<size_t>(pitch) * 8 + 255) & ~size_t(255));
+                      2 * ((static_cast<size_t>(pitch) * 8 + 255) & ~size_t(255));
   if (need > ctx->arena_bytes) {
     if (ctx->arena) cudaFree(ctx->arena);
     ctx->arena = nullptr;
@@ -385,6 +385,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   uint64_t* ax0 = carve<uint64_t>(cur, std::max<uint64_t>(nstart * axw64, 1));
   uint64_t* AX_out = carve<uint64_t>(cur, std::max<uint64_t>(std::max<uint64_t>(w, 1) * axw64, 1));
   double* zfull = carve<double>(cur, static_cast<size_t>(pitch));
+  double* zstate = carve<double>(cur, static_cast<size_t>(pitch));
 
   // ---- host staging (pinned) for the start vectors ----
   const size_t t0_bytes = nstart * wn * 8, ax0_bytes = nstart * axw64 * 8;
@@ -498,6 +499,8 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   kp.ax0 = reinterpret_cast<const uint32_t*>(ax0);
   kp.AX_out = reinterpret_cast<uint32_t*>(AX_out);
   kp.zfull = zfull;
+  kp.zstate = zstate;
+  kp.delta = tensor ? 0 : static_cast<int>(env_size("SCB_DELTA", 1));
   // Dot-pass form: the two-phase pass reads R twice per sweep but has no per-row
   // serial chain -- the better choice while R stays in SMEM / L2; once R spills
   // to HBM the fused single-read pass wins (14336x4096 f32: 77.6 vs 84 us/pass).

@@ -1005,6 +1005,121 @@ __device__ __noinline__ void dot_pass_chunked(const DotArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Sparse delta dot pass (the GPU form of the reference's delta caches,
+// kernels.hpp:92-156 / search.hpp:145-186): with y = R t and z = R^T s kept from
+// the previous pass, only the columns whose t flipped and the rows whose s flips
+// are read --
+//   y_j += 2 sum_{c: t flipped} t'_c R[j,c]   (gather; lanes walk the t-XOR words)
+//   s'  = sgn(y)
+//   dz  = 2 sum_{j: s flipped} s'_j R[j,:]    (this CTA's rows; owners add it to z)
+// No rows are streamed.  Dense passes refresh y and z (restart/term start, every
+// 16th sweep, or when many columns flipped), bounding the drift of the caches.
+struct DeltaArgs {
+  unsigned res, yrow, s_cur, s_nxt, tws, txor;
+  const void* Rrows;  // global row 0 of this CTA's band
+  double* zrow;       // this CTA's z partial row of this pass
+  unsigned* errp;
+  int* has_dz;
+  long long pitch;
+  unsigned rowB;
+  int rows_g, nres, Q, NV, P;
+};
+
+template <typename E, int NW, int VPT>
+__device__ __noinline__ void delta_pass(const DeltaArgs a) {
+  using VT = typename Vec<E>::T;
+  constexpr int EPV = Vec<E>::N;
+  constexpr int NE = VPT * EPV;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows_g = a.rows_g, nres = a.nres, Q = a.Q, NV = a.NV, P = a.P;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* yrow = reinterpret_cast<double*>(smem + a.yrow);
+  const uint32_t* s_cur = reinterpret_cast<const uint32_t*>(smem + a.s_cur);
+  uint32_t* s_nxt = reinterpret_cast<uint32_t*>(smem + a.s_nxt);
+  const uint32_t* tws = reinterpret_cast<const uint32_t*>(smem + a.tws);
+  const uint32_t* txor = reinterpret_cast<const uint32_t*>(smem + a.txor);
+  const E* Rg = static_cast<const E*>(a.Rrows);
+  auto row_ptr = [&](int j) -> const E* {
+    return j < nres ? reinterpret_cast<const E*>(smem + a.res + static_cast<size_t>(j) * a.rowB)
+                    : Rg + static_cast<size_t>(j) * a.pitch;
+  };
+  auto elem = [&](const E* row, int j, int c) -> double {  // R may have been rewritten this launch: no __ldg
+    return j < nres ? static_cast<double>(row[c]) : static_cast<double>(__ldcg(row + c));
+  };
+  // ---- y update: one warp per row, lanes over the t-XOR words (fixed order) ----
+  for (int j = warp; j < rows_g; j += NW) {
+    const E* row = row_ptr(j);
+    double acc = 0.0;
+    for (int w = lane; w < Q; w += 32) {
+      uint32_t x = txor[w];
+      const uint32_t tn = tws[w];
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        const double v = elem(row, j, w * 32 + b);
+        acc += ((tn >> b) & 1u) ? -v : v;
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) yrow[j] += 2.0 * acc;
+  }
+  consumer_sync(NW * 32);
+  // ---- s' = sgn(y) ----
+  for (int jb = 0; jb < rows_g; jb += NW * 32) {
+    const int jj = jb + tid;
+    const bool ok = jj < rows_g;
+    const double y = ok ? yrow[jj] : 0.0;
+    if (ok && !isfinite(y)) atomicMin(a.errp + ERR_Y, static_cast<unsigned>(P));
+    const unsigned word = __ballot_sync(0xffffffffu, ok && y < 0.0);
+    if (lane == 0 && jb + warp * 32 < rows_g) s_nxt[(jb >> 5) + warp] = word;
+  }
+  consumer_sync(NW * 32);
+  // ---- dz over the rows whose sign flipped (ascending rows) ----
+  int vidx[VPT];
+  bool vok[VPT];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int v = (k * NW + warp) * 32 + lane;
+    vok[k] = v < NV;
+    vidx[k] = vok[k] ? v : 0;
+  }
+  double zacc[NE];
+#pragma unroll
+  for (int i = 0; i < NE; ++i) zacc[i] = 0.0;
+  bool any = false;
+  const int sw = (rows_g + 31) / 32;
+  for (int w = 0; w < sw; ++w) {
+    uint32_t f = s_nxt[w] ^ s_cur[w];
+    if (w == sw - 1 && (rows_g & 31)) f &= (1u << (rows_g & 31)) - 1u;
+    while (f) {
+      const int j = w * 32 + __ffs(f) - 1;
+      f &= f - 1;
+      any = true;
+      const double g = ((s_nxt[j >> 5] >> (j & 31)) & 1u) ? -2.0 : 2.0;
+      const VT* rv = reinterpret_cast<const VT*>(row_ptr(j));
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        E x[EPV];
+        Vec<E>::split(j < nres ? rv[vidx[k]] : __ldcg(rv + vidx[k]), x);
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) zacc[k * EPV + e] = fma(static_cast<double>(x[e]), g, zacc[k * EPV + e]);
+      }
+    }
+  }
+  if (any) {  // uniform across the CTA (every thread walks the same bits)
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      if (vok[k]) {
+#pragma unroll
+        for (int e = 0; e < EPV; e += 2)
+          __stcg(reinterpret_cast<double2*>(a.zrow + vidx[k] * EPV + e), make_double2(zacc[k * EPV + e], zacc[k * EPV + e + 1]));
+      }
+    }
+  }
+  if (tid == 0) *a.has_dz = any ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
 // Order-k tensors (axial_run, search.hpp:191-213) on the matrix view
 // M = n_0 x N', N' = n_1 ... n_{k-1} (row-major, last axis fastest).  Axis 0 of
 // a sweep is the dot pass (y = M kron(s_1..s_{k-1}), s_0 = sgn(y)); its column
@@ -1149,6 +1264,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   uint32_t* uws = reinterpret_cast<uint32_t*>(smem + L.uws);               // [Q] t of the update
   double* zseg = reinterpret_cast<double*>(smem + L.zseg);                 // [zl][CW][32]
   uint32_t* sb = reinterpret_cast<uint32_t*>(smem + L.sb);                 // [3][sw]
+  uint32_t* txor = reinterpret_cast<uint32_t*>(smem + L.txor);             // [Q] t ^ previous t
+  uint32_t* tprev = txor + p.Q;                                            // [Q] previous pass's t
+  uint32_t* dzmask = reinterpret_cast<uint32_t*>(smem + L.dzmask);         // [64] CTAs with a dz partial
+  double* ybak = reinterpret_cast<double*>(smem + L.ybak);                 // [rows_max] cached y
   uint32_t* sax = reinterpret_cast<uint32_t*>(smem + L.ax);                // [axw] axes 1..k-1 (order-k)
   uint32_t* sax_best = sax + p.axw;                                        // [axw] best restart's
   E* R = static_cast<E*>(p.R);
@@ -1168,6 +1287,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     ctl->abort = 0;
     ctl->pp = p.tensor ? 1 : 0;  // order-k: pp = sweep of the current pass (1-based)
     ctl->kron_upd = 0;
+    ctl->nflip = 0;
+    ctl->since_dense = 0;
+    ctl->has_dz = 0;
+    ctl->keep = 0;
     ctl->term = 0;
     ctl->restart = 0;
     ctl->tsel = -1;
@@ -1221,7 +1344,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         // the two-phase dot pass reads the streamed rows twice (y, then z); wide
         // rows go as column chunks, chunk-major in dot passes, row-major otherwise
         const bool dotp = (kind & F_DOT) && p.two_phase;
-        const int reps = dotp ? 2 : 1;
+        const int reps = (kind & F_DELTA) ? 0 : (dotp ? 2 : 1);  // delta passes stream nothing
         for (int rep = 0; rep < reps; ++rep) {
           int row = 0, chunk = 0;  // piece cursor: chunk-major in dot passes, row-major otherwise
           for (int idx = 0; idx < npieces; ++idx, ++q) {
@@ -1287,7 +1410,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   // Owner CTAs sum the G column partials of their 32-column words in a fixed
   // order; matrix mode publishes sgn(z) as tagged t words, order-k mode stores
   // z itself.  Ends with a grid barrier.
-  auto col_reduce = [&](bool zmode, int P) {
+  auto col_reduce = [&](bool zmode, int P, bool delta) {
     unsigned long long* tout = p.tb64 + static_cast<size_t>(ctl->tsel & 1) * p.Q;
     const unsigned long long tag = static_cast<unsigned long long>(P + 1) << 32;
     // owners by global CTA index: the CTAs of all ranks share the column words
@@ -1307,7 +1430,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
             const int gp = g0 + u;
             const double* zp = p.world > 1 ? p.zpart_pe[gp / G] + static_cast<size_t>(gp % G) * pitch
                                            : p.zpart + static_cast<size_t>(gp) * pitch;
-            v[u] = (gp < ge) ? __ldcg(zp + par) : 0.0;
+            const bool take = gp < ge && (!delta || ((dzmask[gp >> 5] >> (gp & 31)) & 1u));
+            v[u] = take ? __ldcg(zp + par) : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < 32; ++u) a += v[u];
@@ -1322,6 +1446,13 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
 #pragma unroll
         for (int w = 0; w < CW; ++w) z += zseg[(j * CW + w) * 32 + lane];
         const bool valid = col < p.n;
+        if (!zmode && p.delta && valid) {  // z state for delta passes: dense sets it, delta adds to it
+          if (ctl->keep && !delta)
+            z = __ldcg(p.zstate + col);  // fixed point: z as cached
+          else if (delta)
+            z = __ldcg(p.zstate + col) + z;
+          __stcg(p.zstate + col, z);
+        }
         if (valid && !isfinite(z)) atomicMin(const_cast<unsigned*>(errp) + ERR_Z, static_cast<unsigned>(P));
         if (zmode) {  // order-k: Z = M^T s_0 for the axial step
           if (valid) __stcg(p.zfull + col, z);
@@ -1379,6 +1510,17 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           tws[i] = static_cast<uint32_t>(x);
         }
       }
+      if (!p.tensor) {  // t flips since the previous pass (delta passes), counted exactly
+        int nf = 0;
+        for (int i = tid; i < p.Q; i += CT) {
+          const uint32_t x = tws[i] ^ tprev[i];
+          txor[i] = x;
+          tprev[i] = tws[i];
+          nf += __popc(x);
+        }
+        if (nf) atomicAdd(&ctl->nflip, nf);
+        if (tid < 64) dzmask[tid] = 0u;
+      }
       if (tid == 0)
         for (int i = 0; i < p.sw; ++i) s_nxt[i] = 0u;
     }
@@ -1389,6 +1531,13 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     }
     consumer_sync(CT);
     if (prof && tid == 0) pacc[5] += clock64() - t_pass0;
+    // A sweep whose t equals the previous pass's t is a fixed point of the cached
+    // products: y, s' and z stay exactly as cached whatever pass form runs, so a
+    // dense refresh can never nudge c by rounding there (the reference's caches
+    // behave the same way outside its 16-sweep refreshes).
+    const bool keep = (kind & F_DOT) && !p.tensor && p.delta && pp >= 1 && ctl->nflip == 0;
+    if (keep && !(kind & F_DELTA))
+      for (int j = tid; j < rows_g; j += CT) ybak[j] = yrow[j];
 
     double nacc = 0.0;
     bool bad = false;
@@ -1422,7 +1571,27 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       da.prof = prof ? prof + g * 16 + 8 : nullptr;
       da.cpr = p.cpr;
       da.chunk_cols = p.chunk_cols;
-      if (p.cpr > 1) {
+      if (kind & F_DELTA) {
+        DeltaArgs dl;
+        dl.res = static_cast<unsigned>(L.res);
+        dl.yrow = static_cast<unsigned>(L.yrow);
+        dl.s_cur = static_cast<unsigned>(reinterpret_cast<const unsigned char*>(s_cur) - smem);
+        dl.s_nxt = da.s_nxt;
+        dl.tws = static_cast<unsigned>(L.tws);
+        dl.txor = static_cast<unsigned>(L.txor);
+        dl.Rrows = R + static_cast<size_t>(r0) * pitch;
+        dl.zrow = da.zrow;
+        dl.errp = da.errp;
+        dl.has_dz = &ctl->has_dz;
+        dl.pitch = pitch;
+        dl.rowB = static_cast<unsigned>(rowB);
+        dl.rows_g = rows_g;
+        dl.nres = nres;
+        dl.Q = p.Q;
+        dl.NV = NV;
+        dl.P = P;
+        delta_pass<E, NW, VPT>(dl);
+      } else if (p.cpr > 1) {
         da.rowB = static_cast<unsigned>(stageB);
         dot_pass_chunked<E, NW, VPT>(da);
       } else if (p.two_phase) {
@@ -1430,6 +1599,12 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       } else {
         dot_pass<E, NW, VPT, RG, CPS>(da);
       }
+      if (keep && !(kind & F_DELTA)) {  // fixed point reached through a dense pass: keep the cache
+        consumer_sync(CT);
+        for (int j = tid; j < rows_g; j += CT) yrow[j] = ybak[j];
+        for (int i = tid; i < p.sw; i += CT) s_nxt[i] = s_cur[i];
+      }
+      if (tid == 0) ctl->keep = keep;
       const int ngroups = (rows_g + RG - 1) / RG;
       gcount += static_cast<unsigned>(ngroups);
     } else {
@@ -1486,7 +1661,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       }
     }
     if (D > 0) {  // advance the stage ring past this pass's streamed rows
-      const int t = qs + npieces * (((kind & F_DOT) && p.two_phase) ? 2 : 1);
+      const int t = qs + npieces * ((kind & F_DELTA) ? 0 : (((kind & F_DOT) && p.two_phase) ? 2 : 1));
       qph ^= (t / D) & 1;
       qs = t % D;
     }
@@ -1525,6 +1700,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         Slot* my = p.slots + g;
         __stcg(&my->c[P & 1], cl);
         __stcg(&my->n[P & 1], nsum);
+        __stcg(&my->dz[P & 1], ((kind & F_DELTA) && ctl->has_dz) ? 1.0 : 0.0);
       }
     }
     consumer_sync(CT);
@@ -1542,6 +1718,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         const Slot* s = p.world > 1 ? p.slots_pe[i / G] + (i % G) : p.slots + i;
         cs += __ldcg(&s->c[P & 1]);
         ns += __ldcg(&s->n[P & 1]);
+        if ((kind & F_DELTA) && __ldcg(&s->dz[P & 1]) != 0.0) atomicOr(&dzmask[i >> 5], 1u << (i & 31));
       }
       cs = warp_sum(cs);
       ns = warp_sum(ns);
@@ -1563,7 +1740,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       t_pass0 = t;
     }
     if (p.tensor && (kind & F_DOT)) {  // order-k: Z = M^T s_0, then axes 1..k-1 and c
-      col_reduce(true, P);
+      col_reduce(true, P, false);
       axial_step<CW>(p, sax, tws, ctl, P);
     }
 
@@ -1648,6 +1825,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           ctl->tsel = 1;
           need_reduce = 1;
           next = F_DOT;
+          ctl->since_dense = 0;
         } else {
           // matrix: c = <s_pp, R t_pp> from this pass's y; order-k: c of this sweep's axial step
           const double c = p.tensor ? ctl->ax_c : cs;
@@ -1655,6 +1833,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           if (!stop) {
             ctl->c_prev = c;
             ctl->pp = pp + 1;
+            next = F_DOT;
             if (p.tensor) {
               ctl->tsel = 0;  // next t = kron(new axes), already in tws
             } else {
@@ -1663,8 +1842,15 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
               ctl->nxt = t;
               ctl->tsel = (pp + 1) & 1;
               need_reduce = 1;
+              // delta pass next unless it is time to refresh the caches (every 16th
+              // sweep, as the reference) or many columns flipped last time
+              if (p.delta && ctl->since_dense < 15 && static_cast<long long>(ctl->nflip) * 32 <= p.n) {
+                next |= F_DELTA;
+                ctl->since_dense += 1;
+              } else {
+                ctl->since_dense = 0;
+              }
             }
-            next = F_DOT;
           } else if (p.tensor) {
             // axial_run returns the current sweep's (c, signs) (search.hpp:206, :210)
             const bool better = (ctl->restart == 0) || (c > ctl->best_c);
@@ -1716,6 +1902,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       }
       ctl->kind = next;
       ctl->need_reduce = need_reduce;
+      ctl->nflip = 0;  // recounted at the next staging
       ctl->kind_ring[(P + 1) & 3] = next;
       __threadfence_block();
       ctl->decided = P + 2;
@@ -1734,7 +1921,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     }
 
     // --------------------- column reduction: t' = sgn(z) ---------------------
-    if (!p.tensor && ctl->need_reduce) col_reduce(false, P);
+    if (!p.tensor && ctl->need_reduce) col_reduce(false, P, (kind & F_DELTA) != 0);
   }
   if (tid == 0) ctl->abort = 1;  // release a producer still waiting on an unconsumed stage
   if (prof && tid == 0)

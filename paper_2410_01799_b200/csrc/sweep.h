@@ -16,6 +16,7 @@ enum PassFlags : int {
   F_NORM = 4,    // ||R||_F^2 accumulated (f64)
   F_WB = 8,      // write SMEM-resident rows back to global (end of run)
   F_CHECK = 16,  // reject non-finite input values (first pass)
+  F_DELTA = 32,  // with F_DOT: update the cached y, z from the flipped t columns / s rows only
   K_TERM = 256,  // no more passes
 };
 
@@ -24,8 +25,9 @@ enum ErrSlot : int { ERR_Y = 0, ERR_Z = 1, ERR_INPUT = 2 };
 // Per-CTA scalar partials of a pass, double-buffered by pass parity (a CTA can
 // run at most one pass ahead of the slowest reader).
 struct Slot {
-  double c[2];  // sum_i s_i y_i over the CTA's rows
-  double n[2];  // ||R_rows||^2
+  double c[2];   // sum_i s_i y_i over the CTA's rows
+  double n[2];   // ||R_rows||^2
+  double dz[2];  // delta passes: 1 if this CTA wrote a z partial (some row flipped sign)
 };
 
 constexpr int kMaxStages = 16;
@@ -44,6 +46,10 @@ struct Ctl {
   double alpha, c_prev, best_c, first_value;
   double ax_c;  // order-k mode: c = <s_{k-1}, v_{k-1}> of the axial step
   unsigned err_pre[4];  // error flags prefetched after the pass's grid barrier
+  int nflip;            // columns of t that changed at this pass's staging (all CTAs agree)
+  int since_dense;      // delta passes since the last dense dot pass
+  int has_dz;           // this CTA wrote a z partial in a delta pass
+  int keep;             // t unchanged since the last dot pass: y, s, z stay exactly as cached
   double cred[32];
   double nred[32];
 };
@@ -92,6 +98,8 @@ struct KParams {
   uint32_t* AX_out;    // [width][axw] accepted axis words
   double* zfull;       // [pitch] reduced z (order-k mode)
   int two_phase;       // 1: dot pass as (A) y = R t, (B) z = R^T s' (rows streamed twice)
+  int delta;           // 1: sparse delta passes between dense refreshes (matrix mode)
+  double* zstate;      // [pitch] z = R^T s of the previous pass (owners' columns)
   // wide rows: every row is streamed as cpr column chunks of chunk_cols
   // elements (one stage each); cpr == 1, chunk_cols == pitch otherwise
   int cpr;
@@ -120,7 +128,7 @@ constexpr int kRing = 4;  // dot-partial ring depth (groups)
 
 // Shared-memory carve-up (byte offsets from the dynamic smem base).
 struct Layout {
-  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, ypart, total;
+  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, ypart, txor, dzmask, ybak, total;
 };
 
 inline __host__ __device__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
@@ -153,6 +161,12 @@ inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_r
   o += align16(static_cast<size_t>(2) * axw * 4);
   L.ypart = o;  // [rows_max][nw]: per-warp row partials of the two-phase dot pass
   o += align16(static_cast<size_t>(rows_max) * nw * 8);
+  L.txor = o;  // [2][Q]: t XOR previous t, previous t (delta passes)
+  o += align16(static_cast<size_t>(2) * Q * 4);
+  L.dzmask = o;  // [64]: CTAs (global index) that wrote a z partial in a delta pass
+  o += align16(64 * 4);
+  L.ybak = o;  // [rows_max]: y kept across a sweep whose t did not change
+  o += align16(static_cast<size_t>(rows_max) * 8);
   L.total = o;
   return L;
 }
