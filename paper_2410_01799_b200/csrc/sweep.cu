@@ -1263,6 +1263,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   uint32_t* tws = reinterpret_cast<uint32_t*>(smem + L.tws);               // [Q] t of this pass
   uint32_t* uws = reinterpret_cast<uint32_t*>(smem + L.uws);               // [Q] t of the update
   double* zseg = reinterpret_cast<double*>(smem + L.zseg);                 // [zl][CW][32]
+  double* zst = reinterpret_cast<double*>(smem + L.zst);                   // [zl][32]
   uint32_t* sb = reinterpret_cast<uint32_t*>(smem + L.sb);                 // [3][sw]
   uint32_t* txor = reinterpret_cast<uint32_t*>(smem + L.txor);             // [Q] t ^ previous t
   uint32_t* tprev = txor + p.Q;                                            // [Q] previous pass's t
@@ -1410,8 +1411,12 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   // Owner CTAs sum the G column partials of their 32-column words in a fixed
   // order; matrix mode publishes sgn(z) as tagged t words, order-k mode stores
   // z itself.  Ends with a grid barrier.
-  auto col_reduce = [&](bool zmode, int P, bool delta) {
-    unsigned long long* tout = p.tb64 + static_cast<size_t>(ctl->tsel & 1) * p.Q;
+  // tbuf: the tb64 buffer the next pass reads ((pp + 1) & 1); the decision may
+  // still stop the restart -- then these words are simply never read (the kept
+  // triple's t lives in the other buffer).
+  auto col_reduce = [&](bool zmode, int P, bool delta, int tbuf) {
+    double zsv[4];  // warp 0: z state of its word slices, parked in zst before the combine
+    unsigned long long* tout = p.tb64 + static_cast<size_t>(tbuf) * p.Q;
     const unsigned long long tag = static_cast<unsigned long long>(P + 1) << 32;
     // owners by global CTA index: the CTAs of all ranks share the column words
     const int GT = p.GT, gg = p.rank * G + g;
@@ -1422,6 +1427,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       for (int j = 0; j < nls; ++j) {
         const int col = (q0 + j * GT) * 32 + lane;
         const size_t par = static_cast<size_t>(P & 1) * G * pitch + col;  // pass-parity buffer
+        if (!zmode && p.delta && warp == 0 && col < p.n) zsv[j] = __ldcg(p.zstate + col);  // issued early
         double a = 0.0;
         for (int g0 = gs; g0 < ge; g0 += 32) {  // one round of up to 32 L2 loads in flight
           double v[32];
@@ -1437,6 +1443,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           for (int u = 0; u < 32; ++u) a += v[u];
         }
         zseg[(j * CW + warp) * 32 + lane] = a;
+        if (!zmode && p.delta && warp == 0) zst[j * 32 + lane] = (col < p.n) ? zsv[j] : 0.0;
       }
       consumer_sync(CT);
       for (int j = warp; j < nls; j += CW) {
@@ -1447,10 +1454,11 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         for (int w = 0; w < CW; ++w) z += zseg[(j * CW + w) * 32 + lane];
         const bool valid = col < p.n;
         if (!zmode && p.delta && valid) {  // z state for delta passes: dense sets it, delta adds to it
+          const double zs = zst[j * 32 + lane];
           if (ctl->keep && !delta)
-            z = __ldcg(p.zstate + col);  // fixed point: z as cached
+            z = zs;  // fixed point: z as cached
           else if (delta)
-            z = __ldcg(p.zstate + col) + z;
+            z = zs + z;
           __stcg(p.zstate + col, z);
         }
         if (valid && !isfinite(z)) atomicMin(const_cast<unsigned*>(errp) + ERR_Z, static_cast<unsigned>(P));
@@ -1460,7 +1468,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           const unsigned word = __ballot_sync(0xffffffffu, valid && z < 0.0);
           if (p.world > 1) {  // every rank stages t from its own copy
             if (lane < p.world)
-              st_relaxed64_sys(p.tb64_pe[lane] + static_cast<size_t>(ctl->tsel & 1) * p.Q + qq, tag | word);
+              st_relaxed64_sys(p.tb64_pe[lane] + static_cast<size_t>(tbuf) * p.Q + qq, tag | word);
           } else if (lane == 0) {
             st_relaxed64(tout + qq, tag | word);
           }
@@ -1740,9 +1748,13 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       t_pass0 = t;
     }
     if (p.tensor && (kind & F_DOT)) {  // order-k: Z = M^T s_0, then axes 1..k-1 and c
-      col_reduce(true, P, false);
+      col_reduce(true, P, false, 0);
       axial_step<CW>(p, sax, tws, ctl, P);
     }
+
+    // Matrix dot pass: owners reduce z and publish the next t right away (it does
+    // not depend on the decision), taking the decision off every CTA's critical path.
+    if (!p.tensor && (kind & F_DOT)) col_reduce(false, P, (kind & F_DELTA) != 0, (pp + 1) & 1);
 
     // ------------------------------ decision ------------------------------
     if (tid == 0) {
@@ -1844,7 +1856,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
               need_reduce = 1;
               // delta pass next unless it is time to refresh the caches (every 16th
               // sweep, as the reference) or many columns flipped last time
-              if (p.delta && ctl->since_dense < 15 && static_cast<long long>(ctl->nflip) * 32 <= p.n) {
+              if (p.delta && ctl->since_dense + 1 < p.delta_refresh &&
+                  static_cast<long long>(ctl->nflip) * p.delta_div <= p.n) {
                 next |= F_DELTA;
                 ctl->since_dense += 1;
               } else {
@@ -1921,7 +1934,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     }
 
     // --------------------- column reduction: t' = sgn(z) ---------------------
-    if (!p.tensor && ctl->need_reduce) col_reduce(false, P, (kind & F_DELTA) != 0);
+    if (prof && tid == 0) pacc[4] += clock64() - t_pass0;
   }
   if (tid == 0) ctl->abort = 1;  // release a producer still waiting on an unconsumed stage
   if (prof && tid == 0)

@@ -99,6 +99,8 @@ struct KParams {
   double* zfull;       // [pitch] reduced z (order-k mode)
   int two_phase;       // 1: dot pass as (A) y = R t, (B) z = R^T s' (rows streamed twice)
   int delta;           // 1: sparse delta passes between dense refreshes (matrix mode)
+  int delta_div;       // delta pass only if the last sweep flipped <= n / delta_div columns
+  int delta_refresh;   // dense refresh every delta_refresh sweeps
   double* zstate;      // [pitch] z = R^T s of the previous pass (owners' columns)
   // wide rows: every row is streamed as cpr column chunks of chunk_cols
   // elements (one stage each); cpr == 1, chunk_cols == pitch otherwise
@@ -128,7 +130,7 @@ constexpr int kRing = 4;  // dot-partial ring depth (groups)
 
 // Shared-memory carve-up (byte offsets from the dynamic smem base).
 struct Layout {
-  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, ypart, txor, dzmask, ybak, total;
+  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, ypart, txor, dzmask, ybak, zst, total;
 };
 
 inline __host__ __device__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
@@ -167,6 +169,8 @@ inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_r
   o += align16(64 * 4);
   L.ybak = o;  // [rows_max]: y kept across a sweep whose t did not change
   o += align16(static_cast<size_t>(rows_max) * 8);
+  L.zst = o;  // [zl][32]: z state of the owner's column words (delta passes)
+  o += static_cast<size_t>(zl) * 32 * 8;
   L.total = o;
   return L;
 }
