@@ -260,8 +260,10 @@ def main():
                      "algorithmic_bytes": "sum_j (2*sweeps_j+1)*m*n*4 per launch (SURVEY 8d)",
                      "passes_per_launch": passes / args.steps,
                      "physical_stream_bytes_per_launch": passes / args.steps * M * N * 4,
-                     "note": "one fused pass per sweep reads R once (sweeps+1 passes/cut vs 2*sweeps+1 "
-                             "algorithmic); R is L2-resident so frac > 1 is expected"},
+                     "note": "algorithmic bytes count every half-iteration as a full read of R (the "
+                             "BASELINE formula); the engine reads less: one pass per sweep, R resident in "
+                             "SMEM/L2, and sparse delta passes (flipped t columns / s rows only) between "
+                             "dense refreshes, so frac can exceed 1; physical DRAM traffic is 'traffic'"},
         "sweeps_per_cut_mean": float(np.mean(sweeps)),
         "clocks": clocks,
     }
