@@ -1047,21 +1047,72 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
     return j < nres ? static_cast<double>(row[c]) : static_cast<double>(__ldcg(row + c));
   };
   // ---- y update: one warp per row, lanes over the t-XOR words (fixed order) ----
-  for (int j = warp; j < rows_g; j += NW) {
-    const E* row = row_ptr(j);
-    double acc = 0.0;
-    for (int w = lane; w < Q; w += 32) {
-      uint32_t x = txor[w];
-      const uint32_t tn = tws[w];
-      while (x) {
-        const int b = __ffs(x) - 1;
-        x &= x - 1;
-        const double v = elem(row, j, w * 32 + b);
-        acc += ((tn >> b) & 1u) ? -v : v;
+  // Each lane first lists its flipped columns (ascending); with at most kMaxF
+  // per lane every load of two rows is issued at once (one L2 round trip per
+  // row pair instead of one per column).  Summation order is the same either way.
+  constexpr int kMaxF = 8;
+  int fc[kMaxF];
+  uint32_t fneg = 0;
+  int nf = 0;
+  bool over = false;
+  for (int w = lane; w < Q; w += 32) {
+    uint32_t x = txor[w];
+    const uint32_t tn = tws[w];
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      if (nf < kMaxF) {
+        fc[nf] = w * 32 + b;
+        fneg |= ((tn >> b) & 1u) << nf;
+        ++nf;
+      } else {
+        over = true;
       }
     }
-    acc = warp_sum(acc);
-    if (lane == 0) yrow[j] += 2.0 * acc;
+  }
+  if (!__any_sync(0xffffffffu, over)) {
+    auto row_sum = [&](int j) -> double {
+      const E* row = row_ptr(j);
+      double v[kMaxF];
+#pragma unroll
+      for (int k = 0; k < kMaxF; ++k) v[k] = k < nf ? elem(row, j, fc[k]) : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < kMaxF; ++k)
+        if (k < nf) acc += ((fneg >> k) & 1u) ? -v[k] : v[k];
+      return acc;
+    };
+    int j = warp;
+    for (; j + NW < rows_g; j += 2 * NW) {
+      double a0 = row_sum(j), a1 = row_sum(j + NW);
+      a0 = warp_sum(a0);
+      a1 = warp_sum(a1);
+      if (lane == 0) {
+        yrow[j] += 2.0 * a0;
+        yrow[j + NW] += 2.0 * a1;
+      }
+    }
+    if (j < rows_g) {
+      const double a0 = warp_sum(row_sum(j));
+      if (lane == 0) yrow[j] += 2.0 * a0;
+    }
+  } else {
+    for (int j = warp; j < rows_g; j += NW) {
+      const E* row = row_ptr(j);
+      double acc = 0.0;
+      for (int w = lane; w < Q; w += 32) {
+        uint32_t x = txor[w];
+        const uint32_t tn = tws[w];
+        while (x) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1;
+          const double v = elem(row, j, w * 32 + b);
+          acc += ((tn >> b) & 1u) ? -v : v;
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) yrow[j] += 2.0 * acc;
+    }
   }
   consumer_sync(NW * 32);
   // ---- s' = sgn(y) ----
@@ -1088,6 +1139,22 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
   for (int i = 0; i < NE; ++i) zacc[i] = 0.0;
   bool any = false;
   const int sw = (rows_g + 31) / 32;
+  auto add_row = [&](int j, const VT (&xv)[VPT]) {
+    const double g = ((s_nxt[j >> 5] >> (j & 31)) & 1u) ? -2.0 : 2.0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      E x[EPV];
+      Vec<E>::split(xv[k], x);
+#pragma unroll
+      for (int e = 0; e < EPV; ++e) zacc[k * EPV + e] = fma(static_cast<double>(x[e]), g, zacc[k * EPV + e]);
+    }
+  };
+  auto load_row = [&](int j, VT (&xv)[VPT]) {
+    const VT* rv = reinterpret_cast<const VT*>(row_ptr(j));
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) xv[k] = j < nres ? rv[vidx[k]] : __ldcg(rv + vidx[k]);
+  };
+  int pend = -1;  // a flipped row whose loads are waiting for a partner (two rows per round trip)
   for (int w = 0; w < sw; ++w) {
     uint32_t f = s_nxt[w] ^ s_cur[w];
     if (w == sw - 1 && (rows_g & 31)) f &= (1u << (rows_g & 31)) - 1u;
@@ -1095,16 +1162,22 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
       const int j = w * 32 + __ffs(f) - 1;
       f &= f - 1;
       any = true;
-      const double g = ((s_nxt[j >> 5] >> (j & 31)) & 1u) ? -2.0 : 2.0;
-      const VT* rv = reinterpret_cast<const VT*>(row_ptr(j));
-#pragma unroll
-      for (int k = 0; k < VPT; ++k) {
-        E x[EPV];
-        Vec<E>::split(j < nres ? rv[vidx[k]] : __ldcg(rv + vidx[k]), x);
-#pragma unroll
-        for (int e = 0; e < EPV; ++e) zacc[k * EPV + e] = fma(static_cast<double>(x[e]), g, zacc[k * EPV + e]);
+      if (pend < 0) {
+        pend = j;
+        continue;
       }
+      VT x0[VPT], x1[VPT];
+      load_row(pend, x0);
+      load_row(j, x1);
+      add_row(pend, x0);  // ascending row order, as before
+      add_row(j, x1);
+      pend = -1;
     }
+  }
+  if (pend >= 0) {
+    VT x0[VPT];
+    load_row(pend, x0);
+    add_row(pend, x0);
   }
   if (any) {  // uniform across the CTA (every thread walks the same bits)
 #pragma unroll
