@@ -1487,20 +1487,29 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   // tbuf: the tb64 buffer the next pass reads ((pp + 1) & 1); the decision may
   // still stop the restart -- then these words are simply never read (the kept
   // triple's t lives in the other buffer).
-  auto col_reduce = [&](bool zmode, int P, bool delta, int tbuf) {
+  // Warps w0..CW-1 take part (w0 = 1: warp 0 runs the controller decision meanwhile
+  // and the participants synchronise on named barrier 2).
+  auto col_reduce = [&](bool zmode, int P, bool delta, int tbuf, int w0) {
+    const int NP = CW - w0, lw = warp - w0;
+    auto psync = [&]() {
+      if (w0 == 0)
+        consumer_sync(CT);
+      else
+        asm volatile("bar.sync 2, %0;" ::"r"(NP * 32) : "memory");
+    };
     double zsv[4];  // warp 0: z state of its word slices, parked in zst before the combine
     unsigned long long* tout = p.tb64 + static_cast<size_t>(tbuf) * p.Q;
     const unsigned long long tag = static_cast<unsigned long long>(P + 1) << 32;
     // owners by global CTA index: the CTAs of all ranks share the column words
     const int GT = p.GT, gg = p.rank * G + g;
-    const int gs = (warp * GT) / CW, ge = ((warp + 1) * GT) / CW;
+    const int gs = (lw * GT) / NP, ge = ((lw + 1) * GT) / NP;
     for (int q0 = gg; q0 < p.Q; q0 += GT * p.zl) {
       int nls = 0;
       for (int j = 0; j < p.zl && q0 + j * GT < p.Q; ++j) nls = j + 1;
       for (int j = 0; j < nls; ++j) {
         const int col = (q0 + j * GT) * 32 + lane;
         const size_t par = static_cast<size_t>(P & 1) * G * pitch + col;  // pass-parity buffer
-        if (!zmode && p.delta && warp == 0 && col < p.n) zsv[j] = __ldcg(p.zstate + col);  // issued early
+        if (!zmode && p.delta && lw == 0 && col < p.n) zsv[j] = __ldcg(p.zstate + col);  // issued early
         double a = 0.0;
         for (int g0 = gs; g0 < ge; g0 += 32) {  // one round of up to 32 L2 loads in flight
           double v[32];
@@ -1515,16 +1524,16 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
 #pragma unroll
           for (int u = 0; u < 32; ++u) a += v[u];
         }
-        zseg[(j * CW + warp) * 32 + lane] = a;
-        if (!zmode && p.delta && warp == 0) zst[j * 32 + lane] = (col < p.n) ? zsv[j] : 0.0;
+        zseg[(j * CW + lw) * 32 + lane] = a;
+        if (!zmode && p.delta && lw == 0) zst[j * 32 + lane] = (col < p.n) ? zsv[j] : 0.0;
       }
-      consumer_sync(CT);
-      for (int j = warp; j < nls; j += CW) {
+      psync();
+      for (int j = lw; j < nls; j += NP) {
         const int qq = q0 + j * GT;
         const int col = qq * 32 + lane;
         double z = 0.0;
 #pragma unroll
-        for (int w = 0; w < CW; ++w) z += zseg[(j * CW + w) * 32 + lane];
+        for (int w = 0; w < NP; ++w) z += zseg[(j * CW + w) * 32 + lane];
         const bool valid = col < p.n;
         if (!zmode && p.delta && valid) {  // z state for delta passes: dense sets it, delta adds to it
           const double zs = zst[j * 32 + lane];
@@ -1547,7 +1556,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           }
         }
       }
-      consumer_sync(CT);
+      psync();
     }
     // Order-k (single GPU): every CTA reads all of Z next, so the reduction ends
     // in a grid barrier.  Matrix mode needs none: the next pass polls the
@@ -1821,13 +1830,14 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       t_pass0 = t;
     }
     if (p.tensor && (kind & F_DOT)) {  // order-k: Z = M^T s_0, then axes 1..k-1 and c
-      col_reduce(true, P, false, 0);
+      col_reduce(true, P, false, 0, 0);
       axial_step<CW>(p, sax, tws, ctl, P);
     }
 
     // Matrix dot pass: owners reduce z and publish the next t right away (it does
     // not depend on the decision), taking the decision off every CTA's critical path.
-    if (!p.tensor && (kind & F_DOT)) col_reduce(false, P, (kind & F_DELTA) != 0, (pp + 1) & 1);
+    if (!p.tensor && (kind & F_DOT) && warp >= 1)  // warp 0 runs the decision below meanwhile
+      col_reduce(false, P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
 
     // ------------------------------ decision ------------------------------
     if (tid == 0) {
