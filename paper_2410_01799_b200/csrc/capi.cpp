@@ -553,6 +553,30 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
     double acc[12] = {0};
     for (int g = 0; g < G; ++g)
       for (int i = 0; i < 12; ++i) acc[i] += static_cast<double>(hp[g * 16 + i]) / G;
+    {
+      double mn[8], mx[8];
+      for (int i = 0; i < 8; ++i) {
+        mn[i] = 1e300;
+        mx[i] = 0;
+      }
+      for (int g = 0; g < G; ++g)
+        for (int i = 0; i < 8; ++i) {
+          mn[i] = std::min(mn[i], static_cast<double>(hp[g * 16 + i]));
+          mx[i] = std::max(mx[i], static_cast<double>(hp[g * 16 + i]));
+        }
+      const double np_ = std::max<double>(1.0, static_cast<double>(h_stats[1]));
+      if (std::getenv("SCB_PROF_CTA")) {
+        std::fprintf(stderr, "[scb cta] barrier wait per pass:");
+        for (int g = 0; g < G; ++g) std::fprintf(stderr, " %.0f", static_cast<double>(hp[g * 16 + 6]) / np_);
+        std::fprintf(stderr, "\n");
+      }
+      std::fprintf(stderr, "[scb prof3] per pass min/max over CTAs: chunks %.0f/%.0f passend %.0f/%.0f decision %.0f/%.0f reduce %.0f/%.0f staging %.0f/%.0f\n",
+                   mn[1] / np_, mx[1] / np_, mn[2] / np_, mx[2] / np_, mn[3] / np_, mx[3] / np_, mn[4] / np_, mx[4] / np_,
+                   mn[5] / np_, mx[5] / np_);
+    }
+    std::fprintf(stderr, "[scb passes] dense dot %llu, delta dot %llu, total %llu\n",
+                 static_cast<unsigned long long>(h_stats[2]), static_cast<unsigned long long>(h_stats[3]),
+                 static_cast<unsigned long long>(h_stats[1]));
     std::fprintf(stderr, "[scb prof2] per pass: stagewait=%.0f A=%.0f B=%.0f C=%.0f\n",
                  acc[8] / std::max<double>(1.0, static_cast<double>(h_stats[1])),
                  acc[9] / std::max<double>(1.0, static_cast<double>(h_stats[1])),

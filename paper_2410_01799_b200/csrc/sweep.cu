@@ -110,6 +110,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   }
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
+
 // the same across GPUs: the counter lives on rank 0, peers reach it over NVLink
 __device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
   unsigned v;
@@ -1472,6 +1473,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   int qs = 0, qph = 0;     // stage / phase of this pass's first streamed row
   unsigned gcount = 0;     // dot-partial groups published in earlier passes
   unsigned epoch = 0;      // grid barriers passed (thread 0)
+  unsigned long long dot_passes[2] = {0, 0};  // CTA 0: dense, delta dot passes (-> stats[2], [3])
   int vidx[VPT];           // owned vectors (clamped to a valid address when out of range)
   bool vok[VPT];
 #pragma unroll
@@ -1794,11 +1796,18 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       }
     }
     consumer_sync(CT);
+    if (g == 0 && tid == 0 && (kind & F_DOT)) ++dot_passes[(kind & F_DELTA) ? 1 : 0];
+    if (prof && tid == 0) {  // pre-barrier part of the pass end
+      const long long t = clock64();
+      pacc[0] += t - t_pass0;
+    }
     if (tid == 0) {
+      const long long tb0 = prof ? clock64() : 0;
       if (p.world > 1)
         grid_barrier_sys(p.bar, ++epoch * static_cast<unsigned>(p.GT));
       else
         grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
+      if (prof) pacc[6] += clock64() - tb0;  // barrier (incl. waiting for the last CTA)
     }
     consumer_sync(CT);
     {
@@ -2020,6 +2029,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     if (prof && tid == 0) pacc[4] += clock64() - t_pass0;
   }
   if (tid == 0) ctl->abort = 1;  // release a producer still waiting on an unconsumed stage
+  if (g == 0 && tid == 0) {
+    p.stats[2] = dot_passes[0];
+    p.stats[3] = dot_passes[1];
+  }
   if (prof && tid == 0)
     for (int i = 0; i < 7; ++i) prof[g * 16 + i] = static_cast<unsigned long long>(pacc[i]);
 }

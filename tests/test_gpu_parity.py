@@ -377,3 +377,36 @@ def test_fused_pass_default_beyond_l2(engine, ref):
     od = ref.greedy_decompose(a.astype(np.float64), 3, seed=2)
     assert (dec.factors[0] == od.signs[0]).all() and (dec.factors[1] == od.signs[1]).all()
     assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F32_TOL
+
+
+# ------------------------------------------------------------- delta passes
+def test_delta_passes_keep_the_trajectory(engine, ref, monkeypatch):
+    """Sparse delta passes (cached y = Rt, z = R^T s updated from the flipped
+    columns / rows, dense refresh every 16 sweeps) against dense-only passes and
+    the reference on the same input: identical signs and sweeps, c to 1e-12."""
+    a = ref.fill_normal(11, 1024 * 1024).reshape(1024, 1024).astype(np.float32)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SCB_DELTA", mode)
+        out[mode] = run(engine, a, 40, seed=3, dtype="f32")
+    (d0, r0, _), (d1, r1, _) = out["0"], out["1"]
+    assert all((x == y).all() for x, y in zip(d0.factors, d1.factors))
+    assert np.array_equal(r0.sweeps, r1.sweeps)
+    assert np.max(np.abs(r1._cut_values - r0._cut_values) / np.abs(r0._cut_values)) <= 1e-12
+    od = ref.greedy_decompose(a.astype(np.float64), 40, seed=3)
+    assert (d1.factors[0] == od.signs[0]).all() and (d1.factors[1] == od.signs[1]).all()
+    assert sweeps_ok(r1.sweeps, od.iterations)
+
+
+@pytest.mark.parametrize("refresh,div", [("1", "32"), ("4", "1"), ("64", "1000000")])
+def test_delta_policy_extremes(engine, ref, monkeypatch, refresh, div):
+    """Every refresh cadence / flip threshold gives the reference's signs: all
+    dense (refresh 1), delta even after many flips (div 1), delta only on
+    near-converged sweeps (div huge)."""
+    monkeypatch.setenv("SCB_DELTA_REFRESH", refresh)
+    monkeypatch.setenv("SCB_DELTA_DIV", div)
+    a = ref.fill_normal(12, 300 * 257).reshape(300, 257)
+    dec, rep, _ = run(engine, a, 12, seed=4)
+    od = ref.greedy_decompose(a, 12, seed=4)
+    assert (dec.factors[0] == od.signs[0]).all() and (dec.factors[1] == od.signs[1]).all()
+    assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F64_TOL
