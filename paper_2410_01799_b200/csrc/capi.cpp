@@ -246,6 +246,17 @@ void sc_lpt_schedule(const double* costs, uint64_t count, uint32_t bins, uint32_
 
 namespace {
 sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc_ctx::Shard* sh);
+
+// CTAs for m rows (the engine and the sharded path agree, so world-1 sharding is
+// bit-identical to the engine)
+uint64_t auto_ctas(int num_sms, int cps, uint64_t m) {
+  uint64_t g = std::min<uint64_t>(static_cast<uint64_t>(num_sms) * cps, m);
+  if (cps == 1 && m <= 8ull * num_sms) {
+    const uint64_t k = (m + 127) / 128;
+    g = std::min<uint64_t>(g, (m + k - 1) / k);
+  }
+  return g;
+}
 }
 
 sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) {
@@ -300,7 +311,12 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   const int cpr = pitch > tile_cols ? static_cast<int>((pitch + tile_cols - 1) / tile_cols) : 1;
   if (sh && (tensor || var.cps != 1 || static_cast<uint64_t>(sh->G) > m))
     return set_err(ctx, SC_NOT_SUPPORTED, "row sharding: matrices only, one CTA per SM, band >= %d rows", sh ? sh->G : 0);
-  const int G = sh ? sh->G : static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(ctx->num_sms) * var.cps, m));
+  // CTAs: one per SM; small matrices (<= 8 rows per SM) use at most 128 CTAs with
+  // equal bands -- the pass is synchronisation-bound there and a smaller, balanced
+  // grid is faster (1024^2 f32: 11.5 vs 13.1 us/pass).  SCB_CTAS caps G (tuning).
+  const uint64_t g_auto = auto_ctas(ctx->num_sms, var.cps, m);
+  const int G = sh ? sh->G
+                  : static_cast<int>(std::min<uint64_t>(g_auto, env_size("SCB_CTAS", static_cast<size_t>(g_auto))));
   const int rows_base = static_cast<int>(m / G), rows_rem = static_cast<int>(m % G);
   const int rows_max = rows_base + (rows_rem ? 1 : 0);
   const int Q = static_cast<int>(pitch / 32);
@@ -507,7 +523,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   // serial chain -- the better choice while R stays in SMEM / L2; once R spills
   // to HBM the fused single-read pass wins (14336x4096 f32: 77.6 vs 84 us/pass).
   // Wide rows (cpr > 1) always take the two-phase pass.  SCB_2PH=0/1 overrides.
-  const bool l2_resident = m * rowB <= (size_t{96} << 20);
+  const bool l2_resident = m * rowB <= (size_t{160} << 20);  // 4096^2 f64 (128 MB): two-phase 24.0 vs 24.6 us/pass
   kp.two_phase = cpr > 1 ? 1 : static_cast<int>(env_size("SCB_2PH", l2_resident ? 1 : 0));
   kp.cpr = cpr;
   kp.world = sh ? sh->world : 1;
@@ -662,7 +678,7 @@ sc_status sc_shard_open(sc_ctx* ctx, const sc_shard_config* cfg, void* handle_ou
   S.n = cfg->n;
   S.pitch = static_cast<long long>((cfg->n + 31) / 32 * 32);
   const uint64_t min_band = cfg->m_global / cfg->world;  // bands are floor/ceil of m/world
-  S.G = cfg->ctas > 0 ? cfg->ctas : static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(ctx->num_sms), min_band));
+  S.G = cfg->ctas > 0 ? cfg->ctas : static_cast<int>(auto_ctas(ctx->num_sms, 1, min_band));
   const int Q = static_cast<int>(S.pitch / 32);
   S.tw32 = std::max(Q, static_cast<int>(2 * words64(cfg->n)));
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };

@@ -371,7 +371,7 @@ def test_dot_pass_forms_f32_1024_trajectory(engine, ref, monkeypatch, two_phase)
 
 def test_fused_pass_default_beyond_l2(engine, ref):
     """A matrix larger than the L2 budget takes the fused pass by default."""
-    m, n = 6200, 4096  # 101 MB f32
+    m, n = 10300, 4096  # 169 MB f32
     a = (ref.fill_normal(5, m * n).reshape(m, n)).astype(np.float32)
     dec, rep, _ = run(engine, a, 3, seed=2, dtype="f32")
     od = ref.greedy_decompose(a.astype(np.float64), 3, seed=2)
