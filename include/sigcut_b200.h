@@ -20,6 +20,18 @@
  *                                  best_of_restarts (search.hpp:222)
  *   sc_width_for_compression restates width_for_compression  metrics.hpp:55-63
  *
+ * Around the path, same boundary rules:
+ *   sc_accumulate_expansion replaces detail::accumulate_expansion decompose.hpp:182-197
+ *                        and (zero_fill)  sigcut::expand            decompose.hpp:266-270
+ *   sc_gram_matrix       replaces  detail::build_gram (Gram part)   decompose.hpp:383-393
+ *   sc_contract_terms    replaces  detail::contract_term            decompose.hpp:218-260
+ *   sc_solve_gram        restates  sigcut::solve_gram               gram.hpp:83-107
+ *   sc_correct_coefficients replaces sigcut::correct_coefficients  decompose.hpp:418-428
+ *   sc_lstsq_decompose   replaces  sigcut::lstsq_decompose          decompose.hpp:434-469
+ *                        and (channel_axis >= 0) rgb_scalars_decompose :485-536
+ *   sc_write_scd / sc_read_scd(_header) restate write_scd / read_scd io.hpp:135-213
+ *   sc_write_dten / sc_read_dten(_header) restate write_raw / read_raw io.hpp:226-292
+ *
  * Plain pointers and sizes only.  Status codes map 1:1 onto the reference's
  * exceptions: SC_INVALID_ARGUMENT <-> std::invalid_argument,
  * SC_RUNTIME_ERROR <-> std::runtime_error (include/sigcut_b200.hpp does the mapping).
@@ -45,7 +57,8 @@ typedef enum sc_status {
   SC_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
   SC_RUNTIME_ERROR = 2,    /* std::runtime_error in the reference */
   SC_CUDA_ERROR = 3,       /* device / driver failure (no reference analogue) */
-  SC_NOT_SUPPORTED = 4     /* shape outside the kernels' envelope */
+  SC_NOT_SUPPORTED = 4,    /* shape outside the kernels' envelope */
+  SC_IO_ERROR = 5          /* sigcut::io_error (io.hpp:22-24) in the reference */
 } sc_status;
 
 typedef enum sc_dtype { SC_F32 = 0, SC_F64 = 1 } sc_dtype;
@@ -140,6 +153,91 @@ uint64_t sc_width_for_compression(int coeff_bits, int source_bits, int order,
  * the given costs to `bins` devices; writes the bin of each job.  Used by the
  * multi-GPU batch path (one process per GPU, no data-path collective). */
 void sc_lpt_schedule(const double* costs, uint64_t count, uint32_t bins, uint32_t* bin_of_job);
+
+/* ------------------------------------------------------------------------ */
+/* Sign-term factors of a CutDecomposition (decompose.hpp:30-100) in host
+ * memory.  sign_words[i] belongs to the i-th SIGN axis in ascending axis order
+ * (every axis except channel_axis): width x ceil(n/64) u64, term-major,
+ * SignVector layout.  coefficients: width x channels, term-major (channels =
+ * shape[channel_axis], or 1 when channel_axis == -1). */
+typedef struct sc_factors {
+  int32_t order;
+  const uint64_t* shape;
+  int32_t channel_axis;
+  uint64_t width;
+  const uint64_t* sign_words[SC_MAX_ORDER];
+  const double* coefficients;
+} sc_factors;
+
+/* Per-call accounting of the auxiliary ops. */
+typedef struct sc_op_stats {
+  double kernel_ms;
+  double total_ms;
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+  int32_t kernel_launches;
+} sc_op_stats;
+
+/* data[e] += sum over terms j in [first_term, last_term) of
+ * flip(scale * coef_j(channel of e), parity_j(e)), summed in term order from 0.0
+ * and added last (accumulate_terms, decompose.hpp:128-180): bit-identical to the
+ * reference.  data: numel f64, row-major, host (data_on_device = 0) or device.
+ * zero_fill != 0 zeroes data first (expand).  stats may be NULL. */
+sc_status sc_accumulate_expansion(sc_ctx* ctx, const sc_factors* d, double scale, uint64_t first_term,
+                                  uint64_t last_term, double* data, int32_t data_on_device, int32_t zero_fill,
+                                  sc_op_stats* stats);
+
+/* gram[i * width + j] = prod over sign axes of sign_dot(f_i, f_j): width x width
+ * (exact integers in f64; bit-identical to gram_column). */
+sc_status sc_gram_matrix(sc_ctx* ctx, const sc_factors* d, double* gram, sc_op_stats* stats);
+
+/* rhs[(j - first_term) * channels + ch] = <sign outer product of term j, channel
+ * ch of A> for j in [first_term, first_term + count).  A: numel values of
+ * a_dtype (sc_dtype) in the factors' shape, host or device.  f64 sums in a fixed
+ * parallel order (the reference sums sequentially: agreement to rounding). */
+sc_status sc_contract_terms(sc_ctx* ctx, const sc_factors* d, int32_t a_dtype, const void* a, int32_t a_on_device,
+                            uint64_t first_term, uint64_t count, double* rhs, sc_op_stats* stats);
+
+/* Host Cholesky solve of the normal equations with the reference's ridge retry
+ * (gram.hpp:48-107, same loop order).  gram: width x width; rhs / out: width x
+ * channels, term-major.  SC_RUNTIME_ERROR when the factorisation fails. */
+sc_status sc_solve_gram(uint64_t width, uint64_t channels, const double* gram, const double* rhs, double* out,
+                        char* msg, size_t msg_len);
+
+/* correct_coefficients (decompose.hpp:418-428): refit with the signs held fixed;
+ * keeps the old coefficients when the solve is not better.  coeffs_out: width x
+ * channels. */
+sc_status sc_correct_coefficients(sc_ctx* ctx, const sc_factors* d, int32_t a_dtype, const void* a,
+                                  int32_t a_on_device, double* coeffs_out, sc_op_stats* stats);
+
+/* lstsq_decompose (decompose.hpp:434-469; channel_axis == -1) or
+ * rgb_scalars_decompose (:485-536; channel_axis >= 0, channels <= 8): every
+ * term is searched on the device on the explicit residual A - expand(d), the
+ * coefficients are re-solved, and the residual is re-expanded on the device.
+ * result: sign_words per SIGN axis (ascending), alpha = width x channels
+ * coefficients, cut_value, resid_norm (= ||A - expand||_F after each term),
+ * sweeps; resid_norm_exact and remainder as in sc_greedy_decompose. */
+sc_status sc_lstsq_decompose(sc_ctx* ctx, const sc_problem* problem, int32_t channel_axis, sc_result* result);
+
+/* SCD container (io.hpp:113-213), bytes identical to write_scd. */
+uint64_t sc_scd_size(const sc_factors* d, int coeff_bits);
+sc_status sc_write_scd(const sc_factors* d, int coeff_bits, uint8_t* out, uint64_t capacity, uint64_t* written,
+                       char* msg, size_t msg_len);
+/* shape must hold SC_MAX_ORDER entries. */
+sc_status sc_read_scd_header(const uint8_t* in, uint64_t size, int32_t* order, uint64_t* shape,
+                             int32_t* channel_axis, uint64_t* width, int32_t* coeff_bits, char* msg, size_t msg_len);
+/* sign_words[i]: width x ceil(n/64) per sign axis; coefficients: width x channels. */
+sc_status sc_read_scd(const uint8_t* in, uint64_t size, uint64_t** sign_words, double* coefficients, char* msg,
+                      size_t msg_len);
+
+/* DTEN raw tensors (io.hpp:215-292).  raw_dtype: 0 f64, 1 f32, 2 u8 (RawDType).
+ * sc_write_dten encodes f64 values; sc_read_dten widens to f64 like read_raw. */
+uint64_t sc_dten_size(int32_t order, const uint64_t* shape, int32_t raw_dtype);
+sc_status sc_write_dten(int32_t order, const uint64_t* shape, const double* data, int32_t raw_dtype, uint8_t* out,
+                        uint64_t capacity, uint64_t* written, char* msg, size_t msg_len);
+sc_status sc_read_dten_header(const uint8_t* in, uint64_t size, int32_t* order, uint64_t* shape, int32_t* raw_dtype,
+                              char* msg, size_t msg_len);
+sc_status sc_read_dten(const uint8_t* in, uint64_t size, double* data, char* msg, size_t msg_len);
 
 /* ------------------------------------------------------------------------ */
 /* Row-sharded decomposition of ONE matrix over `world` GPUs (one process and

@@ -76,7 +76,44 @@ typedef struct oracle_output {
                                     const uint64_t* shape, double rate);               \
   double P##compression_rate(uint64_t k, int coeff_bits, int source_bits, int order,   \
                              const uint64_t* shape);                                   \
-  void P##quantize_bf16(uint64_t count, const double* in, double* out);
+  void P##quantize_bf16(uint64_t count, const double* in, double* out);                \
+  /* --- around the path ---------------------------------------- */ \
+  /* factors[i]: i-th SIGN axis (ascending), width x words(n) u64; coeffs: width x    \
+   * channels.  data[numel] += sum_{j >= first_term} flip(scale coef, parity)        \
+   * (detail::accumulate_expansion, decompose.hpp:182-197). */                        \
+  int P##accumulate_expansion(int order, const uint64_t* shape, int channel_axis,      \
+                              uint64_t width, const uint64_t* const* factors,          \
+                              const double* coeffs, double scale, uint64_t first_term, \
+                              double* data);                                           \
+  /* build_gram (decompose.hpp:383-393): gram width x width, rhs width x channels */ \
+  int P##build_gram(const double* a, int order, const uint64_t* shape, int channel_axis, \
+                    uint64_t width, const uint64_t* const* factors, double* gram,      \
+                    double* rhs);                                                      \
+  /* solve_gram (gram.hpp:83-107) */                                                  \
+  int P##solve_gram(uint64_t width, uint64_t channels, const double* gram,             \
+                    const double* rhs, double* out);                                   \
+  /* correct_coefficients (decompose.hpp:418-428) */                                  \
+  int P##correct_coefficients(const double* a, int order, const uint64_t* shape,       \
+                              int channel_axis, uint64_t width,                        \
+                              const uint64_t* const* factors, const double* coeffs,    \
+                              double* out);                                            \
+  /* lstsq_decompose (channel_axis == -1, decompose.hpp:434-469) or                   \
+   * rgb_scalars_decompose (:485-536): out->signs per SIGN axis, out->alpha width x   \
+   * channels, resid_norm = CutStep::residual_norm. */                                \
+  int P##lstsq_decompose(const double* a, int order, const uint64_t* shape,            \
+                         int channel_axis, const oracle_config* cfg, oracle_output* out); \
+  /* write_scd (io.hpp:142-166) into buf (capacity cap); *size = bytes */             \
+  int P##write_scd(int order, const uint64_t* shape, int channel_axis, uint64_t width, \
+                   const uint64_t* const* factors, const double* coeffs, int coeff_bits, \
+                   uint8_t* buf, uint64_t cap, uint64_t* size);                        \
+  /* read_scd (io.hpp:168-213): header fields, then factors / coeffs if non-NULL */   \
+  int P##read_scd(const uint8_t* buf, uint64_t size, int* order, uint64_t* shape,      \
+                  int* channel_axis, uint64_t* width, uint64_t** factors, double* coeffs); \
+  /* write_raw / read_raw (io.hpp:226-292) */                                         \
+  int P##write_raw(int order, const uint64_t* shape, const double* data, int dtype,    \
+                   uint8_t* buf, uint64_t cap, uint64_t* size);                        \
+  int P##read_raw(const uint8_t* buf, uint64_t size, int* order, uint64_t* shape,      \
+                  double* data);
 
 ORACLE_DECLARE(orc_)
 ORACLE_DECLARE(ref_)

@@ -102,6 +102,21 @@ class Oracle:
             "width_for_compression": (u64, [C.c_int, C.c_int, C.c_int, P(u64), C.c_double]),
             "compression_rate": (C.c_double, [u64, C.c_int, C.c_int, C.c_int, P(u64)]),
             "quantize_bf16": (None, [u64, P(C.c_double), P(C.c_double)]),
+            "accumulate_expansion": (C.c_int, [C.c_int, P(u64), C.c_int, u64, P(P(u64)), P(C.c_double),
+                                               C.c_double, u64, P(C.c_double)]),
+            "build_gram": (C.c_int, [P(C.c_double), C.c_int, P(u64), C.c_int, u64, P(P(u64)), P(C.c_double),
+                                     P(C.c_double)]),
+            "solve_gram": (C.c_int, [u64, u64, P(C.c_double), P(C.c_double), P(C.c_double)]),
+            "correct_coefficients": (C.c_int, [P(C.c_double), C.c_int, P(u64), C.c_int, u64, P(P(u64)),
+                                               P(C.c_double), P(C.c_double)]),
+            "lstsq_decompose": (C.c_int, [P(C.c_double), C.c_int, P(u64), C.c_int, P(OracleConfig),
+                                          P(OracleOutput)]),
+            "write_scd": (C.c_int, [C.c_int, P(u64), C.c_int, u64, P(P(u64)), P(C.c_double), C.c_int,
+                                    P(C.c_uint8), u64, P(u64)]),
+            "read_scd": (C.c_int, [P(C.c_uint8), u64, P(C.c_int), P(u64), P(C.c_int), P(u64), P(P(u64)),
+                                   P(C.c_double)]),
+            "write_raw": (C.c_int, [C.c_int, P(u64), P(C.c_double), C.c_int, P(C.c_uint8), u64, P(u64)]),
+            "read_raw": (C.c_int, [P(C.c_uint8), u64, P(C.c_int), P(u64), P(C.c_double)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, p + name)
@@ -195,6 +210,132 @@ class Oracle:
                                         _ptr(sv, C.c_double), C.byref(nsv)))
         return dict(value=value.value, signs=signs, iterations=int(iters.value),
                     sweep_values=sv[: nsv.value].copy())
+
+
+    # -- around the path -------------------------------------
+    @staticmethod
+    def _fac(factors):
+        fs = [np.ascontiguousarray(f, np.uint64) for f in factors]
+        arr = (P(u64) * max(1, len(fs)))(*[_ptr(f, u64) for f in fs])
+        return fs, arr
+
+    def accumulate_expansion(self, shape, factors, coeffs, data=None, scale=1.0, first_term=0,
+                             channel_axis=-1) -> np.ndarray:
+        """data (f64, shape) += sum_{j >= first_term} flip(scale coef_j, parity); zeros if None."""
+        shape = tuple(int(d) for d in shape)
+        sh = np.asarray(shape, np.uint64)
+        out = np.zeros(shape) if data is None else np.array(data, np.float64, copy=True)
+        co = np.ascontiguousarray(coeffs, np.float64)
+        width = co.shape[0] if co.ndim else 0
+        fs, arr = self._fac(factors)
+        self._err(self._f["accumulate_expansion"](len(shape), _ptr(sh, u64), channel_axis, width, arr,
+                                                  _ptr(co, C.c_double), scale, first_term, _ptr(out, C.c_double)))
+        return out
+
+    def build_gram(self, a, factors, width, channel_axis=-1):
+        a = np.ascontiguousarray(a, np.float64)
+        sh = np.asarray(a.shape, np.uint64)
+        q = a.shape[channel_axis] if channel_axis >= 0 else 1
+        gram = np.zeros((width, width))
+        rhs = np.zeros((width, q))
+        fs, arr = self._fac(factors)
+        self._err(self._f["build_gram"](_ptr(a, C.c_double), a.ndim, _ptr(sh, u64), channel_axis, width, arr,
+                                        _ptr(gram, C.c_double), _ptr(rhs, C.c_double)))
+        return gram, rhs
+
+    def solve_gram(self, gram, rhs):
+        gram = np.ascontiguousarray(gram, np.float64)
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        w = gram.shape[0]
+        ch = rhs.size // max(w, 1)
+        out = np.zeros_like(rhs)
+        self._err(self._f["solve_gram"](w, ch, _ptr(gram, C.c_double), _ptr(rhs, C.c_double), _ptr(out, C.c_double)))
+        return out
+
+    def correct_coefficients(self, a, factors, coeffs, channel_axis=-1):
+        a = np.ascontiguousarray(a, np.float64)
+        sh = np.asarray(a.shape, np.uint64)
+        co = np.ascontiguousarray(coeffs, np.float64)
+        out = np.zeros_like(co)
+        fs, arr = self._fac(factors)
+        self._err(self._f["correct_coefficients"](_ptr(a, C.c_double), a.ndim, _ptr(sh, u64), channel_axis,
+                                                  co.shape[0], arr, _ptr(co, C.c_double), _ptr(out, C.c_double)))
+        return out
+
+    def lstsq_decompose(self, a, width, seed=0, channel_axis=-1, restarts=1, max_sweeps=100,
+                        min_value_fraction=0.0, max_factor_bytes=1 << 30) -> Decomposition:
+        a = np.ascontiguousarray(a, np.float64)
+        shape = tuple(int(d) for d in a.shape)
+        sh = np.asarray(shape, np.uint64)
+        cfg = OracleConfig(width, 32, seed, restarts, max_sweeps, min_value_fraction, max_factor_bytes)
+        q = shape[channel_axis] if channel_axis >= 0 else 1
+        axes = [i for i in range(len(shape)) if i != channel_axis]
+        alloc_w = max(width, 1)
+        signs = [np.zeros((alloc_w, words(shape[i])), np.uint64) for i in axes]
+        out = OracleOutput()
+        for i, s in enumerate(signs):
+            out.signs[i] = _ptr(s, u64)
+        alpha = np.zeros((alloc_w, q))
+        cut, rn = np.zeros(alloc_w), np.zeros(alloc_w)
+        it = np.zeros(alloc_w, np.uint64)
+        out.alpha, out.cut_value, out.resid_norm = _ptr(alpha, C.c_double), _ptr(cut, C.c_double), _ptr(rn, C.c_double)
+        out.iterations = _ptr(it, u64) if self.which == "orc" else None
+        out.remainder = None
+        self._err(self._f["lstsq_decompose"](_ptr(a, C.c_double), len(shape), _ptr(sh, u64), channel_axis,
+                                             C.byref(cfg), C.byref(out)))
+        w = int(out.width_done)
+        return Decomposition(shape, [s[:w] for s in signs], alpha[:w] if channel_axis >= 0 else alpha[:w, 0],
+                             cut[:w], rn[:w], it[:w] if self.which == "orc" else None, None,
+                             out.input_norm, out.final_residual_norm, w)
+
+    def write_scd(self, shape, factors, coeffs, channel_axis=-1, coeff_bits=64) -> bytes:
+        sh = np.asarray(shape, np.uint64)
+        co = np.ascontiguousarray(coeffs, np.float64)
+        fs, arr = self._fac(factors)
+        size = u64()
+        cap = 64 + 8 * len(shape) + co.size * 8 + sum(f.size * 8 for f in fs) + 1024
+        buf = np.zeros(cap, np.uint8)
+        self._err(self._f["write_scd"](len(shape), _ptr(sh, u64), channel_axis, co.shape[0] if co.ndim else 0, arr,
+                                       _ptr(co, C.c_double), coeff_bits, _ptr(buf, C.c_uint8), cap, C.byref(size)))
+        return bytes(buf[: size.value])
+
+    def read_scd(self, data: bytes):
+        buf = np.frombuffer(data, np.uint8).copy() if len(data) else np.zeros(1, np.uint8)
+        order, chax, width = C.c_int(), C.c_int(), u64()
+        shape = np.zeros(8, np.uint64)
+        self._err(self._f["read_scd"](_ptr(buf, C.c_uint8), len(data), C.byref(order), _ptr(shape, u64),
+                                      C.byref(chax), C.byref(width), None, None))
+        k, ca, w = order.value, chax.value, int(width.value)
+        shp = tuple(int(x) for x in shape[:k])
+        q = shp[ca] if ca >= 0 else 1
+        axes = [i for i in range(k) if i != ca]
+        fs = [np.zeros((max(w, 1), words(shp[i])), np.uint64) for i in axes]
+        co = np.zeros((max(w, 1), q))
+        _, arr = self._fac(fs)
+        self._err(self._f["read_scd"](_ptr(buf, C.c_uint8), len(data), C.byref(order), _ptr(shape, u64),
+                                      C.byref(chax), C.byref(width), arr, _ptr(co, C.c_double)))
+        return shp, ca, [f[:w] for f in fs], (co[:w] if ca >= 0 else co[:w, 0])
+
+    def write_raw(self, a, dtype=0) -> bytes:
+        a = np.ascontiguousarray(a, np.float64)
+        sh = np.asarray(a.shape, np.uint64)
+        cap = 16 + 8 * a.ndim + a.size * 8
+        buf = np.zeros(cap, np.uint8)
+        size = u64()
+        self._err(self._f["write_raw"](a.ndim, _ptr(sh, u64), _ptr(a, C.c_double), dtype, _ptr(buf, C.c_uint8), cap,
+                                       C.byref(size)))
+        return bytes(buf[: size.value])
+
+    def read_raw(self, data: bytes) -> np.ndarray:
+        buf = np.frombuffer(data, np.uint8).copy() if len(data) else np.zeros(1, np.uint8)
+        order = C.c_int()
+        shape = np.zeros(8, np.uint64)
+        self._err(self._f["read_raw"](_ptr(buf, C.c_uint8), len(data), C.byref(order), _ptr(shape, u64), None))
+        shp = tuple(int(x) for x in shape[: order.value])
+        out = np.zeros(shp)
+        self._err(self._f["read_raw"](_ptr(buf, C.c_uint8), len(data), C.byref(order), _ptr(shape, u64),
+                                      _ptr(out, C.c_double)))
+        return out
 
 
 def normal_matrix(seed: int, shape, oracle: Oracle | None = None) -> np.ndarray:

@@ -6,6 +6,7 @@
 // oracle/_ref/libsigcut_ref.so.  Tests use it to pin oracle/sigcut_oracle.c and
 // to generate tests/golden/ fixtures; bench.py --impl reference times it.
 #include <cstring>
+#include <sstream>
 #include <exception>
 #include <stdexcept>
 #include <string>
@@ -20,7 +21,38 @@ std::string g_err;
 
 int map_exc(const std::exception& e) {
   g_err = e.what();
+  if (dynamic_cast<const sigcut::io_error*>(&e) != nullptr) return 3;
   return dynamic_cast<const std::invalid_argument*>(&e) != nullptr ? 1 : 2;
+}
+
+// A CutDecomposition assembled from raw factor words (per sign axis) and coefficients.
+sigcut::CutDecomposition make_dec(int order, const uint64_t* shape, int channel_axis, uint64_t width,
+                                  const uint64_t* const* factors, const double* coeffs) {
+  auto d = sigcut::CutDecomposition::with_shape(std::vector<std::size_t>(shape, shape + order), channel_axis);
+  const auto axes = d.sign_axes();
+  for (uint64_t j = 0; j < width; ++j) {
+    std::vector<sigcut::SignVector> signs;
+    for (std::size_t i = 0; i < axes.size(); ++i) {
+      const std::size_t n = shape[axes[i]];
+      const std::size_t nw = sigcut::SignVector::word_count(n);
+      signs.push_back(sigcut::SignVector::from_words(
+          n, std::vector<std::uint64_t>(factors[i] + j * nw, factors[i] + (j + 1) * nw)));
+    }
+    d.append_term(signs, std::span<const double>(coeffs + j * d.channels(), d.channels()));
+  }
+  return d;
+}
+
+void put_dec(const sigcut::CutDecomposition& d, uint64_t** factors, double* coeffs) {
+  const auto axes = d.sign_axes();
+  for (std::size_t i = 0; i < axes.size(); ++i) {
+    const std::size_t nw = sigcut::SignVector::word_count(d.shape[axes[i]]);
+    for (std::size_t j = 0; j < d.width(); ++j) {
+      const auto w = d.factors[i].column(j).words();
+      std::memcpy(factors[i] + j * nw, w.data(), nw * 8);
+    }
+  }
+  std::memcpy(coeffs, d.coefficients.data(), d.coefficients.size() * 8);
 }
 
 std::vector<std::size_t> to_shape(int order, const uint64_t* shape) {
@@ -153,6 +185,162 @@ void ref_quantize_bf16(uint64_t count, const double* in, double* out) {
   auto t = sigcut::DenseTensor::from_raw({count}, std::vector<double>(in, in + count));
   const auto q = sigcut::quantize_half(t, sigcut::HalfFormat::kBf16);
   std::memcpy(out, q.data().data(), count * sizeof(double));
+}
+
+int ref_accumulate_expansion(int order, const uint64_t* shape, int channel_axis, uint64_t width,
+                             const uint64_t* const* factors, const double* coeffs, double scale,
+                             uint64_t first_term, double* data) {
+  try {
+    const auto d = make_dec(order, shape, channel_axis, width, factors, coeffs);
+    const std::size_t numel = sigcut::DenseTensor::checked_numel(d.shape);
+    auto t = sigcut::DenseTensor::from_raw(d.shape, std::vector<double>(data, data + numel));
+    sigcut::detail::accumulate_expansion(t, d, scale, first_term);
+    std::memcpy(data, t.data().data(), numel * 8);
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_build_gram(const double* a, int order, const uint64_t* shape, int channel_axis, uint64_t width,
+                   const uint64_t* const* factors, double* gram, double* rhs) {
+  try {
+    std::vector<double> zero(width * (channel_axis >= 0 ? shape[channel_axis] : 1), 0.0);
+    const auto d = make_dec(order, shape, channel_axis, width, factors, zero.data());
+    const std::size_t numel = sigcut::DenseTensor::checked_numel(d.shape);
+    sigcut::DenseTensor t(d.shape, std::vector<double>(a, a + numel));
+    const sigcut::GramSystem sys = sigcut::detail::build_gram(t, d);
+    std::memcpy(gram, sys.gram.data(), sys.gram.size() * 8);
+    std::memcpy(rhs, sys.rhs.data(), sys.rhs.size() * 8);
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_solve_gram(uint64_t width, uint64_t channels, const double* gram, const double* rhs, double* out) {
+  try {
+    sigcut::GramSystem sys;
+    sys.width = width;
+    sys.channels = channels;
+    sys.gram.assign(gram, gram + width * width);
+    sys.rhs.assign(rhs, rhs + width * channels);
+    const auto x = sigcut::solve_gram(sys);
+    std::memcpy(out, x.data(), x.size() * 8);
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_correct_coefficients(const double* a, int order, const uint64_t* shape, int channel_axis, uint64_t width,
+                             const uint64_t* const* factors, const double* coeffs, double* out) {
+  try {
+    const auto d = make_dec(order, shape, channel_axis, width, factors, coeffs);
+    const std::size_t numel = sigcut::DenseTensor::checked_numel(d.shape);
+    sigcut::DenseTensor t(d.shape, std::vector<double>(a, a + numel));
+    const auto c = sigcut::correct_coefficients(t, d);
+    std::memcpy(out, c.coefficients.data(), c.coefficients.size() * 8);
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_lstsq_decompose(const double* a, int order, const uint64_t* shape, int channel_axis,
+                        const oracle_config* cfg, oracle_output* out) {
+  try {
+    const auto sh = to_shape(order, shape);
+    const std::size_t numel = sigcut::DenseTensor::checked_numel(sh);
+    sigcut::DenseTensor t(sh, std::vector<double>(a, a + numel));
+    sigcut::DecomposeConfig dc;
+    dc.width = cfg->width;
+    dc.flush_width = cfg->flush_width;
+    dc.search.seed = cfg->seed;
+    dc.search.restarts = cfg->restarts;
+    dc.search.max_sweeps = cfg->max_sweeps;
+    dc.record_curve = true;
+    dc.min_value_fraction = cfg->min_value_fraction;
+    dc.max_factor_bytes = cfg->max_factor_bytes;
+    dc.method = sigcut::DecomposeConfig::Method::kLeastSquares;
+    auto [d, report] = channel_axis >= 0
+                           ? sigcut::rgb_scalars_decompose(t, dc, static_cast<std::size_t>(channel_axis))
+                           : sigcut::decompose(t, dc);
+    put_dec(d, out->signs, out->alpha);
+    for (std::size_t j = 0; j < d.width(); ++j) {
+      out->cut_value[j] = report.steps[j].cut_value;
+      out->resid_norm[j] = report.steps[j].residual_norm;
+    }
+    out->width_done = d.width();
+    out->input_norm = report.input_norm;
+    out->final_residual_norm = report.final_residual_norm;
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_write_scd(int order, const uint64_t* shape, int channel_axis, uint64_t width, const uint64_t* const* factors,
+                  const double* coeffs, int coeff_bits, uint8_t* buf, uint64_t cap, uint64_t* size) {
+  try {
+    const auto d = make_dec(order, shape, channel_axis, width, factors, coeffs);
+    std::ostringstream os(std::ios::binary);
+    sigcut::write_scd(os, d, coeff_bits);
+    const std::string b = os.str();
+    *size = b.size();
+    if (b.size() > cap) throw std::invalid_argument("buffer too small");
+    std::memcpy(buf, b.data(), b.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_read_scd(const uint8_t* buf, uint64_t size, int* order, uint64_t* shape, int* channel_axis, uint64_t* width,
+                 uint64_t** factors, double* coeffs) {
+  try {
+    std::istringstream is(std::string(reinterpret_cast<const char*>(buf), size), std::ios::binary);
+    const auto d = sigcut::read_scd(is);
+    *order = static_cast<int>(d.order());
+    for (std::size_t i = 0; i < d.order(); ++i) shape[i] = d.shape[i];
+    *channel_axis = d.channel_axis;
+    *width = d.width();
+    if (factors != nullptr && coeffs != nullptr) put_dec(d, factors, coeffs);
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_write_raw(int order, const uint64_t* shape, const double* data, int dtype, uint8_t* buf, uint64_t cap,
+                  uint64_t* size) {
+  try {
+    const auto sh = to_shape(order, shape);
+    const std::size_t numel = sigcut::DenseTensor::checked_numel(sh);
+    auto t = sigcut::DenseTensor::from_raw(sh, std::vector<double>(data, data + numel));
+    std::ostringstream os(std::ios::binary);
+    sigcut::write_raw(os, t, static_cast<sigcut::RawDType>(dtype));
+    const std::string b = os.str();
+    *size = b.size();
+    if (b.size() > cap) throw std::invalid_argument("buffer too small");
+    std::memcpy(buf, b.data(), b.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_read_raw(const uint8_t* buf, uint64_t size, int* order, uint64_t* shape, double* data) {
+  try {
+    std::istringstream is(std::string(reinterpret_cast<const char*>(buf), size), std::ios::binary);
+    const auto t = sigcut::read_raw(is);
+    *order = static_cast<int>(t.order());
+    for (std::size_t i = 0; i < t.order(); ++i) shape[i] = t.shape()[i];
+    if (data != nullptr) std::memcpy(data, t.data().data(), t.numel() * 8);
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
 }
 
 }  // extern "C"

@@ -613,3 +613,526 @@ int orc_signed_cut(const double* a, int order, const uint64_t* shape, uint64_t s
   if (n_sweep_values) *n_sweep_values = log.count;
   return 0;
 }
+
+/* ======================================================================== *
+ * Around the path: expansion, Gram system, least squares,
+ * SCD / DTEN containers.
+ * ======================================================================== */
+
+/* sign slot of every axis (-1 for the channel axis) */
+static int sign_slots(int order, int channel_axis, int* slot_of) {
+  int s = 0;
+  for (int i = 0; i < order; ++i) slot_of[i] = i == channel_axis ? -1 : s++;
+  return s;
+}
+
+/* accumulate_terms (decompose.hpp:128-180) via accumulate_expansion (:182-197):
+ * per element, acc = sum over terms j >= first of flip(scale*coef_j(ch), parity_j)
+ * in term order from 0.0, then data[e] += acc. */
+int orc_accumulate_expansion(int order, const uint64_t* shape, int channel_axis, uint64_t width,
+                             const uint64_t* const* factors, const double* coeffs, double scale,
+                             uint64_t first_term, double* data) {
+  size_t sh[8], numel;
+  int rc = check_shape(order, shape, sh, &numel);
+  if (rc) return rc;
+  if (channel_axis < -1 || channel_axis >= order) return fail(1, "CutDecomposition: channel axis out of range");
+  if (first_term >= width) return 0;
+  int slot_of[8];
+  sign_slots(order, channel_axis, slot_of);
+  const size_t q = channel_axis >= 0 ? sh[channel_axis] : 1;
+  const size_t w = (size_t)(width - first_term);
+  double* scaled = malloc(w * q * sizeof(double));
+  for (size_t j = 0; j < w; ++j)
+    for (size_t c = 0; c < q; ++c) scaled[j * q + c] = scale * coeffs[(first_term + j) * q + c];
+  size_t idx[8] = {0};
+  for (size_t e = 0; e < numel; ++e) {
+    const size_t ch = channel_axis >= 0 ? idx[channel_axis] : 0;
+    double acc = 0.0;
+    for (size_t j = 0; j < w; ++j) {
+      uint64_t xb = 0;
+      for (int d = 0; d < order; ++d)
+        if (slot_of[d] >= 0) xb ^= (uint64_t)bit_at(factors[slot_of[d]] + (first_term + j) * nwords(sh[d]), idx[d]);
+      acc += flip(scaled[j * q + ch], xb);
+    }
+    data[e] += acc;
+    for (int d = order - 1; d >= 0; --d) {
+      if (++idx[d] < sh[d]) break;
+      idx[d] = 0;
+    }
+  }
+  free(scaled);
+  return 0;
+}
+
+/* contract_term (decompose.hpp:218-260): out[ch] += flip(a[e], parity) in element order */
+static void contract_term(const double* a, int order, const size_t* sh, size_t numel, int channel_axis,
+                          const int* slot_of, const uint64_t* const* signs, double* out) {
+  const size_t q = channel_axis >= 0 ? sh[channel_axis] : 1;
+  for (size_t c = 0; c < q; ++c) out[c] = 0.0;
+  size_t idx[8] = {0};
+  for (size_t e = 0; e < numel; ++e) {
+    uint64_t xb = 0;
+    for (int d = 0; d < order; ++d)
+      if (slot_of[d] >= 0) xb ^= (uint64_t)bit_at(signs[slot_of[d]], idx[d]);
+    out[channel_axis >= 0 ? idx[channel_axis] : 0] += flip(a[e], xb);
+    for (int d = order - 1; d >= 0; --d) {
+      if (++idx[d] < sh[d]) break;
+      idx[d] = 0;
+    }
+  }
+}
+
+/* gram_column (decompose.hpp:367-381): products of per-axis sign dots, diag = prod n */
+static void gram_column(int order, const size_t* sh, const int* slot_of, const uint64_t* const* factors,
+                        size_t count, const uint64_t* const* new_signs, double* col) {
+  for (size_t j = 0; j < count; ++j) {
+    double g = 1.0;
+    for (int d = 0; d < order; ++d) {
+      if (slot_of[d] < 0) continue;
+      g *= (double)sign_dot(factors[slot_of[d]] + j * nwords(sh[d]), new_signs[slot_of[d]], sh[d]);
+    }
+    col[j] = g;
+  }
+  double diag = 1.0;
+  for (int d = 0; d < order; ++d)
+    if (slot_of[d] >= 0) diag *= (double)sh[d];
+  col[count] = diag;
+}
+
+int orc_build_gram(const double* a, int order, const uint64_t* shape, int channel_axis, uint64_t width,
+                   const uint64_t* const* factors, double* gram, double* rhs) {
+  size_t sh[8], numel;
+  int rc = check_shape(order, shape, sh, &numel);
+  if (rc) return rc;
+  int slot_of[8];
+  const int ns = sign_slots(order, channel_axis, slot_of);
+  const size_t q = channel_axis >= 0 ? sh[channel_axis] : 1;
+  double* col = malloc((width + 1) * sizeof(double));
+  const uint64_t* sig[8];
+  for (size_t j = 0; j < width; ++j) {
+    for (int s = 0, d = 0; d < order; ++d)
+      if (slot_of[d] >= 0) {
+        sig[s] = factors[s] + j * nwords(sh[d]);
+        ++s;
+      }
+    gram_column(order, sh, slot_of, factors, j, sig, col);
+    for (size_t i = 0; i < j; ++i) gram[i * width + j] = gram[j * width + i] = col[i];
+    gram[j * width + j] = col[j];
+    contract_term(a, order, sh, numel, channel_axis, slot_of, sig, rhs + j * q);
+  }
+  (void)ns;
+  free(col);
+  return 0;
+}
+
+/* cholesky / cholesky_solve / solve_gram (gram.hpp:48-107) */
+static int cholesky(double* m, size_t n) {
+  for (size_t j = 0; j < n; ++j) {
+    double d = m[j * n + j];
+    for (size_t p = 0; p < j; ++p) d -= m[j * n + p] * m[j * n + p];
+    if (!(d > 0.0) || !isfinite(d)) return 0;
+    const double l = sqrt(d);
+    m[j * n + j] = l;
+    for (size_t i = j + 1; i < n; ++i) {
+      double v = m[i * n + j];
+      for (size_t p = 0; p < j; ++p) v -= m[i * n + p] * m[j * n + p];
+      m[i * n + j] = v / l;
+    }
+  }
+  return 1;
+}
+
+static void cholesky_solve(const double* l, size_t n, double* x) {
+  for (size_t i = 0; i < n; ++i) {
+    double v = x[i];
+    for (size_t p = 0; p < i; ++p) v -= l[i * n + p] * x[p];
+    x[i] = v / l[i * n + i];
+  }
+  for (size_t i = n; i-- > 0;) {
+    double v = x[i];
+    for (size_t p = i + 1; p < n; ++p) v -= l[p * n + i] * x[p];
+    x[i] = v / l[i * n + i];
+  }
+}
+
+int orc_solve_gram(uint64_t width, uint64_t channels, const double* gram, const double* rhs, double* out) {
+  const size_t w = (size_t)width;
+  if (w == 0) return 0;
+  const double base_ridge = 1e-10 * gram[0];
+  double* factor = malloc(w * w * sizeof(double));
+  int ok = 0;
+  for (int attempt = 0; attempt < 5 && !ok; ++attempt) {
+    memcpy(factor, gram, w * w * sizeof(double));
+    if (attempt > 0) {
+      const double ridge = base_ridge * (double)(1 << (attempt - 1));
+      for (size_t j = 0; j < w; ++j) factor[j * w + j] += ridge;
+    }
+    ok = cholesky(factor, w);
+  }
+  if (!ok) {
+    free(factor);
+    return fail(2, "solve_gram: factorization failed");
+  }
+  double* x = malloc(w * sizeof(double));
+  for (size_t c = 0; c < channels; ++c) {
+    for (size_t j = 0; j < w; ++j) x[j] = rhs[j * channels + c];
+    cholesky_solve(factor, w, x);
+    for (size_t j = 0; j < w; ++j) out[j * channels + c] = x[j];
+  }
+  free(x);
+  free(factor);
+  return 0;
+}
+
+/* gram_quadratic (decompose.hpp:397-410) */
+static double gram_quadratic(size_t w, size_t ch, const double* gram, const double* rhs, const double* c) {
+  double value = 0.0;
+  for (size_t k = 0; k < ch; ++k) {
+    for (size_t i = 0; i < w; ++i) {
+      const double ci = c[i * ch + k];
+      value -= 2.0 * ci * rhs[i * ch + k];
+      double row = 0.0;
+      for (size_t j = 0; j < w; ++j) row += gram[i * w + j] * c[j * ch + k];
+      value += ci * row;
+    }
+  }
+  return value;
+}
+
+/* correct_coefficients (decompose.hpp:418-428) */
+int orc_correct_coefficients(const double* a, int order, const uint64_t* shape, int channel_axis, uint64_t width,
+                             const uint64_t* const* factors, const double* coeffs, double* out) {
+  size_t sh[8], numel;
+  int rc = check_shape(order, shape, sh, &numel);
+  if (rc) return rc;
+  const size_t q = channel_axis >= 0 ? sh[channel_axis] : 1;
+  const size_t w = (size_t)width;
+  if (w == 0) return 0;
+  double* gram = malloc(w * w * sizeof(double));
+  double* rhs = malloc(w * q * sizeof(double));
+  double* solved = malloc(w * q * sizeof(double));
+  rc = orc_build_gram(a, order, shape, channel_axis, width, factors, gram, rhs);
+  if (!rc) rc = orc_solve_gram(width, q, gram, rhs, solved);
+  if (!rc) {
+    const int better = gram_quadratic(w, q, gram, rhs, solved) <= gram_quadratic(w, q, gram, rhs, coeffs);
+    memcpy(out, better ? solved : coeffs, w * q * sizeof(double));
+  }
+  free(gram);
+  free(rhs);
+  free(solved);
+  return rc;
+}
+
+/* lstsq_decompose (decompose.hpp:434-469) and rgb_scalars_decompose (:485-536) */
+int orc_lstsq_decompose(const double* a, int order, const uint64_t* shape, int channel_axis,
+                        const oracle_config* cfg, oracle_output* out) {
+  size_t sh[8], numel;
+  int rc = check_shape(order, shape, sh, &numel);
+  if (rc) return rc;
+  for (size_t i = 0; i < numel; ++i)
+    if (!isfinite(a[i])) return fail(1, "DenseTensor: non-finite value");
+  size_t q = 1;
+  if (channel_axis >= 0) {
+    if (order < 2) return fail(1, "rgb_scalars_decompose: order >= 2 required");
+    if (channel_axis >= order) return fail(1, "rgb_scalars_decompose: channel axis out of range");
+    q = sh[channel_axis];
+    if (q > 8) return fail(1, "rgb_scalars_decompose: channel axis too long");
+  }
+  if (cfg->flush_width < 1) return fail(1, "DecomposeConfig: flush_width must be >= 1");
+  size_t per_term = q * sizeof(double);
+  for (int i = 0; i < order; ++i) per_term += nwords(sh[i]) * sizeof(uint64_t);
+  if (cfg->width > 0 && per_term > cfg->max_factor_bytes / cfg->width)
+    return fail(1, "DecomposeConfig: width exceeds the factor memory budget");
+  int slot_of[8];
+  sign_slots(order, channel_axis, slot_of);
+  const size_t w = (size_t)cfg->width;
+  double* residual = malloc(numel * sizeof(double));
+  memcpy(residual, a, numel * sizeof(double));
+  double* gram = NULL;
+  double* rhs = malloc((w ? w : 1) * q * sizeof(double));
+  double* col = malloc((w + 1) * sizeof(double));
+  double* coef = calloc((w ? w : 1) * q, sizeof(double));
+  out->input_norm = sqrt(squared_norm(a, numel));
+  out->final_residual_norm = out->input_norm;
+  cut_result res;
+  for (int i = 0; i < order; ++i) res.signs[i] = calloc(nwords(sh[i]), 8);
+  double first_value = 0.0;
+  size_t gw = 0;
+  for (size_t term = 0; term < w; ++term) {
+    rc = search_residual(residual, order, sh, numel, NULL, 0, orc_substream(cfg->seed, term), cfg->restarts,
+                         cfg->max_sweeps, &res, NULL);
+    if (rc) break;
+    if (term == 0) first_value = res.value;
+    else if (res.value < cfg->min_value_fraction * first_value) break;
+    const uint64_t* sig[8];
+    for (int d = 0; d < order; ++d)
+      if (slot_of[d] >= 0) sig[slot_of[d]] = res.signs[d];
+    gram_column(order, sh, slot_of, (const uint64_t* const*)out->signs, gw, sig, col);
+    double* grown = malloc((gw + 1) * (gw + 1) * sizeof(double));
+    for (size_t i = 0; i < gw; ++i) {
+      for (size_t j = 0; j < gw; ++j) grown[i * (gw + 1) + j] = gram[i * gw + j];
+      grown[i * (gw + 1) + gw] = col[i];
+      grown[gw * (gw + 1) + i] = col[i];
+    }
+    grown[gw * (gw + 1) + gw] = col[gw];
+    free(gram);
+    gram = grown;
+    contract_term(a, order, sh, numel, channel_axis, slot_of, sig, rhs + gw * q);
+    for (int d = 0; d < order; ++d)
+      if (slot_of[d] >= 0) memcpy(out->signs[slot_of[d]] + gw * nwords(sh[d]), res.signs[d], nwords(sh[d]) * 8);
+    ++gw;
+    rc = orc_solve_gram(gw, q, gram, rhs, coef);
+    if (rc) break;
+    memcpy(residual, a, numel * sizeof(double));
+    orc_accumulate_expansion(order, shape, channel_axis, gw, (const uint64_t* const*)out->signs, coef, -1.0, 0,
+                             residual);
+    out->final_residual_norm = sqrt(squared_norm(residual, numel));
+    out->cut_value[term] = res.value;
+    out->resid_norm[term] = out->final_residual_norm;
+    if (out->iterations) out->iterations[term] = res.iterations;
+  }
+  if (!rc) {
+    memcpy(out->alpha, coef, gw * q * sizeof(double));
+    out->width_done = gw;
+  }
+  for (int i = 0; i < order; ++i) free(res.signs[i]);
+  free(residual);
+  free(gram);
+  free(rhs);
+  free(col);
+  free(coef);
+  return rc;
+}
+
+/* ---- SCD / DTEN containers: inc/io.hpp -------------------------------- */
+
+typedef struct {
+  uint8_t* buf;
+  uint64_t cap, pos;
+} bytes_out;
+
+static void put(bytes_out* o, const void* p, size_t n) {
+  if (o->pos + n <= o->cap) memcpy(o->buf + o->pos, p, n);
+  o->pos += n;
+}
+static void put_u64le(bytes_out* o, uint64_t v) {
+  uint8_t b[8];
+  for (int i = 0; i < 8; ++i) b[i] = (uint8_t)(v >> (8 * i));
+  put(o, b, 8);
+}
+static void put_u8(bytes_out* o, uint8_t v) { put(o, &v, 1); }
+
+/* write_scd (io.hpp:142-166) */
+int orc_write_scd(int order, const uint64_t* shape, int channel_axis, uint64_t width, const uint64_t* const* factors,
+                  const double* coeffs, int coeff_bits, uint8_t* buf, uint64_t cap, uint64_t* size) {
+  if (coeff_bits != 32 && coeff_bits != 64) return fail(1, "write_scd: coeff_bits must be 32 or 64");
+  size_t sh[8], numel;
+  int rc = check_shape(order, shape, sh, &numel);
+  if (rc) return rc;
+  const size_t q = channel_axis >= 0 ? sh[channel_axis] : 1;
+  for (size_t i = 0; i < width * q; ++i)
+    if (!isfinite(coeffs[i])) return fail(1, "CutDecomposition: non-finite coefficient");
+  int slot_of[8];
+  sign_slots(order, channel_axis, slot_of);
+  bytes_out o = {buf, cap, 0};
+  put(&o, "SCD1", 4);
+  put_u8(&o, (uint8_t)order);
+  put_u8(&o, channel_axis >= 0 ? 1 : 0);
+  if (channel_axis >= 0) put_u8(&o, (uint8_t)channel_axis);
+  for (int i = 0; i < order; ++i) put_u64le(&o, shape[i]);
+  put_u64le(&o, width);
+  put_u8(&o, (uint8_t)coeff_bits);
+  for (uint64_t j = 0; j < width; ++j) {
+    for (size_t c = 0; c < q; ++c) {
+      uint64_t u;
+      if (coeff_bits == 64) {
+        memcpy(&u, &coeffs[j * q + c], 8);
+        put_u64le(&o, u);
+      } else {
+        const float f = (float)coeffs[j * q + c];
+        uint32_t v;
+        memcpy(&v, &f, 4);
+        uint8_t b[4];
+        for (int i = 0; i < 4; ++i) b[i] = (uint8_t)(v >> (8 * i));
+        put(&o, b, 4);
+      }
+    }
+    for (int d = 0; d < order; ++d) { /* put_sign_column, io.hpp:82-92 */
+      if (slot_of[d] < 0) continue;
+      const uint64_t* wds = factors[slot_of[d]] + j * nwords(sh[d]);
+      for (size_t byte = 0; byte < (sh[d] + 7) / 8; ++byte) put_u8(&o, (uint8_t)(wds[byte / 8] >> (8 * (byte % 8))));
+    }
+  }
+  *size = o.pos;
+  if (o.pos > cap) return fail(1, "buffer too small");
+  return 0;
+}
+
+typedef struct {
+  const uint8_t* buf;
+  uint64_t size, pos;
+} bytes_in;
+
+static int get(bytes_in* in, void* p, size_t n) {
+  if (in->pos + n > in->size) return fail(3, "truncated payload");
+  memcpy(p, in->buf + in->pos, n);
+  in->pos += n;
+  return 0;
+}
+static int get_u64le(bytes_in* in, uint64_t* v) {
+  uint8_t b[8];
+  if (get(in, b, 8)) return 3;
+  *v = 0;
+  for (int i = 0; i < 8; ++i) *v |= (uint64_t)b[i] << (8 * i);
+  return 0;
+}
+
+/* read_scd (io.hpp:168-213) */
+int orc_read_scd(const uint8_t* buf, uint64_t size, int* order, uint64_t* shape, int* channel_axis, uint64_t* width,
+                 uint64_t** factors, double* coeffs) {
+  bytes_in in = {buf, size, 0};
+  char magic[4];
+  uint8_t k, mode, cb, ca = 0;
+  if (get(&in, magic, 4)) return 3;
+  if (memcmp(magic, "SCD1", 4) != 0) return fail(3, "bad SCD magic");
+  if (get(&in, &k, 1)) return 3;
+  if (k == 0) return fail(3, "SCD order must be >= 1");
+  if (get(&in, &mode, 1)) return 3;
+  if (mode > 1) return fail(3, "bad SCD channel mode");
+  int chax = -1;
+  if (mode == 1) {
+    if (get(&in, &ca, 1)) return 3;
+    if (ca >= k) return fail(3, "SCD channel axis out of range");
+    chax = ca;
+  }
+  if (k > 8) return fail(3, "SCD order above the oracle's limit");
+  uint64_t numel = 1;
+  for (int i = 0; i < k; ++i) {
+    if (get_u64le(&in, &shape[i])) return 3;
+    if (shape[i] == 0) return fail(3, "bad SCD shape");
+    if (shape[i] > UINT64_MAX / numel) return fail(3, "SCD shape overflow");
+    numel *= shape[i];
+  }
+  uint64_t w;
+  if (get_u64le(&in, &w)) return 3;
+  if (get(&in, &cb, 1)) return 3;
+  if (cb != 32 && cb != 64) return fail(3, "bad SCD coefficient width");
+  *order = k;
+  *channel_axis = chax;
+  *width = w;
+  if (factors == NULL || coeffs == NULL) return 0;
+  const uint64_t q = chax >= 0 ? shape[chax] : 1;
+  for (uint64_t j = 0; j < w; ++j) {
+    for (uint64_t c = 0; c < q; ++c) {
+      double v;
+      if (cb == 64) {
+        uint64_t u;
+        if (get_u64le(&in, &u)) return 3;
+        memcpy(&v, &u, 8);
+      } else {
+        uint8_t b[4];
+        if (get(&in, b, 4)) return 3;
+        uint32_t u = 0;
+        for (int i = 0; i < 4; ++i) u |= (uint32_t)b[i] << (8 * i);
+        float f;
+        memcpy(&f, &u, 4);
+        v = (double)f;
+      }
+      if (!isfinite(v)) return fail(3, "non-finite SCD coefficient");
+      coeffs[j * q + c] = v;
+    }
+    for (int d = 0, s = 0; d < k; ++d) { /* get_sign_column, io.hpp:94-109 */
+      if (d == chax) continue;
+      const size_t nw = nwords(shape[d]);
+      uint64_t* wds = factors[s] + j * nw;
+      memset(wds, 0, nw * 8);
+      for (size_t byte = 0; byte < (shape[d] + 7) / 8; ++byte) {
+        uint8_t b;
+        if (get(&in, &b, 1)) return 3;
+        wds[byte / 8] |= (uint64_t)b << (8 * (byte % 8));
+      }
+      const size_t tail = shape[d] % 64;
+      if (tail != 0 && (wds[nw - 1] >> tail) != 0) return fail(3, "sign column has nonzero pad bits");
+      ++s;
+    }
+  }
+  return 0;
+}
+
+/* write_raw (io.hpp:226-246) */
+int orc_write_raw(int order, const uint64_t* shape, const double* data, int dtype, uint8_t* buf, uint64_t cap,
+                  uint64_t* size) {
+  size_t sh[8], numel;
+  int rc = check_shape(order, shape, sh, &numel);
+  if (rc) return rc;
+  bytes_out o = {buf, cap, 0};
+  put(&o, "DTEN", 4);
+  put_u8(&o, (uint8_t)order);
+  for (int i = 0; i < order; ++i) put_u64le(&o, shape[i]);
+  put_u8(&o, (uint8_t)dtype);
+  for (size_t e = 0; e < numel; ++e) {
+    if (dtype == 0) {
+      uint64_t u;
+      memcpy(&u, &data[e], 8);
+      put_u64le(&o, u);
+    } else if (dtype == 1) {
+      const float f = (float)data[e];
+      uint32_t v;
+      memcpy(&v, &f, 4);
+      uint8_t b[4];
+      for (int i = 0; i < 4; ++i) b[i] = (uint8_t)(v >> (8 * i));
+      put(&o, b, 4);
+    } else {
+      double v = data[e] < 0.0 ? 0.0 : (data[e] > 255.0 ? 255.0 : data[e]);
+      put_u8(&o, (uint8_t)lround(v));
+    }
+  }
+  *size = o.pos;
+  if (o.pos > cap) return fail(1, "buffer too small");
+  return 0;
+}
+
+/* read_raw (io.hpp:250-292) */
+int orc_read_raw(const uint8_t* buf, uint64_t size, int* order, uint64_t* shape, double* data) {
+  bytes_in in = {buf, size, 0};
+  char magic[4];
+  uint8_t k, dt;
+  if (get(&in, magic, 4)) return 3;
+  if (memcmp(magic, "DTEN", 4) != 0) return fail(3, "bad DTEN magic");
+  if (get(&in, &k, 1)) return 3;
+  if (k == 0) return fail(3, "DTEN order must be >= 1");
+  if (k > 8) return fail(3, "DTEN order above the oracle's limit");
+  uint64_t numel = 1;
+  for (int i = 0; i < k; ++i) {
+    if (get_u64le(&in, &shape[i])) return 3;
+    if (shape[i] == 0) return fail(3, "DTEN zero-length axis");
+    if (shape[i] > UINT64_MAX / numel) return fail(3, "DTEN shape overflow");
+    numel *= shape[i];
+  }
+  if (get(&in, &dt, 1)) return 3;
+  if (dt > 2) return fail(3, "bad DTEN dtype");
+  *order = k;
+  if (data == NULL) return 0;
+  for (uint64_t e = 0; e < numel; ++e) {
+    if (dt == 0) {
+      uint64_t u;
+      if (get_u64le(&in, &u)) return 3;
+      memcpy(&data[e], &u, 8);
+    } else if (dt == 1) {
+      uint8_t b[4];
+      if (get(&in, b, 4)) return 3;
+      uint32_t u = 0;
+      for (int i = 0; i < 4; ++i) u |= (uint32_t)b[i] << (8 * i);
+      float f;
+      memcpy(&f, &u, 4);
+      data[e] = (double)f;
+    } else {
+      uint8_t b;
+      if (get(&in, &b, 1)) return 3;
+      data[e] = (double)b;
+    }
+  }
+  for (uint64_t e = 0; e < numel; ++e)
+    if (!isfinite(data[e])) return fail(3, "invalid DTEN payload: DenseTensor: non-finite value");
+  return 0;
+}

@@ -13,10 +13,12 @@ from .api import (  # noqa: F401
     DeviceError,
     Engine,
     InvalidArgument,
+    IOError_,
     NotSupported,
     SearchConfig,
     SigcutRuntimeError,
     axial_greedy_cut,
+    correct_coefficients,
     decompose,
     default_engine,
     expand,
@@ -24,9 +26,15 @@ from .api import (  # noqa: F401
     greedy_decompose,
     greedy_signed_cut,
     lpt_schedule,
+    lstsq_decompose,
+    rgb_scalars_decompose,
+    solve_gram,
     start_vectors,
+    truncated,
     unpack_signs,
     width_for_compression,
 )
+
+from . import io  # noqa: F401,E402  (SCD / DTEN containers)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsigcut_b200.so")
 
-SC_OK, SC_INVALID_ARGUMENT, SC_RUNTIME_ERROR, SC_CUDA_ERROR, SC_NOT_SUPPORTED = 0, 1, 2, 3, 4
+SC_OK, SC_INVALID_ARGUMENT, SC_RUNTIME_ERROR, SC_CUDA_ERROR, SC_NOT_SUPPORTED, SC_IO_ERROR = 0, 1, 2, 3, 4, 5
 SC_F32, SC_F64 = 0, 1
 SC_SEED_PER_TERM, SC_SEED_DIRECT = 0, 1
 SC_MAX_ORDER = 8
@@ -72,7 +72,29 @@ class ScShardConfig(C.Structure):
     ]
 
 
+class ScFactors(C.Structure):
+    _fields_ = [
+        ("order", C.c_int32),
+        ("shape", P(u64)),
+        ("channel_axis", C.c_int32),
+        ("width", u64),
+        ("sign_words", P(u64) * SC_MAX_ORDER),
+        ("coefficients", P(C.c_double)),
+    ]
+
+
+class ScOpStats(C.Structure):
+    _fields_ = [
+        ("kernel_ms", C.c_double),
+        ("total_ms", C.c_double),
+        ("h2d_bytes", u64),
+        ("d2h_bytes", u64),
+        ("kernel_launches", C.c_int32),
+    ]
+
+
 SC_IPC_HANDLE_BYTES = 64
+B = P(C.c_uint8)
 
 # every symbol the header declares, with its ctypes signature
 SIGNATURES = {
@@ -93,6 +115,25 @@ SIGNATURES = {
     "sc_shard_reset": (C.c_int, [C.c_void_p]),
     "sc_greedy_decompose_sharded": (C.c_int, [C.c_void_p, P(ScProblem), P(ScShardConfig), P(ScResult)]),
     "sc_shard_close": (None, [C.c_void_p]),
+    "sc_accumulate_expansion": (C.c_int, [C.c_void_p, P(ScFactors), C.c_double, u64, u64, C.c_void_p, C.c_int32,
+                                          C.c_int32, P(ScOpStats)]),
+    "sc_gram_matrix": (C.c_int, [C.c_void_p, P(ScFactors), P(C.c_double), P(ScOpStats)]),
+    "sc_contract_terms": (C.c_int, [C.c_void_p, P(ScFactors), C.c_int32, C.c_void_p, C.c_int32, u64, u64,
+                                    P(C.c_double), P(ScOpStats)]),
+    "sc_solve_gram": (C.c_int, [u64, u64, P(C.c_double), P(C.c_double), P(C.c_double), C.c_char_p, C.c_size_t]),
+    "sc_correct_coefficients": (C.c_int, [C.c_void_p, P(ScFactors), C.c_int32, C.c_void_p, C.c_int32,
+                                          P(C.c_double), P(ScOpStats)]),
+    "sc_lstsq_decompose": (C.c_int, [C.c_void_p, P(ScProblem), C.c_int32, P(ScResult)]),
+    "sc_scd_size": (u64, [P(ScFactors), C.c_int]),
+    "sc_write_scd": (C.c_int, [P(ScFactors), C.c_int, B, u64, P(u64), C.c_char_p, C.c_size_t]),
+    "sc_read_scd_header": (C.c_int, [B, u64, P(C.c_int32), P(u64), P(C.c_int32), P(u64), P(C.c_int32),
+                                     C.c_char_p, C.c_size_t]),
+    "sc_read_scd": (C.c_int, [B, u64, P(P(u64)), P(C.c_double), C.c_char_p, C.c_size_t]),
+    "sc_dten_size": (u64, [C.c_int32, P(u64), C.c_int32]),
+    "sc_write_dten": (C.c_int, [C.c_int32, P(u64), P(C.c_double), C.c_int32, B, u64, P(u64), C.c_char_p,
+                                C.c_size_t]),
+    "sc_read_dten_header": (C.c_int, [B, u64, P(C.c_int32), P(u64), P(C.c_int32), C.c_char_p, C.c_size_t]),
+    "sc_read_dten": (C.c_int, [B, u64, P(C.c_double), C.c_char_p, C.c_size_t]),
 }
 
 _lib = None

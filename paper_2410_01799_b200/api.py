@@ -16,6 +16,12 @@ this module                    reference
 ``greedy_signed_cut``          search.hpp:259-263
 ``axial_greedy_cut`` (order 2) search.hpp:269-272
 ``width_for_compression``      metrics.hpp:55-63
+``expand`` / ``truncated``     decompose.hpp:266-270 / :103-115
+``accumulate_expansion``       decompose.hpp:182-197
+``build_gram``/``solve_gram``  decompose.hpp:383-393 / gram.hpp:83-107
+``correct_coefficients``       decompose.hpp:418-428
+``lstsq_decompose``            decompose.hpp:434-469
+``rgb_scalars_decompose``      decompose.hpp:485-536
 ``InvalidArgument``            ``std::invalid_argument``
 =============================  ==========================================
 
@@ -49,11 +55,16 @@ class NotSupported(RuntimeError):
     """Shape outside the kernels' envelope."""
 
 
+class IOError_(SigcutRuntimeError):
+    """sigcut::io_error analogue (io.hpp:22-24; derives from std::runtime_error)."""
+
+
 _ERRORS = {
     N.SC_INVALID_ARGUMENT: InvalidArgument,
     N.SC_RUNTIME_ERROR: SigcutRuntimeError,
     N.SC_CUDA_ERROR: DeviceError,
     N.SC_NOT_SUPPORTED: NotSupported,
+    N.SC_IO_ERROR: IOError_,
 }
 
 
@@ -110,8 +121,8 @@ class CutReport:
 @dataclass
 class CutDecomposition:
     shape: tuple
-    factors: List[np.ndarray]  # per axis: (width, words) uint64, SignMatrix columns
-    coefficients: np.ndarray   # alpha_k = c_k / numel
+    factors: List[np.ndarray]  # per SIGN axis (ascending): (width, words) uint64, SignMatrix columns
+    coefficients: np.ndarray   # (width,) alpha_k = c_k / numel; (width, channels) when channel_axis >= 0
     channel_axis: int = -1
 
     def width(self) -> int:
@@ -120,23 +131,41 @@ class CutDecomposition:
     def order(self) -> int:
         return len(self.shape)
 
+    def channels(self) -> int:
+        return int(self.shape[self.channel_axis]) if self.channel_axis >= 0 else 1
+
+    def sign_axes(self) -> List[int]:
+        return [i for i in range(len(self.shape)) if i != self.channel_axis]
+
+    def _c_struct(self):
+        """(ScFactors, keep-alive list) for the C ABI."""
+        sh = _shape_array(self.shape)
+        fs = [np.ascontiguousarray(f, np.uint64) for f in self.factors]
+        co = np.ascontiguousarray(self.coefficients, np.float64)
+        f = N.ScFactors()
+        f.order = len(self.shape)
+        f.shape = C.cast(sh, C.POINTER(N.u64))
+        f.channel_axis = self.channel_axis
+        f.width = self.width()
+        for i, a in enumerate(fs):
+            f.sign_words[i] = a.ctypes.data_as(C.POINTER(N.u64))
+        f.coefficients = co.ctypes.data_as(C.POINTER(C.c_double))
+        return f, [sh, fs, co]
+
+
+def truncated(d: CutDecomposition, new_width: int) -> CutDecomposition:
+    """First ``new_width`` terms (decompose.hpp:103-115)."""
+    if new_width > d.width():
+        raise InvalidArgument("truncated: width exceeds stored width")
+    return CutDecomposition(d.shape, [f[:new_width].copy() for f in d.factors],
+                            d.coefficients[:new_width].copy(), d.channel_axis)
+
 
 def unpack_signs(words: np.ndarray, n: int) -> np.ndarray:
     """Packed SignVector words -> +-1.0 vector (set bit = -1, LSB first)."""
     w = np.ascontiguousarray(words, dtype="<u8")
     bits = np.unpackbits(w.view(np.uint8), bitorder="little")[:n]
     return 1.0 - 2.0 * bits.astype(np.float64)
-
-
-def expand(d: CutDecomposition, first: int = 0, last: Optional[int] = None) -> np.ndarray:
-    """Host reconstruction sum_k alpha_k s_k t_k^T (reference expand(), decompose.hpp:266-270).
-
-    Test/analysis helper for matrices; not on the hot path."""
-    last = d.width() if last is None else last
-    m, n = d.shape
-    S = np.stack([unpack_signs(d.factors[0][k], m) for k in range(first, last)], 1) if last > first else np.zeros((m, 0))
-    T = np.stack([unpack_signs(d.factors[1][k], n) for k in range(first, last)], 1) if last > first else np.zeros((n, 0))
-    return (S * d.coefficients[first:last]) @ T.T
 
 
 def _shape_array(shape):
@@ -180,7 +209,7 @@ class Engine:
         no host copy of the input).  ``dtype`` ('f32'/'f64') selects the storage
         type of the remainder; default: float32 input -> f32, else f64."""
         if cfg.method not in ("greedy", 0):
-            raise InvalidArgument("only the greedy method runs on this engine")
+            raise InvalidArgument("Engine.run is the greedy driver; use lstsq_decompose for least squares")
         on_device = hasattr(a, "data_ptr") and getattr(a, "is_cuda", False)
         if on_device:
             import torch
@@ -262,6 +291,155 @@ class Engine:
         dec, rep, _ = self.run(a, cfg, dtype=dtype)
         return dec, rep
 
+    # -- around the path: expansion, Gram system, least squares ----------------
+    def accumulate_expansion(self, d: CutDecomposition, data=None, scale: float = 1.0, first_term: int = 0,
+                             last_term: Optional[int] = None, stats: Optional[dict] = None):
+        """``data += sum_{first <= j < last} flip(scale coef_j, parity_j)`` on the device,
+        bit-identical to detail::accumulate_expansion (decompose.hpp:182-197).
+
+        ``data``: None (zeros: expand), a numpy array (copied, returned) or a CUDA
+        float64 torch tensor (updated in place, no host copy)."""
+        f, keep = d._c_struct()
+        last = d.width() if last_term is None else int(last_term)
+        st = N.ScOpStats()
+        if data is not None and hasattr(data, "data_ptr") and getattr(data, "is_cuda", False):
+            import torch
+
+            if data.dtype != torch.float64 or not data.is_contiguous():
+                raise InvalidArgument("accumulate_expansion: device data must be contiguous float64")
+            self._check(self.lib.sc_accumulate_expansion(self.handle, C.byref(f), float(scale), int(first_term), last,
+                                                         C.c_void_p(data.data_ptr()), 1, 0, C.byref(st)))
+            out = data
+        else:
+            zero = data is None
+            out = np.zeros(d.shape) if zero else np.array(data, np.float64, copy=True).reshape(d.shape)
+            self._check(self.lib.sc_accumulate_expansion(self.handle, C.byref(f), float(scale), int(first_term), last,
+                                                         C.c_void_p(out.ctypes.data), 0, 1 if zero else 0, C.byref(st)))
+        del keep
+        if stats is not None:
+            stats.update(kernel_ms=st.kernel_ms, total_ms=st.total_ms, h2d_bytes=st.h2d_bytes,
+                         d2h_bytes=st.d2h_bytes, kernel_launches=st.kernel_launches)
+        return out
+
+    def expand(self, d: CutDecomposition, stats: Optional[dict] = None):
+        """Reconstruction sum_j coef_j (outer product of term j's signs) (decompose.hpp:266-270)."""
+        return self.accumulate_expansion(d, None, 1.0, 0, None, stats)
+
+    def gram_matrix(self, d: CutDecomposition) -> np.ndarray:
+        """G[i, j] = prod over sign axes of sign_dot (gram_column, decompose.hpp:367-381)."""
+        f, keep = d._c_struct()
+        w = d.width()
+        g = np.zeros((w, w))
+        self._check(self.lib.sc_gram_matrix(self.handle, C.byref(f), g.ctypes.data_as(C.POINTER(C.c_double)), None))
+        del keep
+        return g
+
+    def _input(self, a, dtype=None):
+        on_device = hasattr(a, "data_ptr") and getattr(a, "is_cuda", False)
+        if on_device:
+            import torch
+
+            if dtype is None:
+                dtype = "f32" if a.dtype == torch.float32 else "f64"
+            a = a.to(torch.float32 if dtype == "f32" else torch.float64).contiguous()
+            return a, a.data_ptr(), 1, dtype
+        arr = np.asarray(a)
+        if dtype is None:
+            dtype = "f32" if arr.dtype == np.float32 else "f64"
+        arr = np.ascontiguousarray(arr, np.float32 if dtype == "f32" else np.float64)
+        return arr, arr.ctypes.data, 0, dtype
+
+    def contract_terms(self, d: CutDecomposition, a, first_term: int = 0, count: Optional[int] = None,
+                       dtype: Optional[str] = None) -> np.ndarray:
+        """<sign outer product of term j, A> per channel (contract_term, decompose.hpp:218-260)."""
+        f, keep = d._c_struct()
+        count = d.width() - first_term if count is None else count
+        arr, ptr, on_dev, dtype = self._input(a, dtype)
+        out = np.zeros((max(count, 0), d.channels()))
+        self._check(self.lib.sc_contract_terms(self.handle, C.byref(f), N.SC_F32 if dtype == "f32" else N.SC_F64,
+                                               C.c_void_p(ptr), on_dev, first_term, count,
+                                               out.ctypes.data_as(C.POINTER(C.c_double)), None))
+        del keep, arr
+        return out if d.channel_axis >= 0 else out[:, 0]
+
+    def correct_coefficients(self, a, d: CutDecomposition, dtype: Optional[str] = None) -> CutDecomposition:
+        """Refit the coefficients with the signs fixed (decompose.hpp:418-428)."""
+        if tuple(np.shape(a)) != tuple(d.shape):
+            raise InvalidArgument("correct_coefficients: shape mismatch")
+        if d.width() == 0:
+            return d
+        f, keep = d._c_struct()
+        arr, ptr, on_dev, dtype = self._input(a, dtype)
+        out = np.zeros_like(np.asarray(d.coefficients, np.float64))
+        self._check(self.lib.sc_correct_coefficients(self.handle, C.byref(f), N.SC_F32 if dtype == "f32" else N.SC_F64,
+                                                     C.c_void_p(ptr), on_dev,
+                                                     out.ctypes.data_as(C.POINTER(C.c_double)), None))
+        del keep, arr
+        return CutDecomposition(d.shape, [x.copy() for x in d.factors], out, d.channel_axis)
+
+    def lstsq_decompose(self, a, cfg: DecomposeConfig, dtype: Optional[str] = None, channel_axis: int = -1):
+        """Least-squares decomposition (decompose.hpp:434-469); with channel_axis >= 0 the
+        scalar-channel variant rgb_scalars_decompose (:485-536).  The term search, the
+        Gram column, the contraction and the residual re-expansion run on the device;
+        the w x w Cholesky solve runs on the host like the reference's."""
+        arr, ptr, on_dev, dtype = self._input(a, dtype)
+        shape = tuple(int(x) for x in arr.shape)
+        if channel_axis is None:
+            channel_axis = len(shape) - 1
+        sh = _shape_array(shape)
+        prob = N.ScProblem()
+        prob.dtype = N.SC_F32 if dtype == "f32" else N.SC_F64
+        prob.order = len(shape)
+        prob.shape = C.cast(sh, C.POINTER(N.u64))
+        prob.data = ptr
+        prob.data_on_device = on_dev
+        prob.seed_mode = N.SC_SEED_PER_TERM
+        prob.width = int(cfg.width)
+        prob.flush_width = int(cfg.flush_width)
+        prob.seed = int(cfg.search.seed) & ((1 << 64) - 1)
+        prob.restarts = int(cfg.search.restarts)
+        prob.max_sweeps = int(cfg.search.max_sweeps)
+        prob.min_value_fraction = float(cfg.min_value_fraction)
+        prob.max_factor_bytes = int(cfg.max_factor_bytes)
+        q = shape[channel_axis] if channel_axis >= 0 else 1
+        axes = [i for i in range(len(shape)) if i != channel_axis]
+        w = max(int(cfg.width), 1)
+        signs = [np.zeros((w, (shape[i] + 63) // 64), np.uint64) for i in axes]
+        alpha = np.zeros((w, q))
+        cut, rn, rne = np.zeros(w), np.zeros(w), np.zeros(w)
+        sweeps = np.zeros(w, np.uint32)
+        res = N.ScResult()
+        for i, sgn in enumerate(signs):
+            res.sign_words[i] = sgn.ctypes.data_as(C.POINTER(N.u64))
+        res.alpha = alpha.ctypes.data_as(C.POINTER(C.c_double))
+        res.cut_value = cut.ctypes.data_as(C.POINTER(C.c_double))
+        res.resid_norm = rn.ctypes.data_as(C.POINTER(C.c_double))
+        res.resid_norm_exact = rne.ctypes.data_as(C.POINTER(C.c_double))
+        res.sweeps = sweeps.ctypes.data_as(C.POINTER(C.c_uint32))
+        self._check(self.lib.sc_lstsq_decompose(self.handle, C.byref(prob), int(channel_axis), C.byref(res)))
+        del arr
+        wd = int(res.width_done)
+        numel = float(np.prod([float(x) for x in shape]))
+        bits_per_term = 64 * q + sum(int(shape[i]) for i in axes)
+        steps = []
+        if cfg.record_curve:
+            steps = [CutStep(k + 1, float(cut[k]), float(rn[k]), (k + 1) * bits_per_term / (64.0 * numel))
+                     for k in range(wd)]
+        coef = alpha[:wd].copy() if channel_axis >= 0 else alpha[:wd, 0].copy()
+        dec = CutDecomposition(shape, [sgn[:wd].copy() for sgn in signs], coef, channel_axis)
+        rep = CutReport(steps, float(res.input_norm), float(res.final_residual_norm), wd,
+                        residual_norm_exact=rne[:wd].copy(), sweeps=sweeps[:wd].copy(), passes=int(res.passes),
+                        kernel_ms=float(res.kernel_ms), total_ms=float(res.total_ms),
+                        h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes),
+                        kernel_launches=int(res.kernel_launches))
+        rep._cut_values = cut[:wd].copy()
+        return dec, rep
+
+    def rgb_scalars_decompose(self, a, cfg: DecomposeConfig, channel_axis: Optional[int] = None,
+                              dtype: Optional[str] = None):
+        return self.lstsq_decompose(a, cfg, dtype=dtype,
+                                    channel_axis=(np.ndim(a) - 1) if channel_axis is None else channel_axis)
+
     def greedy_signed_cut(self, a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None) -> CutResult:
         """One cut searched with cfg.seed itself: order 2 is greedy_signed_cut
         (search.hpp:259-263), any other order axial_greedy_cut (:269-272)."""
@@ -287,9 +465,44 @@ def greedy_decompose(a, cfg: DecomposeConfig, dtype: Optional[str] = None):
 
 
 def decompose(a, cfg: DecomposeConfig, dtype: Optional[str] = None):
-    if cfg.method not in ("greedy", 0):
-        raise InvalidArgument("only DecomposeConfig.method == greedy is on the B200 path")
+    """Dispatch on the configured method (decompose.hpp:472-476)."""
+    if cfg.method in ("least_squares", "lstsq", 1):
+        return default_engine().lstsq_decompose(a, cfg, dtype=dtype)
     return greedy_decompose(a, cfg, dtype=dtype)
+
+
+def lstsq_decompose(a, cfg: DecomposeConfig, dtype: Optional[str] = None):
+    return default_engine().lstsq_decompose(a, cfg, dtype=dtype)
+
+
+def rgb_scalars_decompose(a, cfg: DecomposeConfig, channel_axis: Optional[int] = None, dtype: Optional[str] = None):
+    return default_engine().rgb_scalars_decompose(a, cfg, channel_axis=channel_axis, dtype=dtype)
+
+
+def expand(d: CutDecomposition) -> np.ndarray:
+    """Reconstruction on the device (decompose.hpp:266-270); width 0 gives zeros."""
+    return default_engine().expand(d)
+
+
+def correct_coefficients(a, d: CutDecomposition) -> CutDecomposition:
+    return default_engine().correct_coefficients(a, d)
+
+
+def solve_gram(gram, rhs) -> np.ndarray:
+    """Host Cholesky with the reference's ridge retry (gram.hpp:83-107)."""
+    g = np.ascontiguousarray(gram, np.float64)
+    r = np.ascontiguousarray(rhs, np.float64)
+    w = g.shape[0] if g.ndim == 2 else 0
+    out = np.zeros_like(r)
+    if w == 0:
+        return out
+    msg = C.create_string_buffer(256)
+    st = N.lib().sc_solve_gram(w, r.size // w, g.ctypes.data_as(C.POINTER(C.c_double)),
+                               r.ctypes.data_as(C.POINTER(C.c_double)), out.ctypes.data_as(C.POINTER(C.c_double)),
+                               msg, 256)
+    if st != N.SC_OK:
+        raise _ERRORS.get(st, SigcutRuntimeError)(msg.value.decode())
+    return out
 
 
 def greedy_signed_cut(a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None) -> CutResult:

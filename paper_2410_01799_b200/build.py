@@ -12,8 +12,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsigcut_b200.so")
-SOURCES = ["sweep.cu", "capi.cpp"]
-HEADERS = ["sweep.h", "rng.h"]
+SOURCES = ["sweep.cu", "ops.cu", "capi.cpp", "ops.cpp"]
+HEADERS = ["sweep.h", "rng.h", "ops.h", "ctx.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-cudart", "static",

@@ -19,55 +19,17 @@
 #include <vector>
 
 #include "../../include/sigcut_b200.h"
+#include "ctx.h"
 #include "rng.h"
 #include "sweep.h"
 
-struct sc_ctx {
-  int device = 0;
-  int num_sms = 0;
-  size_t smem_optin = 0;
-  size_t smem_per_sm = 0;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  std::string err;
-  // cached device arena and pinned staging
-  void* arena = nullptr;
-  size_t arena_bytes = 0;
-  void* pinned = nullptr;
-  size_t pinned_bytes = 0;
-  // row-sharded mode (sc_shard_*): this rank's exchange region and the peers'
-  struct Shard {
-    int world = 0, rank = 0, G = 0, dtype = 0;
-    long long pitch = 0;
-    int tw32 = 0;
-    uint64_t m_global = 0, row0 = 0, n = 0;
-    void* exch = nullptr;
-    size_t exch_bytes = 0, off_zpart = 0, off_slots = 0, off_tb64 = 0, off_ctr = 0;
-    void* peers[8] = {};
-    bool connected = false;
-  } shard;
-};
 
 namespace {
 
+using scb::set_err;
+
 constexpr const char* kVersion = "sigcut-b200 0.1 (sm_100a)";
 
-sc_status set_err(sc_ctx* ctx, sc_status st, const char* fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
-  if (ctx) ctx->err = buf;
-  return st;
-}
-
-#define SC_CUDA(ctx, call)                                                                \
-  do {                                                                                    \
-    cudaError_t e_ = (call);                                                              \
-    if (e_ != cudaSuccess)                                                                \
-      return set_err(ctx, SC_CUDA_ERROR, "%s failed: %s", #call, cudaGetErrorString(e_)); \
-  } while (0)
 
 uint64_t words64(uint64_t n) { return (n + 63) / 64; }
 
@@ -180,6 +142,7 @@ void sc_destroy(sc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  scb::pool_release(ctx);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -1,0 +1,88 @@
+// ctx.h -- the engine context behind the opaque sc_ctx handle, shared by the
+// C-ABI translation units (capi.cpp: decomposition; ops.cpp: expansion, Gram
+// system, containers).  Internal: not part of the public headers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <map>
+#include <string>
+#include <utility>
+
+#include "../../include/sigcut_b200.h"
+
+struct sc_ctx {
+  int device = 0;
+  int num_sms = 0;
+  size_t smem_optin = 0;
+  size_t smem_per_sm = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+  // cached device arena and pinned staging
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  // row-sharded mode (sc_shard_*): this rank's exchange region and the peers'
+  struct Shard {
+    int world = 0, rank = 0, G = 0, dtype = 0;
+    long long pitch = 0;
+    int tw32 = 0;
+    uint64_t m_global = 0, row0 = 0, n = 0;
+    void* exch = nullptr;
+    size_t exch_bytes = 0, off_zpart = 0, off_slots = 0, off_tb64 = 0, off_ctr = 0;
+    void* peers[8] = {};
+    bool connected = false;
+  } shard;
+  // auxiliary ops (expansion, Gram system, least squares): named grow-only
+  // device buffers, so a driver can hold several at once
+  std::map<std::string, std::pair<void*, size_t>> pool;
+};
+
+namespace scb {
+
+inline sc_status set_err(sc_ctx* ctx, sc_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return st;
+}
+
+// Named device buffer of at least `bytes` (contents kept unless it must grow).
+inline sc_status pool_get(sc_ctx* ctx, const std::string& name, size_t bytes, void** out) {
+  auto& e = ctx->pool[name];
+  if (e.second < bytes || e.first == nullptr) {
+    if (e.first) cudaFree(e.first);
+    e = {nullptr, 0};
+    const size_t want = bytes < 256 ? 256 : bytes;
+    cudaError_t err = cudaMalloc(&e.first, want);
+    if (err != cudaSuccess) {
+      e = {nullptr, 0};
+      return set_err(ctx, SC_CUDA_ERROR, "cudaMalloc(%zu) for %s failed: %s", want, name.c_str(),
+                     cudaGetErrorString(err));
+    }
+    e.second = want;
+  }
+  *out = e.first;
+  return SC_OK;
+}
+
+inline void pool_release(sc_ctx* ctx) {
+  for (auto& kv : ctx->pool)
+    if (kv.second.first) cudaFree(kv.second.first);
+  ctx->pool.clear();
+}
+
+}  // namespace scb
+
+#define SC_CUDA(ctx, call)                                                                      \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      return ::scb::set_err(ctx, SC_CUDA_ERROR, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)

@@ -103,4 +103,75 @@ dec_case("cap2_40x33", ref.fill_normal(22, 40 * 33).reshape(40, 33), 10, 22, flu
 a32 = ref.fill_normal(0, 256 * 256).reshape(256, 256).astype(np.float32).astype(np.float64)
 dec_case("f32in_256_w64", a32, 64, 0, flush=32, store_input=False)
 dec_case("order3_4x5x3", ref.fill_normal(404, 60).reshape(4, 5, 3), 12, 0, flush=4)    # :124-140
+
+
+# ---- around the path: expansion, Gram, least squares, SCD/DTEN ----
+def rand_factors(seed, shape, channel_axis, width):
+    axes = [i for i in range(len(shape)) if i != channel_axis]
+    fs = []
+    for k, i in enumerate(axes):
+        n = shape[i]
+        nw = (n + 63) // 64
+        f = ref.fill_u64(seed * 100 + k, max(width * nw, 1))[: width * nw].reshape(width, nw)
+        if n % 64:
+            f[:, -1] &= np.uint64((1 << (n % 64)) - 1)
+        fs.append(f)
+    q = shape[channel_axis] if channel_axis >= 0 else 1
+    co = ref.fill_normal(seed * 100 + 50, max(width * q, 1))[: width * q].reshape(width, q)
+    return fs, (co if channel_axis >= 0 else co[:, 0])
+
+
+def fac_dict(fs, co, shape, ch):
+    d = dict(shape=np.array(shape), channel_axis=ch, coeffs=co)
+    for i, f in enumerate(fs):
+        d[f"fac{i}"] = f
+    return d
+
+
+scd_cases = [("sample_4x4", (4, 4), -1, 16), ("order3_5x7x3", (5, 7, 3), -1, 9), ("rgb_6x10x3", (6, 10, 3), 2, 5),
+             ("chw_3x9x8", (3, 9, 8), 0, 4), ("vec_130", (130,), -1, 3), ("empty_7x9", (7, 9), -1, 0),
+             ("wide_3x200", (3, 200), -1, 7)]
+for i, (name, shape, ch, w) in enumerate(scd_cases):
+    fs, co = rand_factors(700 + i, shape, ch, w)
+    d = fac_dict(fs, co, shape, ch)
+    d["scd64"] = np.frombuffer(ref.write_scd(shape, fs, co, ch, 64), np.uint8)
+    d["scd32"] = np.frombuffer(ref.write_scd(shape, fs, co, ch, 32), np.uint8)
+    save("scd_" + name, **d)
+
+exp_cases = [("mat_37x70", (37, 70), -1, 40, 1.0, 0, False), ("resid_37x70", (37, 70), -1, 40, -1.0, 5, True),
+             ("order3_5x7x3", (5, 7, 3), -1, 33, 1.0, 0, True), ("rgb_6x10x3", (6, 10, 3), 2, 12, -1.0, 0, True),
+             ("chw_3x9x8", (3, 9, 8), 0, 9, 1.0, 2, False), ("vec_130", (130,), -1, 70, 1.0, 0, True),
+             ("wide_5x300", (5, 300), -1, 64, 1.0, 0, False), ("tall_150x3", (150, 3), -1, 31, -1.0, 0, True)]
+for i, (name, shape, ch, w, scale, first, base) in enumerate(exp_cases):
+    fs, co = rand_factors(800 + i, shape, ch, w)
+    d = fac_dict(fs, co, shape, ch)
+    a = ref.fill_normal(900 + i, int(np.prod(shape))).reshape(shape) if base else np.zeros(shape)
+    d.update(base=a, scale=scale, first_term=first,
+             out=ref.accumulate_expansion(shape, fs, co, data=a, scale=scale, first_term=first, channel_axis=ch))
+    save("expand_" + name, **d)
+
+gram_cases = [("mat_37x70", (37, 70), -1, 20), ("rgb_6x10x3", (6, 10, 3), 2, 9), ("order3_5x7x3", (5, 7, 3), -1, 11)]
+for i, (name, shape, ch, w) in enumerate(gram_cases):
+    fs, co = rand_factors(1000 + i, shape, ch, w)
+    d = fac_dict(fs, co, shape, ch)
+    a = ref.fill_normal(1100 + i, int(np.prod(shape))).reshape(shape)
+    g, r = ref.build_gram(a, fs, w, ch)
+    d.update(a=a, gram=g, rhs=r, corrected=ref.correct_coefficients(a, fs, co, ch))
+    save("gram_" + name, **d)
+
+lsq_cases = [("mat_24x20", (24, 20), -1, 6, 7), ("mat_40x33", (40, 33), -1, 12, 3), ("rgb_12x10x3", (12, 10, 3), 2, 5, 2),
+             ("order3_5x6x4", (5, 6, 4), -1, 5, 11), ("chw_3x8x7", (3, 8, 7), 0, 4, 5)]
+for i, (name, shape, ch, w, seed) in enumerate(lsq_cases):
+    a = ref.fill_normal(1200 + i, int(np.prod(shape))).reshape(shape)
+    r = ref.lstsq_decompose(a, w, seed=seed, channel_axis=ch)
+    d = dict(a=a, shape=np.array(shape), channel_axis=ch, width=w, seed=np.uint64(seed), alpha=r.alpha,
+             cut_value=r.cut_value, resid_norm=r.resid_norm, input_norm=r.input_norm,
+             final_residual_norm=r.final_residual_norm, width_done=r.width)
+    for k, f in enumerate(r.signs):
+        d[f"signs{k}"] = f
+    save("lsq_" + name, **d)
+
+x = np.array([[0.0, -0.0, 1.5, -2.25], [1e-300, 3.4e38, 255.4, 255.6], [-7.5, 0.5, 1.5, 2.5]])
+save("dten", a=x, f64=np.frombuffer(ref.write_raw(x, 0), np.uint8), f32=np.frombuffer(ref.write_raw(x, 1), np.uint8),
+     u8=np.frombuffer(ref.write_raw(x, 2), np.uint8))
 print("golden fixtures written to", HERE)

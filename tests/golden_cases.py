@@ -44,3 +44,15 @@ def dec_names():
 
 def cut_names():
     return sorted(os.path.basename(p)[4:-4] for p in glob.glob(os.path.join(GOLDEN, "cut_*.npz")))
+
+
+def names(prefix):
+    return sorted(os.path.basename(p)[len(prefix) + 1:-4] for p in glob.glob(os.path.join(GOLDEN, prefix + "_*.npz")))
+
+
+def factors_of(d):
+    """(shape, channel_axis, factors, coeffs) of a fixture written by fac_dict()."""
+    shape = tuple(int(x) for x in d["shape"])
+    ch = int(d["channel_axis"])
+    k = len(shape) - (1 if ch >= 0 else 0)
+    return shape, ch, [d[f"fac{i}"] for i in range(k)], d["coeffs"]

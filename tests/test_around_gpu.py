@@ -1,0 +1,141 @@
+"""GPU parity of the rows around the path, through the C ABI:
+
+* expansion / accumulate_expansion (decompose.hpp:128-197, :266-270): the
+  device result is BIT-IDENTICAL to the reference (same per-element term
+  order, exact sign flips);
+* Gram matrix (gram_column, decompose.hpp:367-381): integers, bit-identical;
+* contract_term (decompose.hpp:218-260): f64 sums in a parallel order, so
+  within 1e-12 of sum|a| (the reference sums sequentially);
+* correct_coefficients / lstsq_decompose / rgb_scalars_decompose: signs
+  bit-identical to the reference, coefficients and residual norms within
+  1e-9 relative (they inherit the contraction's last-bit differences);
+* SCD bytes of a device decomposition identical to the reference's file.
+"""
+import numpy as np
+import pytest
+
+import paper_2410_01799_b200 as sc
+from golden_cases import factors_of, load, names
+from paper_2410_01799_b200 import io as scio
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(x):
+    return np.ascontiguousarray(x, np.float64).view(np.uint64)
+
+
+def dec_of(d):
+    shape, ch, fs, co = factors_of(d)
+    return sc.CutDecomposition(shape, fs, co, ch)
+
+
+@pytest.mark.parametrize("name", names("expand"))
+def test_expansion_bit_identical_golden(engine, name):
+    d = load("expand_" + name)
+    dec = dec_of(d)
+    base = d["base"]
+    st = {}
+    out = engine.accumulate_expansion(dec, None if not base.any() else base, scale=float(d["scale"]),
+                                      first_term=int(d["first_term"]), stats=st)
+    assert (bits(out) == bits(d["out"])).all()
+    assert st["kernel_launches"] >= 1
+
+
+def test_expand_width0_and_truncated(engine, ref):
+    d = dec_of(load("expand_mat_37x70"))
+    z = engine.expand(sc.truncated(d, 0))
+    assert z.shape == (37, 70) and not z.any()
+    t = sc.truncated(d, 17)
+    assert (bits(engine.expand(t)) == bits(ref.accumulate_expansion(t.shape, t.factors, t.coefficients))).all()
+    with pytest.raises(sc.InvalidArgument):
+        sc.truncated(d, 41)
+
+
+def test_expansion_in_place_on_device_tensor(engine, ref):
+    import torch
+
+    d = dec_of(load("expand_resid_37x70"))
+    base = load("expand_resid_37x70")["base"]
+    t = torch.tensor(base, dtype=torch.float64, device="cuda")
+    engine.accumulate_expansion(d, t, scale=-1.0, first_term=5)
+    assert (bits(t.cpu().numpy()) == bits(load("expand_resid_37x70")["out"])).all()
+
+
+@pytest.mark.parametrize("shape,w,ragged", [((1024, 1024), 256, False), ((333, 517), 1000, True),
+                                            ((4096, 64), 65, True)])
+def test_expansion_of_device_decomposition_matches_reference(engine, ref, shape, w, ragged):
+    a = ref.fill_normal(41, shape[0] * shape[1]).reshape(shape)
+    cfg = sc.DecomposeConfig(width=min(w, 64), flush_width=1, search=sc.SearchConfig(seed=3))
+    dec, rep, rem = engine.run(a, cfg, dtype="f64", want_remainder=True)
+    if ragged:  # a longer synthetic term list (random signs, decaying coefficients) on the same shape
+        rng = np.random.default_rng(5)
+        fs = []
+        for n in shape:
+            nw = (n + 63) // 64
+            f = rng.integers(0, 1 << 63, size=(w, nw), dtype=np.uint64) * np.uint64(2)
+            f ^= rng.integers(0, 2, size=(w, nw), dtype=np.uint64)
+            if n % 64:
+                f[:, -1] &= np.uint64((1 << (n % 64)) - 1)
+            fs.append(f)
+        dec = sc.CutDecomposition(shape, fs, np.exp(-np.arange(w) / 300.0) * rng.uniform(0.5, 1.0, w))
+    mine = engine.expand(dec)
+    theirs = ref.accumulate_expansion(shape, dec.factors, dec.coefficients)
+    assert (bits(mine) == bits(theirs)).all()
+    if not ragged:  # A - expand(d) is the remainder up to rounding of the deflation order
+        assert np.abs(a - mine - rem).max() <= 1e-12 * np.abs(a).max()
+
+
+@pytest.mark.parametrize("name", names("gram"))
+def test_gram_bit_identical_and_contraction(engine, name):
+    d = load("gram_" + name)
+    dec = dec_of(d)
+    assert (engine.gram_matrix(dec) == d["gram"]).all()
+    rhs = engine.contract_terms(dec, d["a"])
+    scale = np.abs(d["a"]).sum()
+    assert np.abs(rhs - d["rhs"]).max() <= 1e-12 * scale
+    # f32 storage of A: the contraction widens exactly (DTEN f32 semantics)
+    a32 = d["a"].astype(np.float32)
+    r32 = engine.contract_terms(dec, a32)
+    assert np.abs(r32 - engine.contract_terms(dec, a32.astype(np.float64))).max() == 0.0
+    corr = engine.correct_coefficients(d["a"], dec)
+    np.testing.assert_allclose(corr.coefficients, d["corrected"], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", names("lsq"))
+def test_lstsq_matches_reference(engine, name):
+    d = load("lsq_" + name)
+    ch = int(d["channel_axis"])
+    cfg = sc.DecomposeConfig(width=int(d["width"]), record_curve=True, search=sc.SearchConfig(seed=int(d["seed"])))
+    dec, rep = engine.lstsq_decompose(d["a"], cfg, channel_axis=ch)
+    assert dec.width() == int(d["width_done"])
+    for i, f in enumerate(dec.factors):
+        assert (f == d[f"signs{i}"]).all(), f"axis slot {i}"
+    np.testing.assert_allclose(dec.coefficients, d["alpha"], rtol=1e-9, atol=1e-13)
+    np.testing.assert_allclose([s.residual_norm for s in rep.steps], d["resid_norm"], rtol=1e-10)
+    assert abs(rep.input_norm - float(d["input_norm"])) <= 1e-12 * float(d["input_norm"])
+    # least squares never does worse than greedy's coefficients on the same signs
+    assert rep.final_residual_norm <= rep.input_norm
+
+
+def test_lstsq_dispatch_and_validation(engine, ref):
+    a = load("lsq_mat_24x20")["a"]
+    cfg = sc.DecomposeConfig(width=3, method="least_squares", search=sc.SearchConfig(seed=7))
+    dec, rep = sc.decompose(a, cfg)
+    assert (dec.factors[0] == load("lsq_mat_24x20")["signs0"][:3]).all()
+    with pytest.raises(sc.InvalidArgument, match="channel axis too long"):
+        engine.rgb_scalars_decompose(np.ones((4, 4, 9)), sc.DecomposeConfig(width=1))
+    with pytest.raises(sc.InvalidArgument, match="order >= 2"):
+        engine.rgb_scalars_decompose(np.ones(5), sc.DecomposeConfig(width=1), channel_axis=0)
+
+
+def test_device_decomposition_scd_is_reference_file(engine, ref):
+    # sigcut decompose -> write_scd: the GPU decomposition's container bytes equal
+    # the reference's for the same input (f64 storage, bit-exact trajectory)
+    a = ref.fill_normal(77, 96 * 80).reshape(96, 80)
+    dec, rep = engine.greedy_decompose(a, sc.DecomposeConfig(width=24, search=sc.SearchConfig(seed=0x5CD15EED)),
+                                       dtype="f64")
+    od = ref.greedy_decompose(a, 24, seed=0x5CD15EED)
+    assert scio.write_scd(dec, 64) == ref.write_scd(a.shape, od.signs, od.alpha, -1, 64)
+    back = scio.read_scd(scio.write_scd(dec, 64))
+    assert (bits(engine.expand(back)) == bits(ref.accumulate_expansion(a.shape, od.signs, od.alpha))).all()
