@@ -325,13 +325,18 @@ class Engine:
         """Reconstruction sum_j coef_j (outer product of term j's signs) (decompose.hpp:266-270)."""
         return self.accumulate_expansion(d, None, 1.0, 0, None, stats)
 
-    def gram_matrix(self, d: CutDecomposition) -> np.ndarray:
+    def gram_matrix(self, d: CutDecomposition, stats: Optional[dict] = None) -> np.ndarray:
         """G[i, j] = prod over sign axes of sign_dot (gram_column, decompose.hpp:367-381)."""
         f, keep = d._c_struct()
         w = d.width()
         g = np.zeros((w, w))
-        self._check(self.lib.sc_gram_matrix(self.handle, C.byref(f), g.ctypes.data_as(C.POINTER(C.c_double)), None))
+        st = N.ScOpStats()
+        self._check(self.lib.sc_gram_matrix(self.handle, C.byref(f), g.ctypes.data_as(C.POINTER(C.c_double)),
+                                            C.byref(st)))
         del keep
+        if stats is not None:
+            stats.update(kernel_ms=st.kernel_ms, total_ms=st.total_ms, h2d_bytes=st.h2d_bytes,
+                         d2h_bytes=st.d2h_bytes, kernel_launches=st.kernel_launches)
         return g
 
     def _input(self, a, dtype=None):
