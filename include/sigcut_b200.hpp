@@ -18,7 +18,11 @@
 #include <sigcut/sigcut.hpp>
 
 #include <cstdint>
+#include <istream>
+#include <iterator>
+#include <ostream>
 #include <memory>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -37,6 +41,7 @@ enum class DType : std::int32_t { kF32 = SC_F32, kF64 = SC_F64 };
 namespace detail {
 [[noreturn]] inline void raise(sc_status st, const std::string& msg) {
   if (st == SC_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (st == SC_IO_ERROR) throw io_error(msg);
   throw std::runtime_error(msg);  // SC_RUNTIME_ERROR, SC_CUDA_ERROR, SC_NOT_SUPPORTED
 }
 }  // namespace detail
@@ -193,6 +198,180 @@ inline CutResult greedy_signed_cut(const DenseTensor& a, const SearchConfig& cfg
   res.value = o.result.second.steps.empty() ? 0.0 : o.result.second.steps[0].cut_value;
   res.iterations = o.sweeps.empty() ? 0 : o.sweeps[0];
   return res;
+}
+
+// ---------------------------------------------------------------------------
+// Around the path: reconstruction, least squares, containers.
+// ---------------------------------------------------------------------------
+namespace detail {
+
+/// Flat views of a CutDecomposition for the C ABI (sc_factors).
+struct FactorView {
+  std::vector<std::uint64_t> shape;
+  std::vector<std::vector<std::uint64_t>> words;  // per sign axis, term-major
+  sc_factors f{};
+
+  explicit FactorView(const CutDecomposition& d) : shape(d.shape.begin(), d.shape.end()) {
+    const std::size_t w = d.width();
+    for (const SignMatrix& m : d.factors) {
+      const std::size_t nw = SignVector::word_count(m.rows());
+      std::vector<std::uint64_t> v(w * nw);
+      for (std::size_t j = 0; j < w; ++j) {
+        const auto cw = m.column(j).words();
+        std::copy(cw.begin(), cw.end(), v.begin() + j * nw);
+      }
+      words.push_back(std::move(v));
+    }
+    f.order = static_cast<std::int32_t>(shape.size());
+    f.shape = shape.data();
+    f.channel_axis = d.channel_axis;
+    f.width = w;
+    for (std::size_t i = 0; i < words.size(); ++i) f.sign_words[i] = words[i].data();
+    f.coefficients = d.coefficients.data();
+  }
+};
+
+inline CutDecomposition from_words(const std::vector<std::size_t>& shape, int channel_axis, std::size_t width,
+                                   const std::vector<std::vector<std::uint64_t>>& words,
+                                   const std::vector<double>& coefficients) {
+  CutDecomposition d = CutDecomposition::with_shape(shape, channel_axis);
+  const auto axes = d.sign_axes();
+  for (std::size_t j = 0; j < width; ++j) {
+    std::vector<SignVector> signs;
+    for (std::size_t i = 0; i < axes.size(); ++i) {
+      const std::size_t n = shape[axes[i]], nw = SignVector::word_count(n);
+      signs.push_back(SignVector::from_words(
+          n, std::vector<std::uint64_t>(words[i].begin() + j * nw, words[i].begin() + (j + 1) * nw)));
+    }
+    d.append_term(signs, std::span<const double>(coefficients.data() + j * d.channels(), d.channels()));
+  }
+  return d;
+}
+
+}  // namespace detail
+
+/// Drop-in for sigcut::expand (decompose.hpp:266-270): bit-identical, on the device.
+inline DenseTensor expand(const CutDecomposition& d, Engine& eng = Engine::default_engine()) {
+  detail::FactorView v(d);
+  std::vector<double> out(DenseTensor::checked_numel(d.shape));
+  eng.check(sc_accumulate_expansion(eng.get(), &v.f, 1.0, 0, d.width(), out.data(), 0, 1, nullptr));
+  return DenseTensor::from_raw(d.shape, std::move(out));
+}
+
+/// Drop-in for detail::accumulate_expansion (decompose.hpp:182-197).
+inline void accumulate_expansion(DenseTensor& out, const CutDecomposition& d, double scale,
+                                 std::size_t first_term = 0, Engine& eng = Engine::default_engine()) {
+  detail::FactorView v(d);
+  eng.check(sc_accumulate_expansion(eng.get(), &v.f, scale, first_term, d.width(), out.data().data(), 0, 0, nullptr));
+}
+
+/// Drop-in for sigcut::correct_coefficients (decompose.hpp:418-428).
+inline CutDecomposition correct_coefficients(const DenseTensor& a, const CutDecomposition& d,
+                                             Engine& eng = Engine::default_engine()) {
+  if (a.shape() != d.shape) throw std::invalid_argument("correct_coefficients: shape mismatch");
+  if (d.width() == 0) return d;
+  detail::FactorView v(d);
+  CutDecomposition out = d;
+  eng.check(sc_correct_coefficients(eng.get(), &v.f, SC_F64, a.data().data(), 0, out.coefficients.data(), nullptr));
+  return out;
+}
+
+namespace detail {
+inline std::pair<CutDecomposition, CutReport> lstsq_run(const DenseTensor& a, const DecomposeConfig& cfg,
+                                                        int channel_axis, Engine& eng) {
+  std::vector<std::uint64_t> shp(a.shape().begin(), a.shape().end());
+  sc_problem p{};
+  p.dtype = SC_F64;
+  p.order = static_cast<std::int32_t>(shp.size());
+  p.shape = shp.data();
+  p.data = a.data().data();
+  p.seed_mode = SC_SEED_PER_TERM;
+  p.width = cfg.width;
+  p.flush_width = cfg.flush_width;
+  p.seed = cfg.search.seed;
+  p.restarts = cfg.search.restarts;
+  p.max_sweeps = cfg.search.max_sweeps;
+  p.min_value_fraction = cfg.min_value_fraction;
+  p.max_factor_bytes = cfg.max_factor_bytes;
+  const std::size_t w = cfg.width, k = shp.size();
+  const std::size_t q = channel_axis >= 0 && static_cast<std::size_t>(channel_axis) < k ? shp[channel_axis] : 1;
+  sc_result r{};
+  std::vector<std::vector<std::uint64_t>> words;
+  for (std::size_t i = 0; i < k; ++i)
+    if (static_cast<int>(i) != channel_axis) words.emplace_back(std::max<std::size_t>(w, 1) * SignVector::word_count(shp[i]));
+  for (std::size_t i = 0; i < words.size(); ++i) r.sign_words[i] = words[i].data();
+  std::vector<double> alpha(std::max<std::size_t>(w, 1) * q), cut(std::max<std::size_t>(w, 1)), rn(cut.size());
+  r.alpha = alpha.data();
+  r.cut_value = cut.data();
+  r.resid_norm = rn.data();
+  eng.check(sc_lstsq_decompose(eng.get(), &p, channel_axis, &r));
+  const std::size_t wd = r.width_done;
+  alpha.resize(wd * q);
+  CutDecomposition d = from_words(a.shape(), channel_axis, wd, words, alpha);
+  CutReport rep;
+  rep.input_norm = r.input_norm;
+  rep.final_residual_norm = r.final_residual_norm;
+  const StorageModel model{64, 64, a.shape(), channel_axis};
+  if (cfg.record_curve)
+    for (std::size_t j = 0; j < wd; ++j) rep.steps.push_back(CutStep{j + 1, cut[j], rn[j], compression_rate(j + 1, model)});
+  rep.width = wd;
+  return {std::move(d), std::move(rep)};
+}
+}  // namespace detail
+
+/// Drop-in for sigcut::lstsq_decompose (decompose.hpp:434-469).
+inline std::pair<CutDecomposition, CutReport> lstsq_decompose(const DenseTensor& a, const DecomposeConfig& cfg,
+                                                              Engine& eng = Engine::default_engine()) {
+  return detail::lstsq_run(a, cfg, -1, eng);
+}
+
+/// Drop-in for sigcut::rgb_scalars_decompose (decompose.hpp:485-536).
+inline std::pair<CutDecomposition, CutReport> rgb_scalars_decompose(const DenseTensor& a, const DecomposeConfig& cfg,
+                                                                    std::optional<std::size_t> channel_axis = {},
+                                                                    Engine& eng = Engine::default_engine()) {
+  if (a.order() < 2) throw std::invalid_argument("rgb_scalars_decompose: order >= 2 required");
+  return detail::lstsq_run(a, cfg, static_cast<int>(channel_axis.value_or(a.order() - 1)), eng);
+}
+
+/// Drop-in for sigcut::write_scd (io.hpp:142-166): byte-identical stream.
+inline void write_scd(std::ostream& os, const CutDecomposition& d, int coeff_bits = 64) {
+  detail::FactorView v(d);
+  std::vector<std::uint8_t> buf(sc_scd_size(&v.f, coeff_bits) + 1);
+  std::uint64_t n = 0;
+  char msg[256];
+  const sc_status st = sc_write_scd(&v.f, coeff_bits, buf.data(), buf.size(), &n, msg, sizeof msg);
+  if (st != SC_OK) detail::raise(st, msg);
+  os.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(n));
+  if (!os) throw io_error("write failed");
+}
+
+/// Drop-in for sigcut::read_scd (io.hpp:168-213) over the rest of the stream.
+inline CutDecomposition read_scd(std::istream& is) {
+  const std::string bytes((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+  const auto* p = reinterpret_cast<const std::uint8_t*>(bytes.data());
+  std::int32_t order = 0, chax = -1, cbits = 0;
+  std::uint64_t shape[SC_MAX_ORDER] = {}, width = 0;
+  char msg[256];
+  sc_status st = sc_read_scd_header(p, bytes.size(), &order, shape, &chax, &width, &cbits, msg, sizeof msg);
+  if (st != SC_OK) detail::raise(st, msg);
+  std::vector<std::size_t> shp(shape, shape + order);
+  const std::size_t q = chax >= 0 ? shp[chax] : 1;
+  std::size_t per_term = q * static_cast<std::size_t>(cbits) / 8;
+  for (int i = 0; i < order; ++i)
+    if (i != chax) per_term += (shp[i] + 7) / 8;
+  if (width > 0 && per_term > 0 && width > bytes.size() / per_term + 1) throw io_error("truncated payload");
+  std::vector<std::vector<std::uint64_t>> words;
+  std::vector<std::uint64_t*> ptrs;
+  for (int i = 0; i < order; ++i)
+    if (i != chax) words.emplace_back(std::max<std::uint64_t>(width, 1) * SignVector::word_count(shp[i]));
+  for (auto& w : words) ptrs.push_back(w.data());
+  std::vector<double> co(std::max<std::uint64_t>(width, 1) * q);
+  st = sc_read_scd(p, bytes.size(), ptrs.data(), co.data(), msg, sizeof msg);
+  if (st != SC_OK) detail::raise(st, msg);
+  co.resize(width * q);
+  CutDecomposition d = detail::from_words(shp, chax, width, words, co);
+  d.validate();
+  return d;
 }
 
 }  // namespace sigcut::b200

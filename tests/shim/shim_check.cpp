@@ -5,6 +5,7 @@
 // is present; run by tests/test_gpu_parity.py::test_cpp_shim_matches_reference.
 #include <cmath>
 #include <cstdio>
+#include <sstream>
 #include <stdexcept>
 
 #include <sigcut/sigcut.hpp>
@@ -78,6 +79,60 @@ int main() {
     try { greedy_decompose(a, bad); } catch (const std::invalid_argument&) { ref_threw = true; }
     try { b200::greedy_decompose(a, bad, b200::DType::kF64, eng); } catch (const std::invalid_argument&) { b200_threw = true; }
     CHECK(ref_threw && b200_threw, "invalid_argument mapping (%d, %d)", ref_threw, b200_threw);
+  }
+  {  // expansion: bit-identical DenseTensor (decompose.hpp:266-270)
+    const DenseTensor a = randn({77, 150}, 21);
+    DecomposeConfig cfg;
+    cfg.width = 40;
+    auto [rd, rr] = greedy_decompose(a, cfg);
+    CHECK(expand(rd) == b200::expand(rd, eng), "expand differs");
+    DenseTensor r1 = a, r2 = a;
+    detail::accumulate_expansion(r1, rd, -1.0, 3);
+    b200::accumulate_expansion(r2, rd, -1.0, 3, eng);
+    CHECK(r1 == r2, "accumulate_expansion differs");
+    // SCD: the drop-in writer emits the reference's bytes; its reader round-trips
+    for (int bits : {64, 32}) {
+      std::ostringstream o1(std::ios::binary), o2(std::ios::binary);
+      write_scd(o1, rd, bits);
+      b200::write_scd(o2, rd, bits);
+      CHECK(o1.str() == o2.str(), "scd bytes (%d-bit)", bits);
+      std::istringstream i1(o1.str(), std::ios::binary);
+      CHECK(b200::read_scd(i1) == [&] { std::istringstream i(o1.str(), std::ios::binary); return read_scd(i); }(),
+            "read_scd (%d-bit)", bits);
+    }
+    bool io_ref = false, io_b200 = false;
+    std::string junk = "SCD1\x02";
+    try { std::istringstream i(junk, std::ios::binary); read_scd(i); } catch (const io_error&) { io_ref = true; }
+    try { std::istringstream i(junk, std::ios::binary); b200::read_scd(i); } catch (const io_error&) { io_b200 = true; }
+    CHECK(io_ref && io_b200, "io_error mapping (%d, %d)", io_ref, io_b200);
+  }
+  {  // least squares and scalar channels: same signs, coefficients to 1e-9
+    const DenseTensor a = randn({30, 26}, 31);
+    DecomposeConfig cfg;
+    cfg.width = 6;
+    cfg.record_curve = true;
+    cfg.search.seed = 4;
+    auto [rd, rr] = lstsq_decompose(a, cfg);
+    auto [gd, gr] = b200::lstsq_decompose(a, cfg, eng);
+    CHECK(rd.width() == gd.width(), "lstsq width");
+    for (std::size_t i = 0; i < rd.factors.size(); ++i) CHECK(rd.factors[i] == gd.factors[i], "lstsq factor %zu", i);
+    for (std::size_t k = 0; k < rd.coefficients.size() && k < gd.coefficients.size(); ++k)
+      CHECK(std::fabs(rd.coefficients[k] - gd.coefficients[k]) <= 1e-9 * std::fabs(rd.coefficients[k]) + 1e-13,
+            "lstsq coef %zu", k);
+    CHECK(std::fabs(rr.final_residual_norm - gr.final_residual_norm) <= 1e-10 * rr.input_norm, "lstsq norm");
+    const DenseTensor img = randn({14, 11, 3}, 32);
+    auto [rg, rgr] = rgb_scalars_decompose(img, cfg);
+    auto [gg, ggr] = b200::rgb_scalars_decompose(img, cfg, {}, eng);
+    CHECK(rg.channel_axis == gg.channel_axis && rg.width() == gg.width(), "rgb layout");
+    for (std::size_t i = 0; i < rg.factors.size(); ++i) CHECK(rg.factors[i] == gg.factors[i], "rgb factor %zu", i);
+    for (std::size_t k = 0; k < rg.coefficients.size() && k < gg.coefficients.size(); ++k)
+      CHECK(std::fabs(rg.coefficients[k] - gg.coefficients[k]) <= 1e-9 * std::fabs(rg.coefficients[k]) + 1e-13,
+            "rgb coef %zu", k);
+    const CutDecomposition rc = correct_coefficients(a, rd);
+    const CutDecomposition gc = b200::correct_coefficients(a, rd, eng);
+    for (std::size_t k = 0; k < rc.coefficients.size(); ++k)
+      CHECK(std::fabs(rc.coefficients[k] - gc.coefficients[k]) <= 1e-9 * std::fabs(rc.coefficients[k]) + 1e-13,
+            "correct_coefficients %zu", k);
   }
   std::printf(fails ? "SHIM FAILED (%d)\n" : "SHIM OK\n", fails);
   return fails ? 1 : 0;
