@@ -184,3 +184,21 @@ def test_solve_gram_ridge_and_failure_like_reference(ref):
     assert (bits(sc.solve_gram(g, r)) == bits(ref.solve_gram(g, r))).all()
     with pytest.raises(sc.SigcutRuntimeError, match="factorization failed"):
         sc.solve_gram(np.array([[-1.0]]), np.array([1.0]))
+
+
+def test_workload_generator_is_reference_stream(orc):
+    from paper_2410_01799_b200.workloads import Xoshiro256pp
+
+    r = Xoshiro256pp(2)
+    assert (np.array([r.next_u64() for _ in range(9)], np.uint64) == orc.fill_u64(2, 9)).all()
+    r = Xoshiro256pp(0x5CD15EED)
+    assert (np.array([r.next_f64() for _ in range(9)]) == orc.fill_f64(0x5CD15EED, 9)).all()
+
+
+def test_c3_blob_image_recipe():
+    from paper_2410_01799_b200.workloads import c3_blob_image
+
+    img = c3_blob_image(40, 30)
+    assert img.shape == (40, 30, 3) and img.dtype == np.float32
+    assert img.min() >= 0.0 and img.max() <= 1.0
+    assert (c3_blob_image(40, 30) == img).all()  # seeded, deterministic
