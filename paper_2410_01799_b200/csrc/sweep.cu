@@ -1206,23 +1206,44 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
 __device__ __forceinline__ uint32_t axbit(const KParams& p, const uint32_t* sax, int j, int idx) {
   return (sax[p.ax_off[j] + (idx >> 5)] >> (idx & 31)) & 1u;
 }
-// t word q of kron(s_1, ..., s_{k-1}) over the N' columns
+// t word q of kron(s_1, ..., s_{k-1}) over the N' columns: the multi-index of
+// the word's first column is decomposed once (32-bit), then advanced as an
+// odometer whose running parity is updated incrementally.
 __device__ uint32_t kron_word(const KParams& p, const uint32_t* sax, int q) {
+  const int col0 = q * 32;
+  if (col0 >= p.n) return 0u;
+  int idx[7];
+  uint32_t xb = 0;
+  int c = col0;
+  for (int j = p.kax - 1; j >= 0; --j) {
+    const int nj = p.ax_n[j];
+    idx[j] = c % nj;
+    c /= nj;
+    xb ^= axbit(p, sax, j, idx[j]);
+  }
   uint32_t word = 0;
-  for (int b = 0; b < 32; ++b) {
-    long long col = static_cast<long long>(q) * 32 + b;
-    if (col >= p.n) break;
-    uint32_t xb = 0;
-    for (int j = p.kax - 1; j >= 0; --j) {
-      const int nj = p.ax_n[j];
-      xb ^= axbit(p, sax, j, static_cast<int>(col % nj));
-      col /= nj;
-    }
+  const int nb = min(32, p.n - col0);
+  for (int b = 0; b < nb; ++b) {
     word |= xb << b;
+    for (int j = p.kax - 1; j >= 0; --j) {  // advance the odometer by one column
+      xb ^= axbit(p, sax, j, idx[j]);
+      if (++idx[j] < p.ax_n[j]) {
+        xb ^= axbit(p, sax, j, idx[j]);
+        break;
+      }
+      idx[j] = 0;
+      xb ^= axbit(p, sax, j, 0);
+    }
   }
   return word;
 }
 
+// The trailing-axis update of one sweep.  Outputs of axis i are spread over the
+// CTA by their count n_i: few outputs (n_i <= CW) use the whole CTA per output,
+// otherwise groups of T = 32 / 2^k lanes share one output (T ~ CT / n_i), each
+// group summing a strided slice of the other axes' combinations and combining
+// with a fixed butterfly -- so thousands of L2 loads are in flight instead of a
+// few warps walking the slices serially.  All index arithmetic is 32-bit.
 template <int CW>
 __device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_t* tws, Ctl* ctl, int P) {
   constexpr int CT = CW * 32;
@@ -1230,52 +1251,71 @@ __device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_
   const int kax = p.kax;
   const double* Z = p.zfull;
   unsigned* errp = p.err_pass;
+  int zstride[7];
+  {
+    int st = 1;
+    for (int j = kax - 1; j >= 0; --j) {
+      zstride[j] = st;
+      st *= p.ax_n[j];
+    }
+  }
   double csum = 0.0;
   if (kax == 0 && tid == 0) csum = __ldcg(Z);  // order 1: c = <s_0, a> = Z[0]
   for (int i = 0; i < kax; ++i) {
     const int ni = p.ax_n[i];
-    long long inner = 1;
-    for (int j = i + 1; j < kax; ++j) inner *= p.ax_n[j];
-    const long long other = static_cast<long long>(p.n) / ni;
+    const int other = p.n / ni;
     uint32_t* wi = sax + p.ax_off[i];
     const int nwi = (ni + 31) / 32;
-    // Z entry (index_i = q, r-th combination of the other axes, last fastest), signed
-    auto term = [&](int q, long long r) -> double {
-      long long flat = static_cast<long long>(q) * inner, stride = 1;
+    // signed Z entry of (index_i = q, r-th combination of the other axes, last fastest)
+    auto term = [&](int q, int r) -> double {
+      if (kax == 2) {  // order 3 (the common case): Z is n_1 x n_2, no index arithmetic
+        const int j = 1 - i;
+        return flipd(__ldcg(Z + (i == 0 ? q * p.ax_n[1] + r : r * p.ax_n[1] + q)), axbit(p, sax, j, r) << 31);
+      }
+      int flat = q * zstride[i];
       uint32_t xb = 0;
       for (int j = kax - 1; j >= 0; --j) {
+        if (j == i) continue;
         const int nj = p.ax_n[j];
-        if (j != i) {
-          const int ij = static_cast<int>(r % nj);
-          r /= nj;
-          flat += ij * stride;
-          xb ^= axbit(p, sax, j, ij);
-        }
-        stride *= nj;
+        const int ij = r % nj;
+        r /= nj;
+        flat += ij * zstride[j];
+        xb ^= axbit(p, sax, j, ij);
       }
       return flipd(__ldcg(Z + flat), xb << 31);
     };
-    if (other <= 64) {  // one output per thread, r ascending
-      for (int base = 0; base < ni; base += CT) {
-        const int q = base + tid;
+    for (int wq = tid; wq < nwi; wq += CT) wi[wq] = 0u;
+    consumer_sync(CT);
+    if (ni <= CW) {  // whole CTA per output
+      for (int q = 0; q < ni; ++q) {
+        double v = 0.0;
+#pragma unroll 4
+        for (int r = tid; r < other; r += CT) v += term(q, r);
+        v = warp_sum(v);
+        if (lane == 0) ctl->cred[warp] = v;
+        consumer_sync(CT);
+        if (tid == 0) {
+          double t = 0.0;
+          for (int w = 0; w < CW; ++w) t += ctl->cred[w];
+          if (!isfinite(t)) atomicMin(errp + ERR_Z, static_cast<unsigned>(P));
+          if (t < 0.0) wi[q >> 5] |= 1u << (q & 31);
+          if (i == kax - 1) csum += fabs(t);
+        }
+        consumer_sync(CT);
+      }
+    } else {  // T lanes per output
+      int T = 32;
+      while (T > 1 && ni * T > 2 * CT) T >>= 1;
+      const int groups = CT / T, sub = tid & (T - 1);
+      for (int q = tid / T; q - tid / T < ni; q += groups) {
         const bool ok = q < ni;
         double v = 0.0;
-        if (ok)
-          for (long long r = 0; r < other; ++r) v += term(q, r);
-        if (ok && !isfinite(v)) atomicMin(errp + ERR_Z, static_cast<unsigned>(P));
-        const unsigned word = __ballot_sync(0xffffffffu, ok && v < 0.0);
-        const int wq = (base >> 5) + warp;
-        if (lane == 0 && wq < nwi) wi[wq] = word;
-        if (i == kax - 1 && ok) csum += fabs(v);
-      }
-    } else {  // one output per warp, lanes stride r, fixed butterfly
-      for (int wq = tid; wq < nwi; wq += CT) wi[wq] = 0u;
-      consumer_sync(CT);
-      for (int q = warp; q < ni; q += CW) {
-        double v = 0.0;
-        for (long long r = lane; r < other; r += 32) v += term(q, r);
-        v = warp_sum(v);
-        if (lane == 0) {
+        if (ok) {
+#pragma unroll 4
+          for (int r = sub; r < other; r += T) v += term(q, r);
+        }
+        for (int o = T >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (ok && sub == 0) {
           if (!isfinite(v)) atomicMin(errp + ERR_Z, static_cast<unsigned>(P));
           if (v < 0.0) atomicOr(&wi[q >> 5], 1u << (q & 31));
           if (i == kax - 1) csum += fabs(v);
