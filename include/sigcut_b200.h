@@ -120,6 +120,11 @@ typedef struct sc_result {
   uint64_t h2d_bytes;       /* bytes copied host->device by this call */
   uint64_t d2h_bytes;       /* bytes copied device->host by this call */
   int32_t kernel_launches;  /* kernels launched by this call */
+  /* optional (NULL = not wanted): SearchDiagnostics::sweep_values (search.hpp:37-40)
+   * of term 0's winning restart -- the cut value c after every sweep; room for
+   * max_sweeps values.  n_sweep_values receives their count (= sweeps[0]). */
+  double* sweep_values;
+  uint64_t n_sweep_values;
 } sc_result;
 
 const char* sc_version(void);

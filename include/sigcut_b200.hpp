@@ -84,7 +84,8 @@ struct RunOutput {
 /// Greedy width-w decomposition on the device; fills the reference's result
 /// types exactly as sigcut::greedy_decompose does (decompose.hpp:314-361).
 inline RunOutput run(const DenseTensor& a, const DecomposeConfig& cfg, DType dtype, Engine& eng,
-                     bool want_remainder, sc_seed_mode seed_mode = SC_SEED_PER_TERM) {
+                     bool want_remainder, sc_seed_mode seed_mode = SC_SEED_PER_TERM,
+                     SearchDiagnostics* diag = nullptr) {
   if (cfg.method != DecomposeConfig::Method::kGreedy)
     throw std::invalid_argument("sigcut_b200: only the greedy method runs on the device");
   const std::vector<std::size_t>& shape = a.shape();
@@ -139,7 +140,13 @@ inline RunOutput run(const DenseTensor& a, const DecomposeConfig& cfg, DType dty
       r.remainder = rem64.data();
     }
   }
+  std::vector<double> sv(diag != nullptr ? std::max<std::size_t>(cfg.search.max_sweeps, 1) : 0);
+  r.sweep_values = diag != nullptr ? sv.data() : nullptr;
   eng.check(sc_greedy_decompose(eng.get(), &p, &r));
+  if (diag != nullptr) {  // SearchDiagnostics (search.hpp:37-40); no CPU delta cache to check
+    diag->sweep_values.assign(sv.begin(), sv.begin() + static_cast<std::ptrdiff_t>(r.n_sweep_values));
+    diag->max_cache_rel_error = 0.0;
+  }
 
   RunOutput out;
   CutDecomposition d = CutDecomposition::with_shape(shape);
@@ -185,19 +192,24 @@ inline std::pair<CutDecomposition, CutReport> decompose(const DenseTensor& a, co
 
 /// Drop-in for sigcut::greedy_signed_cut / axial_greedy_cut (search.hpp:259-272):
 /// one cut searched with `cfg.seed` itself (restart r uses substream(seed, r)).
-inline CutResult greedy_signed_cut(const DenseTensor& a, const SearchConfig& cfg = {}, DType dtype = DType::kF64,
-                                   Engine& eng = Engine::default_engine()) {
+inline CutResult greedy_signed_cut(const DenseTensor& a, const SearchConfig& cfg, SearchDiagnostics* diag,
+                                   DType dtype = DType::kF64, Engine& eng = Engine::default_engine()) {
   DecomposeConfig dc;
   dc.width = 1;
   dc.search = cfg;
   dc.record_curve = true;
-  RunOutput o = run(a, dc, dtype, eng, false, SC_SEED_DIRECT);
+  RunOutput o = run(a, dc, dtype, eng, false, SC_SEED_DIRECT, diag);
   CutResult res;
   const CutDecomposition& d = o.result.first;
   for (const SignMatrix& f : d.factors) res.signs.push_back(f.column(0));
   res.value = o.result.second.steps.empty() ? 0.0 : o.result.second.steps[0].cut_value;
   res.iterations = o.sweeps.empty() ? 0 : o.sweeps[0];
   return res;
+}
+
+inline CutResult greedy_signed_cut(const DenseTensor& a, const SearchConfig& cfg = {}, DType dtype = DType::kF64,
+                                   Engine& eng = Engine::default_engine()) {
+  return greedy_signed_cut(a, cfg, nullptr, dtype, eng);
 }
 
 // ---------------------------------------------------------------------------

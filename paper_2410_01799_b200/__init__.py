@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     IOError_,
     NotSupported,
     SearchConfig,
+    SearchDiagnostics,
     SigcutRuntimeError,
     axial_greedy_cut,
     correct_coefficients,

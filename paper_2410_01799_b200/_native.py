@@ -57,6 +57,8 @@ class ScResult(C.Structure):
         ("h2d_bytes", u64),
         ("d2h_bytes", u64),
         ("kernel_launches", C.c_int32),
+        ("sweep_values", P(C.c_double)),
+        ("n_sweep_values", u64),
     ]
 
 

@@ -94,6 +94,15 @@ class CutResult:
 
 
 @dataclass
+class SearchDiagnostics:
+    """search.hpp:37-40.  sweep_values: c after every sweep of the winning restart.
+    The engine recomputes its products (dense refresh) instead of checking a CPU
+    delta cache, so max_cache_rel_error is always 0."""
+    sweep_values: List[float] = field(default_factory=list)
+    max_cache_rel_error: float = 0.0
+
+
+@dataclass
 class CutStep:
     k: int
     cut_value: float
@@ -202,7 +211,7 @@ class Engine:
 
     # -- core call -----------------------------------------------------------
     def run(self, a, cfg: DecomposeConfig, *, dtype: Optional[str] = None, seed_mode: int = N.SC_SEED_PER_TERM,
-            want_remainder: bool = False, shard=None):
+            want_remainder: bool = False, shard=None, diag: Optional[SearchDiagnostics] = None):
         """Runs the device decomposition; returns (CutDecomposition, CutReport, remainder|None).
 
         ``a`` is a numpy array (host path) or a CUDA torch tensor (device path,
@@ -266,6 +275,9 @@ class Engine:
         res.resid_norm_exact = rne.ctypes.data_as(C.POINTER(C.c_double))
         res.sweeps = sweeps.ctypes.data_as(C.POINTER(C.c_uint32))
         res.remainder = rem.ctypes.data if rem is not None else None
+        sv = np.zeros(max(int(cfg.search.max_sweeps), 1)) if diag is not None else None
+        if sv is not None:
+            res.sweep_values = sv.ctypes.data_as(C.POINTER(C.c_double))
         if shard is None:
             self._check(self.lib.sc_greedy_decompose(self.handle, C.byref(prob), C.byref(res)))
         else:  # this rank's band of a row-sharded matrix (sharded.py)
@@ -285,6 +297,9 @@ class Engine:
                         h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes),
                         kernel_launches=int(res.kernel_launches))
         rep._cut_values = cut[:wd].copy()
+        if diag is not None:
+            diag.sweep_values = sv[: int(res.n_sweep_values)].tolist()
+            diag.max_cache_rel_error = 0.0
         return dec, rep, rem
 
     def greedy_decompose(self, a, cfg: DecomposeConfig, dtype: Optional[str] = None):
@@ -445,12 +460,15 @@ class Engine:
         return self.lstsq_decompose(a, cfg, dtype=dtype,
                                     channel_axis=(np.ndim(a) - 1) if channel_axis is None else channel_axis)
 
-    def greedy_signed_cut(self, a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None) -> CutResult:
+    def greedy_signed_cut(self, a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None,
+                          diag: Optional[SearchDiagnostics] = None) -> CutResult:
         """One cut searched with cfg.seed itself: order 2 is greedy_signed_cut
-        (search.hpp:259-263), any other order axial_greedy_cut (:269-272)."""
+        (search.hpp:259-263), any other order axial_greedy_cut (:269-272).  With
+        ``diag`` the winning restart's per-sweep values are returned like
+        SearchDiagnostics."""
         cfg = cfg or SearchConfig()
         dc = DecomposeConfig(width=1, search=cfg)
-        dec, rep, _ = self.run(a, dc, dtype=dtype, seed_mode=N.SC_SEED_DIRECT)
+        dec, rep, _ = self.run(a, dc, dtype=dtype, seed_mode=N.SC_SEED_DIRECT, diag=diag)
         return CutResult(float(rep._cut_values[0]), [f[0] for f in dec.factors], int(rep.sweeps[0]))
 
 
@@ -510,14 +528,16 @@ def solve_gram(gram, rhs) -> np.ndarray:
     return out
 
 
-def greedy_signed_cut(a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None) -> CutResult:
-    return default_engine().greedy_signed_cut(a, cfg, dtype=dtype)
+def greedy_signed_cut(a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None,
+                      diag: Optional[SearchDiagnostics] = None) -> CutResult:
+    return default_engine().greedy_signed_cut(a, cfg, dtype=dtype, diag=diag)
 
 
-def axial_greedy_cut(a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None) -> CutResult:
+def axial_greedy_cut(a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None,
+                     diag: Optional[SearchDiagnostics] = None) -> CutResult:
     """Order-k cut (axial_run, search.hpp:191-213); order 2 routes to the matrix
     alternation exactly as the reference does (search.hpp:247, :269-272)."""
-    return greedy_signed_cut(a, cfg, dtype=dtype)
+    return greedy_signed_cut(a, cfg, dtype=dtype, diag=diag)
 
 
 def width_for_compression(shape, rate: float, coeff_bits: int = 64, source_bits: int = 64) -> int:

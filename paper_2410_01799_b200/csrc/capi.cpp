@@ -341,7 +341,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   double* zpart = carve<double>(cur, 2 * static_cast<size_t>(G) * pitch);  // [2][G][pitch] by pass parity
   scb::Slot* slots = carve<scb::Slot>(cur, G);
   unsigned* ctr = carve<unsigned>(cur, 8);  // [0] grid barrier, [1..3] err_pass
-  unsigned long long* stats = carve<unsigned long long>(cur, 4);
+  unsigned long long* stats = carve<unsigned long long>(cur, 8);
   unsigned long long* tb64 = carve<unsigned long long>(cur, 2 * static_cast<size_t>(tw32));
   unsigned* ctr_g = ctr;  // the grid's barrier / error words (rank 0's when sharded)
   if (sh) {  // exchange buffers live in the peer-mapped shard region (reset by sc_shard_reset)
@@ -429,7 +429,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
     SC_CUDA(ctx, cudaMemsetAsync(tb64, 0, 2 * static_cast<size_t>(tw32) * 8, st));
   }
   SC_CUDA(ctx, cudaMemsetAsync(tbest, 0, static_cast<size_t>(tw32) * 4, st));
-  SC_CUDA(ctx, cudaMemsetAsync(stats, 0, 32, st));
+  SC_CUDA(ctx, cudaMemsetAsync(stats, 0, 64, st));
   if (w > 0) SC_CUDA(ctx, cudaMemsetAsync(S_out, 0, w * wm * 8, st));
 
   scb::KParams kp{};
@@ -507,6 +507,17 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
     SC_CUDA(ctx, cudaMemsetAsync(dprof, 0, static_cast<size_t>(G) * 16 * 8, st));
   }
   kp.prof = dprof;
+  // SearchDiagnostics::sweep_values of term 0, every restart (the host keeps the winner's)
+  double* dsweeps = nullptr;
+  res->n_sweep_values = 0;
+  if (res->sweep_values != nullptr && w > 0 && !sh) {
+    void* pv = nullptr;
+    const size_t nb = static_cast<size_t>(p->restarts) * p->max_sweeps * 8;
+    if (sc_status s2 = scb::pool_get(ctx, "diag.sweeps", nb, &pv); s2 != SC_OK) return s2;
+    dsweeps = static_cast<double*>(pv);
+    SC_CUDA(ctx, cudaMemsetAsync(dsweeps, 0, nb, st));
+  }
+  kp.sweep_vals = dsweeps;
   SC_CUDA(ctx, scb::set_smem_limit(var, smem));
   SC_CUDA(ctx, cudaEventRecord(ctx->ev0, st));
   SC_CUDA(ctx, scb::launch_sweep(var, kp, smem, st));
@@ -514,10 +525,10 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
 
   // ---- results ----
   unsigned h_ctr[4];
-  unsigned long long h_stats[4];
+  unsigned long long h_stats[8];
   std::vector<double> h_norm2(w + 1);
   SC_CUDA(ctx, cudaMemcpyAsync(h_ctr, ctr_g, 16, cudaMemcpyDeviceToHost, st));
-  SC_CUDA(ctx, cudaMemcpyAsync(h_stats, stats, 32, cudaMemcpyDeviceToHost, st));
+  SC_CUDA(ctx, cudaMemcpyAsync(h_stats, stats, 64, cudaMemcpyDeviceToHost, st));
   SC_CUDA(ctx, cudaMemcpyAsync(h_norm2.data(), norm2, (w + 1) * 8, cudaMemcpyDeviceToHost, st));
   SC_CUDA(ctx, cudaStreamSynchronize(st));
   d2h += 16 + 32 + (w + 1) * 8;
@@ -597,6 +608,16 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   if (res->remainder) {
     SC_CUDA(ctx, cudaMemcpy2DAsync(res->remainder, n * es, dR, rowB, n * es, m, cudaMemcpyDeviceToHost, st));
     d2h += m * n * es;
+  }
+  if (dsweeps != nullptr && wd > 0) {
+    uint32_t n0 = 0;
+    SC_CUDA(ctx, cudaMemcpyAsync(&n0, sweeps_out, 4, cudaMemcpyDeviceToHost, st));
+    SC_CUDA(ctx, cudaStreamSynchronize(st));
+    n0 = static_cast<uint32_t>(std::min<uint64_t>(n0, p->max_sweeps));
+    SC_CUDA(ctx, cudaMemcpyAsync(res->sweep_values, dsweeps + h_stats[4] * p->max_sweeps, n0 * 8ull,
+                                 cudaMemcpyDeviceToHost, st));
+    res->n_sweep_values = n0;
+    d2h += 4 + n0 * 8ull;
   }
   SC_CUDA(ctx, cudaStreamSynchronize(st));
 

@@ -1923,6 +1923,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
             p.c_out[term] = bc;
             p.sweeps_out[term] = static_cast<uint32_t>(ctl->best_sweeps);
             p.stats[0] = static_cast<unsigned long long>(term + 1);
+            if (term == 0) p.stats[4] = static_cast<unsigned long long>(ctl->best_restart);
           }
           ctl->alpha = bc / p.numel_d;  // alpha = c / numel (decompose.hpp:340)
           ctl->utsel = ctl->best_tsel;
@@ -1973,6 +1974,9 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         } else {
           // matrix: c = <s_pp, R t_pp> from this pass's y; order-k: c of this sweep's axial step
           const double c = p.tensor ? ctl->ax_c : cs;
+          // SearchDiagnostics::sweep_values of term 0 (search.hpp:177, :207), per restart
+          if (p.sweep_vals != nullptr && ctl->term == 0 && g == 0)
+            p.sweep_vals[static_cast<size_t>(ctl->restart) * p.max_sweeps + (pp - 1)] = c;
           const bool stop = (c <= ctl->c_prev) || (pp >= p.max_sweeps);
           if (!stop) {
             ctl->c_prev = c;
@@ -2002,6 +2006,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
             if (better) {
               ctl->best_c = c;
               ctl->best_sweeps = pp;
+              ctl->best_restart = ctl->restart;
               uint32_t* sbest = sb + ctl->best * p.sw;
               for (int i = 0; i < p.sw; ++i) sbest[i] = s_nxt[i];
               for (int i = 0; i < p.axw; ++i) sax_best[i] = sax[i];
@@ -2021,6 +2026,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
             if (better) {
               ctl->best_c = c;
               ctl->best_sweeps = pp;
+              ctl->best_restart = ctl->restart;
               uint32_t* sbest = sb + ctl->best * p.sw;
               for (int i = 0; i < p.sw; ++i) sbest[i] = s_cur[i];
               if (ctl->restart + 1 < p.restarts) {

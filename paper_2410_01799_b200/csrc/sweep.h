@@ -41,7 +41,7 @@ struct Ctl {
   volatile int abort;
   volatile int kind_ring[4];
   // controller state (thread 0 writes, consumers read after a named barrier)
-  int kind, pp, term, restart, tsel, utsel, best_tsel, best_sweeps;
+  int kind, pp, term, restart, tsel, utsel, best_tsel, best_sweeps, best_restart;
   int cur, nxt, best, need_reduce, norm_idx, kron_upd;
   double alpha, c_prev, best_c, first_value;
   double ax_c;  // order-k mode: c = <s_{k-1}, v_{k-1}> of the axial step
@@ -81,7 +81,8 @@ struct KParams {
   double* c_out;       // [width]
   uint32_t* sweeps_out;  // [width]
   double* norm2_out;   // [width + 1]: [0] = ||A||^2, [k+1] = ||R after term k||^2
-  unsigned long long* stats;  // [0] width_done, [1] passes
+  unsigned long long* stats;  // [0] width_done, [1] passes, [2]/[3] dense/delta dot passes, [4] term 0's winning restart
+  double* sweep_vals;  // [restarts][max_sweeps] c of every sweep of term 0 (SearchDiagnostics) or nullptr
   long long width, restarts, max_sweeps;
   double min_frac;
   double numel_d;

@@ -69,6 +69,13 @@ int main() {
       CHECK(r.signs[i] == g.signs[i], "cut signs axis %zu", i);
     CHECK(std::fabs(r.value - g.value) <= 1e-12 * std::fabs(r.value), "cut value %.17g vs %.17g", r.value, g.value);
     CHECK(r.iterations == g.iterations, "iterations %zu vs %zu", r.iterations, g.iterations);
+    SearchDiagnostics rd, gd;
+    greedy_signed_cut(a, sc, &rd);
+    b200::greedy_signed_cut(a, sc, &gd, b200::DType::kF64, eng);
+    CHECK(rd.sweep_values.size() == gd.sweep_values.size(), "sweep value count");
+    for (std::size_t k = 0; k < rd.sweep_values.size() && k < gd.sweep_values.size(); ++k)
+      CHECK(std::fabs(rd.sweep_values[k] - gd.sweep_values[k]) <= 1e-12 * std::fabs(rd.sweep_values[k]) + 1e-12,
+            "sweep value %zu", k);
   }
   {  // error semantics: same exception type as the reference
     const DenseTensor a = randn({4, 4}, 1);

@@ -410,3 +410,38 @@ def test_delta_policy_extremes(engine, ref, monkeypatch, refresh, div):
     od = ref.greedy_decompose(a, 12, seed=4)
     assert (dec.factors[0] == od.signs[0]).all() and (dec.factors[1] == od.signs[1]).all()
     assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F64_TOL
+
+
+# ------------------------------------------------------------ SearchDiagnostics
+@pytest.mark.parametrize("name", cut_names())
+def test_sweep_values_match_reference(engine, name):
+    """SearchDiagnostics::sweep_values (search.hpp:177, :207) of the winning restart."""
+    d = load("cut_" + name)
+    diag = sc.SearchDiagnostics()
+    r = engine.greedy_signed_cut(d["a"], sc.SearchConfig(seed=int(d["seed"]), restarts=int(d["restarts"]),
+                                                         max_sweeps=int(d["max_sweeps"])), dtype="f64", diag=diag)
+    ref_sv = np.asarray(d["sweep_values"])
+    assert len(diag.sweep_values) == r.iterations
+    if int(d["restarts"]) == 1:
+        assert len(diag.sweep_values) == len(ref_sv)
+    n = min(len(ref_sv), len(diag.sweep_values))
+    np.testing.assert_allclose(diag.sweep_values[:n], ref_sv[:n], rtol=1e-12, atol=1e-12)
+    assert diag.max_cache_rel_error == 0.0
+
+
+def test_sweep_values_monotone_and_fixed_point(engine, orc):
+    """test_search.cpp:184-204 on the device: non-decreasing values, the value is
+    <sign outer product, A>, and one more alternation cannot improve it."""
+    for trial in range(20):
+        a = (orc.fill_f64(41 * 100 + trial, 12 * 18).reshape(12, 18) * 4.0) - 2.0
+        diag = sc.SearchDiagnostics()
+        r = engine.greedy_signed_cut(a, sc.SearchConfig(seed=trial), dtype="f64", diag=diag)
+        slack = 1e-9 * np.linalg.norm(a)
+        sv = diag.sweep_values
+        assert all(sv[j] >= sv[j - 1] - slack for j in range(1, len(sv)))
+        s = sc.unpack_signs(r.signs[0], 12)
+        t = sc.unpack_signs(r.signs[1], 18)
+        assert abs(r.value - s @ a @ t) <= 1e-10 * max(1.0, abs(r.value))
+        s2 = np.where(a @ t < 0, -1.0, 1.0)
+        t2 = np.where(a.T @ s2 < 0, -1.0, 1.0)
+        assert abs(s2 @ a @ t2 - r.value) <= 1e-9 * max(1.0, abs(r.value))
