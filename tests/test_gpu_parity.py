@@ -446,3 +446,17 @@ def test_sweep_values_monotone_and_fixed_point(engine, orc):
         s2 = np.where(a @ t < 0, -1.0, 1.0)
         t2 = np.where(a.T @ s2 < 0, -1.0, 1.0)
         assert abs(s2 @ a @ t2 - r.value) <= 1e-9 * max(1.0, abs(r.value))
+
+
+@pytest.mark.parametrize("shape,dtype", [((40, 3000, 3), "f32"), ((64, 9000), "f32"), ((33, 10240), "f32")])
+def test_rows_8k_to_10k_whole_row_variant(engine, ref, shape, dtype):
+    """Rows of 8193..10240 f32 run whole (16 warps x 5 vectors, one read per pass);
+    the trajectory is the reference's (C3's 3000 x 3 trailing block is 9000 wide)."""
+    a = ref.fill_normal(91, int(np.prod(shape))).reshape(shape).astype(np.float32)
+    cfg = sc.DecomposeConfig(width=6, flush_width=1, record_curve=True, search=sc.SearchConfig(seed=4))
+    dec, rep, _ = engine.run(a, cfg, dtype=dtype)
+    od = ref.greedy_decompose(a.astype(np.float64), 6, seed=4, flush_width=1)
+    for i in range(len(shape)):
+        assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
+    np.testing.assert_allclose(rep._cut_values, od.cut_value, rtol=F32_TOL)
+    assert sweeps_ok(rep.sweeps, od.iterations)
