@@ -540,9 +540,19 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
     std::vector<unsigned long long> hp(static_cast<size_t>(G) * 16);
     cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost);
     cudaFree(dprof);
-    double acc[12] = {0};
+    double acc[16] = {0};
     for (int g = 0; g < G; ++g)
-      for (int i = 0; i < 12; ++i) acc[i] += static_cast<double>(hp[g * 16 + i]) / G;
+      for (int i = 0; i < 16; ++i) acc[i] += static_cast<double>(hp[g * 16 + i]) / G;
+    if (tensor)
+      std::fprintf(stderr, "[scb prof tensor] axis1 %.0f axis2 %.0f kron %.0f (slots 15, 8, 9 per dot pass)\n",
+                   acc[15] / std::max<double>(1.0, static_cast<double>(h_stats[2])),
+                   acc[8] / std::max<double>(1.0, static_cast<double>(h_stats[2])),
+                   acc[9] / std::max<double>(1.0, static_cast<double>(h_stats[2])));
+    if (tensor)
+      std::fprintf(stderr, "[scb prof tensor] per dot pass: Z reduction+barrier %.0f (barrier %.0f), axial step %.0f cycles\n",
+                   acc[12] / std::max<double>(1.0, static_cast<double>(h_stats[2])),
+                   acc[14] / std::max<double>(1.0, static_cast<double>(h_stats[2])),
+                   acc[13] / std::max<double>(1.0, static_cast<double>(h_stats[2])));
     {
       double mn[8], mx[8];
       for (int i = 0; i < 8; ++i) {

@@ -1203,36 +1203,55 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
 //   s_i = sgn(v_i), and c = <s_{k-1}, v_{k-1}> = sum_q |v_{k-1}[q]|.
 // Every CTA runs this redundantly on the same data in the same order, so all
 // CTAs hold identical signs and c (deterministic fixed-order sums).
-__device__ __forceinline__ uint32_t axbit(const KParams& p, const uint32_t* sax, int j, int idx) {
-  return (sax[p.ax_off[j] + (idx >> 5)] >> (idx & 31)) & 1u;
+__device__ __forceinline__ uint32_t axbit(const Ctl* ctl, const uint32_t* sax, int j, int idx) {
+  return (sax[ctl->axoff[j] + (idx >> 5)] >> (idx & 31)) & 1u;
 }
 // t word q of kron(s_1, ..., s_{k-1}) over the N' columns: the multi-index of
 // the word's first column is decomposed once (32-bit), then advanced as an
-// odometer whose running parity is updated incrementally.
-__device__ uint32_t kron_word(const KParams& p, const uint32_t* sax, int q) {
+// odometer whose running parity is updated incrementally.  Axis extents and
+// offsets come from shared memory (ctl), never from the local-memory copy of
+// the kernel parameters.
+__device__ uint32_t kron_word(const KParams& p, const Ctl* ctl, const uint32_t* sax, int q) {
   const int col0 = q * 32;
-  if (col0 >= p.n) return 0u;
+  const int n = p.n, kax = p.kax;
+  if (col0 >= n) return 0u;
+  const int nb = min(32, n - col0);
+  uint32_t word = 0;
+  if (kax == 2) {  // order 3: two trailing axes, scalar odometer
+    const int n2 = ctl->axn[1];
+    int i1 = col0 / n2, i2 = col0 - i1 * n2;
+    const uint32_t* w1 = sax + ctl->axoff[0];
+    const uint32_t* w2 = sax + ctl->axoff[1];
+    uint32_t b1 = (w1[i1 >> 5] >> (i1 & 31)) & 1u;
+    for (int b = 0; b < nb; ++b) {
+      word |= (b1 ^ ((w2[i2 >> 5] >> (i2 & 31)) & 1u)) << b;
+      if (++i2 == n2) {
+        i2 = 0;
+        ++i1;
+        b1 = (w1[i1 >> 5] >> (i1 & 31)) & 1u;
+      }
+    }
+    return word;
+  }
   int idx[7];
   uint32_t xb = 0;
   int c = col0;
-  for (int j = p.kax - 1; j >= 0; --j) {
-    const int nj = p.ax_n[j];
+  for (int j = kax - 1; j >= 0; --j) {
+    const int nj = ctl->axn[j];
     idx[j] = c % nj;
     c /= nj;
-    xb ^= axbit(p, sax, j, idx[j]);
+    xb ^= axbit(ctl, sax, j, idx[j]);
   }
-  uint32_t word = 0;
-  const int nb = min(32, p.n - col0);
   for (int b = 0; b < nb; ++b) {
     word |= xb << b;
-    for (int j = p.kax - 1; j >= 0; --j) {  // advance the odometer by one column
-      xb ^= axbit(p, sax, j, idx[j]);
-      if (++idx[j] < p.ax_n[j]) {
-        xb ^= axbit(p, sax, j, idx[j]);
+    for (int j = kax - 1; j >= 0; --j) {  // advance the odometer by one column
+      xb ^= axbit(ctl, sax, j, idx[j]);
+      if (++idx[j] < ctl->axn[j]) {
+        xb ^= axbit(ctl, sax, j, idx[j]);
         break;
       }
       idx[j] = 0;
-      xb ^= axbit(p, sax, j, 0);
+      xb ^= axbit(ctl, sax, j, 0);
     }
   }
   return word;
@@ -1245,7 +1264,8 @@ __device__ uint32_t kron_word(const KParams& p, const uint32_t* sax, int q) {
 // with a fixed butterfly -- so thousands of L2 loads are in flight instead of a
 // few warps walking the slices serially.  All index arithmetic is 32-bit.
 template <int CW>
-__device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_t* tws, Ctl* ctl, int P) {
+__device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_t* tws, Ctl* ctl, int P,
+                                      long long* tsplit) {
   constexpr int CT = CW * 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kax = p.kax;
@@ -1256,78 +1276,97 @@ __device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_
     int st = 1;
     for (int j = kax - 1; j >= 0; --j) {
       zstride[j] = st;
-      st *= p.ax_n[j];
+      st *= ctl->axn[j];
     }
   }
   double csum = 0.0;
   if (kax == 0 && tid == 0) csum = __ldcg(Z);  // order 1: c = <s_0, a> = Z[0]
+  long long tprev = tsplit ? clock64() : 0;
   for (int i = 0; i < kax; ++i) {
-    const int ni = p.ax_n[i];
+    const int ni = ctl->axn[i];
     const int other = p.n / ni;
-    uint32_t* wi = sax + p.ax_off[i];
+    uint32_t* wi = sax + ctl->axoff[i];
     const int nwi = (ni + 31) / 32;
     // signed Z entry of (index_i = q, r-th combination of the other axes, last fastest)
     auto term = [&](int q, int r) -> double {
       if (kax == 2) {  // order 3 (the common case): Z is n_1 x n_2, no index arithmetic
         const int j = 1 - i;
-        return flipd(__ldcg(Z + (i == 0 ? q * p.ax_n[1] + r : r * p.ax_n[1] + q)), axbit(p, sax, j, r) << 31);
+        return flipd(__ldcg(Z + (i == 0 ? q * ctl->axn[1] + r : r * ctl->axn[1] + q)), axbit(ctl, sax, j, r) << 31);
       }
       int flat = q * zstride[i];
       uint32_t xb = 0;
       for (int j = kax - 1; j >= 0; --j) {
         if (j == i) continue;
-        const int nj = p.ax_n[j];
+        const int nj = ctl->axn[j];
         const int ij = r % nj;
         r /= nj;
         flat += ij * zstride[j];
-        xb ^= axbit(p, sax, j, ij);
+        xb ^= axbit(ctl, sax, j, ij);
       }
       return flipd(__ldcg(Z + flat), xb << 31);
     };
     for (int wq = tid; wq < nwi; wq += CT) wi[wq] = 0u;
     consumer_sync(CT);
-    if (ni <= CW) {  // whole CTA per output
-      for (int q = 0; q < ni; ++q) {
-        double v = 0.0;
-#pragma unroll 4
-        for (int r = tid; r < other; r += CT) v += term(q, r);
-        v = warp_sum(v);
-        if (lane == 0) ctl->cred[warp] = v;
-        consumer_sync(CT);
-        if (tid == 0) {
-          double t = 0.0;
-          for (int w = 0; w < CW; ++w) t += ctl->cred[w];
-          if (!isfinite(t)) atomicMin(errp + ERR_Z, static_cast<unsigned>(P));
-          if (t < 0.0) wi[q >> 5] |= 1u << (q & 31);
-          if (i == kax - 1) csum += fabs(t);
-        }
-        consumer_sync(CT);
+    if (ni <= 4 && ni <= CW) {  // few outputs: the whole CTA sums all of them at once
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+      for (int r = tid; r < other; r += CT) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < ni) v[q] += term(q, r);
       }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double t = warp_sum(v[q]);
+        if (lane == 0 && q < ni) ctl->cred[q * CW + warp] = t;
+      }
+      consumer_sync(CT);
+      if (tid < ni) {
+        const int q = tid;
+        double t = 0.0;
+        for (int w = 0; w < CW; ++w) t += ctl->cred[q * CW + w];
+        if (!isfinite(t)) atomicMin(errp + ERR_Z, static_cast<unsigned>(P));
+        if (t < 0.0) atomicOr(&wi[q >> 5], 1u << (q & 31));
+        if (i == kax - 1) csum += fabs(t);
+      }
+      consumer_sync(CT);
     } else {  // T lanes per output
       int T = 32;
       while (T > 1 && ni * T > 2 * CT) T >>= 1;
       const int groups = CT / T, sub = tid & (T - 1);
+#pragma unroll 1
       for (int q = tid / T; q - tid / T < ni; q += groups) {
         const bool ok = q < ni;
         double v = 0.0;
         if (ok) {
-#pragma unroll 4
+#pragma unroll 1
           for (int r = sub; r < other; r += T) v += term(q, r);
         }
         for (int o = T >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (T == 1) {  // the warp's 32 consecutive outputs form one word: no atomics
+          const unsigned word = __ballot_sync(0xffffffffu, ok && v < 0.0);
+          if (lane == 0 && q < ni) wi[q >> 5] = word;
+        } else if (ok && sub == 0 && v < 0.0) {
+          atomicOr(&wi[q >> 5], 1u << (q & 31));
+        }
         if (ok && sub == 0) {
           if (!isfinite(v)) atomicMin(errp + ERR_Z, static_cast<unsigned>(P));
-          if (v < 0.0) atomicOr(&wi[q >> 5], 1u << (q & 31));
           if (i == kax - 1) csum += fabs(v);
         }
       }
     }
     consumer_sync(CT);
+    if (tsplit && tid == 0 && i < 2) {
+      const long long t = clock64();
+      tsplit[i] += t - tprev;
+      tprev = t;
+    }
   }
   csum = warp_sum(csum);
   if (lane == 0) ctl->cred[warp] = csum;
-  for (int q = tid; q < p.Q; q += CT) tws[q] = kron_word(p, sax, q);
+  for (int q = tid; q < p.Q; q += CT) tws[q] = kron_word(p, ctl, sax, q);
   consumer_sync(CT);
+  if (tsplit && tid == 0) tsplit[2] += clock64() - tprev;
   if (tid == 0) {
     double c = 0.0;
     for (int w = 0; w < CW; ++w) c += ctl->cred[w];
@@ -1401,6 +1440,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     ctl->stored = 0;
     ctl->abort = 0;
     ctl->pp = p.tensor ? 1 : 0;  // order-k: pp = sweep of the current pass (1-based)
+    for (int j = 0; j < 8; ++j) {  // read by the axial step from shared memory, not the param copy
+      ctl->axn[j] = j < 7 ? p.ax_n[j] : 1;
+      ctl->axoff[j] = j < 7 ? p.ax_off[j] : 0;
+    }
     ctl->kron_upd = 0;
     ctl->nflip = 0;
     ctl->since_dense = 0;
@@ -1509,6 +1552,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   constexpr unsigned long long* prof = nullptr;
 #endif
   long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long pten[6] = {0, 0, 0, 0, 0, 0};  // order-k: Z reduction (+ barrier), axial step, Z barrier, axis 1, axis 2, kron
   const unsigned* errp = p.err_pass;
   int qs = 0, qph = 0;     // stage / phase of this pass's first streamed row
   unsigned gcount = 0;     // dot-partial groups published in earlier passes
@@ -1606,8 +1650,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     // later, i.e. after the next pass's grid barrier, which every CTA reaches
     // only after finishing this reduction.
     if (zmode) {
+      const long long tz = prof ? clock64() : 0;
       if (tid == 0) grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
       consumer_sync(CT);
+      if (prof && tid == 0) pten[2] += clock64() - tz;
     }
   };
 
@@ -1879,8 +1925,14 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       t_pass0 = t;
     }
     if (p.tensor && (kind & F_DOT)) {  // order-k: Z = M^T s_0, then axes 1..k-1 and c
+      const long long ta = prof ? clock64() : 0;
       col_reduce(true, P, false, 0, 0);
-      axial_step<CW>(p, sax, tws, ctl, P);
+      const long long tb = prof ? clock64() : 0;
+      axial_step<CW>(p, sax, tws, ctl, P, prof ? pten + 3 : nullptr);
+      if (prof && tid == 0) {
+        pten[0] += tb - ta;
+        pten[1] += clock64() - tb;
+      }
     }
 
     // Matrix dot pass: owners reduce z and publish the next t right away (it does
@@ -2066,7 +2118,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       t_pass0 = t;
     }
     if (p.tensor && ctl->kron_upd) {  // order-k: t of the rank-1 update = kron(best axes)
-      for (int q = tid; q < p.Q; q += CT) uws[q] = kron_word(p, sax_best, q);
+      for (int q = tid; q < p.Q; q += CT) uws[q] = kron_word(p, ctl, sax_best, q);
       consumer_sync(CT);
       if (tid == 0) ctl->kron_upd = 0;
     }
@@ -2079,8 +2131,15 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     p.stats[2] = dot_passes[0];
     p.stats[3] = dot_passes[1];
   }
-  if (prof && tid == 0)
+  if (prof && tid == 0) {
     for (int i = 0; i < 7; ++i) prof[g * 16 + i] = static_cast<unsigned long long>(pacc[i]);
+    prof[g * 16 + 12] = static_cast<unsigned long long>(pten[0]);
+    prof[g * 16 + 13] = static_cast<unsigned long long>(pten[1]);
+    prof[g * 16 + 14] = static_cast<unsigned long long>(pten[2]);
+    prof[g * 16 + 15] = static_cast<unsigned long long>(pten[3]);
+    prof[g * 16 + 8] = static_cast<unsigned long long>(pten[4]);
+    prof[g * 16 + 9] = static_cast<unsigned long long>(pten[5]);
+  }
 }
 
 template <typename E, int NW, int VPT, int RG>

@@ -50,7 +50,8 @@ struct Ctl {
   int since_dense;      // delta passes since the last dense dot pass
   int has_dz;           // this CTA wrote a z partial in a delta pass
   int keep;             // t unchanged since the last dot pass: y, s, z stay exactly as cached
-  double cred[32];
+  double cred[64];  // per-warp partials (axial step: 4 outputs x up to 16 warps)
+  int axn[8], axoff[8];  // order-k: n_1..n_{k-1} and their axis-word offsets (shared-memory copies)
   double nred[32];
 };
 
