@@ -1599,13 +1599,21 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         double a = 0.0;
         for (int g0 = gs; g0 < ge; g0 += 32) {  // one round of up to 32 L2 loads in flight
           double v[32];
+          if (p.world > 1) {  // partials of every rank through the peer mappings
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            const int gp = g0 + u;
-            const double* zp = p.world > 1 ? p.zpart_pe[gp / G] + static_cast<size_t>(gp % G) * pitch
-                                           : p.zpart + static_cast<size_t>(gp) * pitch;
-            const bool take = gp < ge && (!delta || ((dzmask[gp >> 5] >> (gp & 31)) & 1u));
-            v[u] = take ? __ldcg(zp + par) : 0.0;
+            for (int u = 0; u < 32; ++u) {
+              const int gp = g0 + u;
+              const bool take = gp < ge && (!delta || ((dzmask[gp >> 5] >> (gp & 31)) & 1u));
+              v[u] = take ? __ldcg(p.zpart_pe[gp / G] + static_cast<size_t>(gp % G) * pitch + par) : 0.0;
+            }
+          } else {  // single GPU: no per-load division or parameter-array indexing
+            const double* zb = p.zpart + par;
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+              const int gp = g0 + u;
+              const bool take = gp < ge && (!delta || ((dzmask[gp >> 5] >> (gp & 31)) & 1u));
+              v[u] = take ? __ldcg(zb + static_cast<size_t>(gp) * pitch) : 0.0;
+            }
           }
 #pragma unroll
           for (int u = 0; u < 32; ++u) a += v[u];
@@ -1899,8 +1907,9 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     {
       // every CTA (of every rank) reduces the GT partials in the same fixed order
       double cs = 0.0, ns = 0.0;
+      const bool multi = p.world > 1;
       for (int i = tid; i < p.GT; i += CT) {
-        const Slot* s = p.world > 1 ? p.slots_pe[i / G] + (i % G) : p.slots + i;
+        const Slot* s = multi ? p.slots_pe[i / G] + (i % G) : p.slots + i;
         cs += __ldcg(&s->c[P & 1]);
         ns += __ldcg(&s->n[P & 1]);
         if ((kind & F_DELTA) && __ldcg(&s->dz[P & 1]) != 0.0) atomicOr(&dzmask[i >> 5], 1u << (i & 31));
