@@ -149,3 +149,40 @@ def test_device_decomposition_scd_is_reference_file(engine, ref):
         r0 = header + j * per + 8
         assert mine[r0: r0 + 22] == theirs[r0: r0 + 22]
     assert (bits(engine.expand(back)) == bits(ref.accumulate_expansion(a.shape, back.factors, back.coefficients))).all()
+
+
+def test_lstsq_f32_and_device_inputs(engine, ref):
+    import torch
+
+    a = ref.fill_normal(505, 30 * 22).reshape(30, 22)
+    a32 = a.astype(np.float32)
+    cfg = sc.DecomposeConfig(width=5, search=sc.SearchConfig(seed=9))
+    d_host, r_host = engine.lstsq_decompose(a32, cfg)
+    d_dev, r_dev = engine.lstsq_decompose(torch.tensor(a32, device="cuda"), cfg)
+    od = ref.lstsq_decompose(a32.astype(np.float64), 5, seed=9)
+    for x, y, z in zip(d_host.factors, d_dev.factors, od.signs):
+        assert (x == z).all() and (y == z).all()
+    np.testing.assert_allclose(d_host.coefficients, od.alpha, rtol=1e-9, atol=1e-13)
+    assert (d_host.coefficients == d_dev.coefficients).all()
+    # width 0: nothing appended, the residual is the input
+    d0, r0 = engine.lstsq_decompose(a, sc.DecomposeConfig(width=0))
+    assert d0.width() == 0 and abs(r0.final_residual_norm - np.linalg.norm(a)) <= 1e-12 * np.linalg.norm(a)
+
+
+def test_lstsq_min_value_fraction_and_budget(engine, ref):
+    a = load("lsq_mat_40x33")["a"]
+    cfg = sc.DecomposeConfig(width=12, min_value_fraction=0.9, search=sc.SearchConfig(seed=3))
+    dec, rep = engine.lstsq_decompose(a, cfg)
+    od = ref.lstsq_decompose(a, 12, seed=3, min_value_fraction=0.9)
+    assert dec.width() == od.width < 12
+    with pytest.raises(sc.InvalidArgument, match="factor memory budget"):
+        engine.lstsq_decompose(a, sc.DecomposeConfig(width=1000, max_factor_bytes=1024))
+
+
+def test_tensor_decomposition_scd_round_trip(engine, ref):
+    a = ref.fill_normal(606, 6 * 7 * 5).reshape(6, 7, 5)
+    dec, rep = engine.greedy_decompose(a, sc.DecomposeConfig(width=9, search=sc.SearchConfig(seed=1)), dtype="f64")
+    blob = scio.write_scd(dec)
+    assert blob == ref.write_scd(a.shape, dec.factors, dec.coefficients, -1, 64)
+    back = scio.read_scd(blob)
+    assert (bits(engine.expand(back)) == bits(ref.accumulate_expansion(a.shape, dec.factors, dec.coefficients))).all()
