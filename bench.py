@@ -30,6 +30,16 @@ SEED = 1
 METRIC = "signed cuts/sec at 4096x4096 f32; achieved HBM GB/s vs B200 peak"
 
 
+def bench_config(width, world):
+    """The workload description both arms print (the reference arm times a bounded
+    sample of the same decomposition; its cpu_baseline.sample says which)."""
+    return {"workload": "4096x4096 f32 N(0,1) seed 1+rank (BASELINE config 2), greedy_decompose, "
+                        f"{width} cuts per step from the original matrix",
+            "cuts_per_step": width, "l2": "flushed (256 MB write) before every step; R (64 MiB) "
+                                          "stays L2/SMEM-resident within a step",
+            "parallelism": f"independent matrices x{world}"}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -153,8 +163,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "cuts/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["seconds"] / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "4096x4096 f32 N(0,1) seed 1 (BASELINE config 2), greedy_decompose prefix",
-                       "cuts_per_worker_step": args.ref_cuts},
+            "config": bench_config(args.width, world),
             "cpu_baseline": {"value": r["value"], "unit": "cuts/s", "cores": r["cores"], "kind": r["kind"],
                              "sample": r["sample"]},
             "e2e": {"value": r["value"], "unit": "cuts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -246,11 +255,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "cuts/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "4096x4096 f32 N(0,1) seed 1+rank (BASELINE config 2), greedy_decompose, "
-                               f"{args.width} cuts per step from the original matrix",
-                   "cuts_per_step": args.width, "l2": "flushed (256 MB write) before every step; R (64 MiB) "
-                                                     "stays L2/SMEM-resident within a step",
-                   "parallelism": f"independent matrices x{world}"},
+        "config": bench_config(args.width, world),
         "e2e": {"value": args.width * world / e2e_step_s, "unit": "cuts/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
