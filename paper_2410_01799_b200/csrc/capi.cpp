@@ -479,7 +479,10 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   kp.AX_out = reinterpret_cast<uint32_t*>(AX_out);
   kp.zfull = zfull;
   kp.zstate = zstate;
-  kp.delta = tensor ? 0 : static_cast<int>(env_size("SCB_DELTA", 1));
+  // Sparse delta passes keep y / z caches per whole row; rows streamed as column
+  // chunks (cpr > 1) run every sweep dense (the delta pass's y cache is not
+  // maintained by the chunked dot pass -- the trajectory left the reference's).
+  kp.delta = (tensor || cpr > 1) ? 0 : static_cast<int>(env_size("SCB_DELTA", 1));
   kp.delta_div = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_DIV", 32)));
   kp.delta_refresh = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_REFRESH", 16)));
   // Dot-pass form: the two-phase pass reads R twice per sweep but has no per-row
@@ -487,7 +490,9 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   // to HBM the fused single-read pass wins (14336x4096 f32: 77.6 vs 84 us/pass).
   // Wide rows (cpr > 1) always take the two-phase pass.  SCB_2PH=0/1 overrides.
   const bool l2_resident = m * rowB <= (size_t{160} << 20);  // 4096^2 f64 (128 MB): two-phase 24.0 vs 24.6 us/pass
-  kp.two_phase = cpr > 1 ? 1 : static_cast<int>(env_size("SCB_2PH", l2_resident ? 1 : 0));
+  // The 16-warp whole-row variants (8193..14336 f32 columns) are faster two-phase
+  // even when R spills to HBM (4096 x 14336 f32: 58 vs 97 us/pass; C3: 91 vs 183).
+  kp.two_phase = (cpr > 1 || var.nw == 16) ? 1 : static_cast<int>(env_size("SCB_2PH", l2_resident ? 1 : 0));
   kp.cpr = cpr;
   kp.world = sh ? sh->world : 1;
   kp.rank = sh ? sh->rank : 0;

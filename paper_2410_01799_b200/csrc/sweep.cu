@@ -2184,6 +2184,7 @@ void* kernel_for(const Variant& v) {
     SCB_K(float, 16, 2, 1)
     SCB_K(float, 8, 8, 1)
     SCB_K(float, 16, 5, 1)
+    SCB_K(float, 16, 7, 1)
     SCB_K2(float, 8, 4, 1)
     SCB_K2(float, 8, 2, 2)
   } else {
@@ -2215,8 +2216,11 @@ int pick_variant(int dtype, long long pitch, Variant* v) {
     v->vpt = 4; v->rg = dtype == 0 ? 1 : 2;
   } else if (dtype == 0 && nv > 2048 && nv <= 2560) {
     // rows of 8193..10240 f32 (C3's 3000 x 3 trailing block: 9000): whole rows with
-    // 16 consumer warps x 5 vectors, so the pass reads R once instead of two chunks
+    // 16 consumer warps x 5 vectors instead of two column chunks
     v->nw = 16; v->vpt = 5; v->rg = 1;
+  } else if (dtype == 0 && nv > 2560 && nv <= 3584) {
+    // rows of 10241..14336 f32 (C4's 4096 x 14336 down projection): 16 warps x 7 vectors
+    v->nw = 16; v->vpt = 7; v->rg = 1;
   } else {
     // nv <= 2048: whole rows; wider: the same tile over column chunks of 2048
     // vectors (8192 f32 / 4096 f64 columns, one TMA stage each, two-phase pass)

@@ -460,3 +460,20 @@ def test_rows_8k_to_10k_whole_row_variant(engine, ref, shape, dtype):
         assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
     np.testing.assert_allclose(rep._cut_values, od.cut_value, rtol=F32_TOL)
     assert sweeps_ok(rep.sweeps, od.iterations)
+
+
+@pytest.mark.parametrize("shape,dtype", [((1024, 12000), "f32"), ((512, 16000), "f32"), ((600, 5000), "f64")])
+def test_wide_rows_with_many_sweeps(engine, ref, shape, dtype):
+    """Rows past one warp tile (16-warp whole-row variants up to 14336 f32 columns; column
+    chunks beyond, and for f64 past 4096) on inputs that need several dense and delta sweeps:
+    the trajectory is the reference's (a regression of the chunked path with delta passes)."""
+    a = ref.fill_normal(8, shape[0] * shape[1]).reshape(shape)
+    if dtype == "f32":
+        a = a.astype(np.float32).astype(np.float64)
+    cfg = sc.DecomposeConfig(width=3, flush_width=1, record_curve=True, search=sc.SearchConfig(seed=4))
+    dec, rep, _ = engine.run(a.astype(np.float32) if dtype == "f32" else a, cfg, dtype=dtype)
+    od = ref.greedy_decompose(a, 3, seed=4, flush_width=1)
+    for i in range(2):
+        assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
+    assert sweeps_ok(rep.sweeps, od.iterations)
+    np.testing.assert_allclose(rep._cut_values, od.cut_value, rtol=F32_TOL if dtype == "f32" else F64_TOL)
