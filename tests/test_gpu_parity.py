@@ -477,3 +477,20 @@ def test_wide_rows_with_many_sweeps(engine, ref, shape, dtype):
         assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
     assert sweeps_ok(rep.sweeps, od.iterations)
     np.testing.assert_allclose(rep._cut_values, od.cut_value, rtol=F32_TOL if dtype == "f32" else F64_TOL)
+
+
+@pytest.mark.parametrize("idx", [0, 1, 6])  # q 4096^2, k 1024x4096, down 4096x14336
+def test_mistral_shapes_first_cuts_match_reference(engine, ref, idx):
+    """C4 inputs (rank-64 + noise, bf16-rounded, f32): the first cuts follow the reference's
+    trajectory exactly (all five shapes: profiles/r01/parity_shapes.txt)."""
+    from paper_2410_01799_b200.batch import mistral_jobs, mistral_matrix
+
+    j = mistral_jobs()[idx]
+    a = mistral_matrix(j)
+    cfg = sc.DecomposeConfig(width=2, flush_width=1, record_curve=True, search=sc.SearchConfig(seed=j.seed))
+    dec, rep, _ = engine.run(a, cfg, dtype="f32")
+    od = ref.greedy_decompose(a.astype(np.float64), 2, seed=j.seed, flush_width=1)
+    for i in range(2):
+        assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
+    assert (rep.sweeps == od.iterations).all()
+    np.testing.assert_allclose(rep._cut_values, od.cut_value, rtol=F32_TOL)
