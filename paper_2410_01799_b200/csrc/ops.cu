@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.h"
 
@@ -24,9 +25,9 @@ constexpr unsigned kFull = 0xffffffffu;
 // ---------------------------------------------------------------------------
 // expansion
 // ---------------------------------------------------------------------------
-constexpr int XR = 16;  // rows per CTA tile (f64 accumulators per column per thread)
 constexpr int XK = 32;  // terms per chunk (one u32 of column bits)
-constexpr int XW = 8;   // warps per CTA; a warp owns 64 columns (lane, lane + 32)
+// Tile shapes (template): XR rows per CTA tile (f64 accumulators per column per
+// thread), XW warps per CTA (a warp owns 64 columns: lane, lane + 32), MINB CTAs/SM.
 
 // 32x32 bit transpose across a warp: lane c returns the word whose bit L is bit c
 // of lane L's input (five butterfly rounds).
@@ -60,8 +61,8 @@ __device__ __forceinline__ double flipd(double x, uint32_t bit) {
 // exactly: mode A (COLCH = false) rho = flip(scale coef, u), kappa = +-1 (column
 // bit); mode B (COLCH, per-column channel coefficient) rho = +-1 (row bit),
 // kappa = flip(scale coef[ch(q)], v).
-template <bool COLCH>
-__global__ void __launch_bounds__(XW * 32, 2) expand_kernel(ExpandParams p) {
+template <bool COLCH, int XR, int XW, int MINB>
+__global__ void __launch_bounds__(XW * 32, MINB) expand_kernel(ExpandParams p) {
   __shared__ __align__(16) double rho[2][XR][XK];
   __shared__ double cc[2][XK][8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -353,17 +354,28 @@ cudaError_t launch_widen(const float* src, double* dst, long long n, cudaStream_
   return cudaGetLastError();
 }
 
-cudaError_t launch_expand(const ExpandParams& p, cudaStream_t st) {
-  if (p.P <= 0 || p.Q <= 0 || p.nterms <= 0) return cudaSuccess;
+template <int XR, int XW, int MINB>
+cudaError_t launch_expand_t(const ExpandParams& p, cudaStream_t st) {
   const long long gx = (p.Q + XW * 64 - 1) / (XW * 64);
   const long long gy = std::min<long long>((p.P + XR - 1) / XR, 65535);
   if (gx > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
   if (p.chan == 2)
-    expand_kernel<true><<<grid, XW * 32, 0, st>>>(p);
+    expand_kernel<true, XR, XW, MINB><<<grid, XW * 32, 0, st>>>(p);
   else
-    expand_kernel<false><<<grid, XW * 32, 0, st>>>(p);
+    expand_kernel<false, XR, XW, MINB><<<grid, XW * 32, 0, st>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const ExpandParams& p, cudaStream_t st) {
+  if (p.P <= 0 || p.Q <= 0 || p.nterms <= 0) return cudaSuccess;
+  // SCB_XTILE: tuning override (0: 16 rows x 8 warps x 2 CTAs/SM, 1: 24 x 4 x 3)
+  static const int tile = [] {
+    const char* e = std::getenv("SCB_XTILE");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (tile == 1) return launch_expand_t<24, 4, 3>(p, st);
+  return launch_expand_t<16, 8, 2>(p, st);
 }
 
 cudaError_t launch_kron(const KronParams& p, cudaStream_t st) {
