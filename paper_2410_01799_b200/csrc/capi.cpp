@@ -573,6 +573,10 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
       if (std::getenv("SCB_PROF_CTA")) {
         std::fprintf(stderr, "[scb cta] barrier wait per pass:");
         for (int g = 0; g < G; ++g) std::fprintf(stderr, " %.0f", static_cast<double>(hp[g * 16 + 6]) / np_);
+        std::fprintf(stderr, "\n[scb cta] dot pass per pass:");
+        for (int g = 0; g < G; ++g) std::fprintf(stderr, " %.0f", static_cast<double>(hp[g * 16 + 1]) / np_);
+        std::fprintf(stderr, "\n[scb cta] staging per pass:");
+        for (int g = 0; g < G; ++g) std::fprintf(stderr, " %.0f", static_cast<double>(hp[g * 16 + 5]) / np_);
         std::fprintf(stderr, "\n");
       }
       std::fprintf(stderr, "[scb prof3] per pass min/max over CTAs: chunks %.0f/%.0f passend %.0f/%.0f decision %.0f/%.0f reduce %.0f/%.0f staging %.0f/%.0f\n",
