@@ -245,8 +245,9 @@ sc_status contract(sc_ctx* ctx, const Layout& L, const DevFactors& F, uint64_t f
   if (sc_status s = scb::pool_get(ctx, "contract.part", sizeof(double) * scb::kContractCtas * scb::kContractTerms * 8, &part);
       s != SC_OK)
     return s;
-  if (sc_status s = scb::pool_get(ctx, "contract.out", sizeof(double) * 64, &out); s != SC_OK) return s;
-  std::vector<double> tmp(64);
+  // every batch writes its outputs at its own offset; one copy back at the end
+  const uint64_t nbatch = (count + per - 1) / per;
+  if (sc_status s = scb::pool_get(ctx, "contract.out", sizeof(double) * nbatch * per * slots, &out); s != SC_OK) return s;
   for (uint64_t b = 0; b < count; b += per) {
     const uint64_t nt = std::min<uint64_t>(per, count - b);
     const uint64_t j = first + b;
@@ -264,15 +265,16 @@ sc_status contract(sc_ctx* ctx, const Layout& L, const DevFactors& F, uint64_t f
     cp.chan = L.chan;
     cp.cstride = L.cstride;
     cp.part = static_cast<double*>(part);
-    cp.out = static_cast<double*>(out);
+    cp.out = static_cast<double*>(out) + b * slots;
     SC_CUDA(ctx, scb::launch_contract(cp, ctx->stream));
     st->kernel_launches += 2;
-    SC_CUDA(ctx, cudaMemcpyAsync(tmp.data(), out, nt * slots * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    SC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    st->d2h_bytes += nt * slots * 8;
-    for (uint64_t t = 0; t < nt; ++t)
-      for (int c = 0; c < L.nch; ++c) rhs_host[(b + t) * L.nch + c] = tmp[t * slots + c];
   }
+  std::vector<double> tmp(count * slots);
+  SC_CUDA(ctx, cudaMemcpyAsync(tmp.data(), out, count * slots * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  SC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  st->d2h_bytes += count * slots * 8;
+  for (uint64_t t = 0; t < count; ++t)
+    for (int c = 0; c < L.nch; ++c) rhs_host[t * L.nch + c] = tmp[t * slots + c];
   return SC_OK;
 }
 
