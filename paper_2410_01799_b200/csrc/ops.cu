@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(XW * 32, MINB) expand_kernel(ExpandParams p) {
         }
         rho[buf][r][b] = v;
       }
-      if (COLCH) {
+      if (COLCH && p.nch <= 8) {  // more channels: coefficients read directly (ccoef below)
         for (int e = tid; e < XK * p.nch; e += XW * 32) {
           const int b = e / p.nch, ch = e % p.nch;
           const long long j = static_cast<long long>(c) * XK + b;
@@ -113,6 +113,12 @@ __global__ void __launch_bounds__(XW * 32, MINB) expand_kernel(ExpandParams p) {
       }
     };
 
+    // scale * coef of (term b of chunk c, channel ch): staged for <= 8 channels, else global
+    auto ccoef = [&](int c, int buf, int b, int ch) -> double {
+      if (p.nch <= 8) return cc[buf][b][ch];
+      const long long j = static_cast<long long>(c) * XK + b;
+      return j < p.nterms ? p.scale * __ldg(p.coef + j * p.nch + ch) : 0.0;
+    };
     double acc[XR][2];
 #pragma unroll
     for (int r = 0; r < XR; ++r) acc[r][0] = acc[r][1] = 0.0;
@@ -134,10 +140,10 @@ __global__ void __launch_bounds__(XW * 32, MINB) expand_kernel(ExpandParams p) {
         for (int b = 0; b < XK; b += 2) {
           double k00, k01, k10, k11;
           if (COLCH) {
-            k00 = flipd(cc[buf][b][ch0], (v0 >> b) & 1u);
-            k01 = flipd(cc[buf][b + 1][ch0], (v0 >> (b + 1)) & 1u);
-            k10 = flipd(cc[buf][b][ch1], (v1 >> b) & 1u);
-            k11 = flipd(cc[buf][b + 1][ch1], (v1 >> (b + 1)) & 1u);
+            k00 = flipd(ccoef(c, buf, b, ch0), (v0 >> b) & 1u);
+            k01 = flipd(ccoef(c, buf, b + 1, ch0), (v0 >> (b + 1)) & 1u);
+            k10 = flipd(ccoef(c, buf, b, ch1), (v1 >> b) & 1u);
+            k11 = flipd(ccoef(c, buf, b + 1, ch1), (v1 >> (b + 1)) & 1u);
           } else {
             k00 = pm1(v0, b);
             k01 = pm1(v0, b + 1);
@@ -157,8 +163,8 @@ __global__ void __launch_bounds__(XW * 32, MINB) expand_kernel(ExpandParams p) {
         for (int b = 0; b < static_cast<int>(left); ++b) {
           double k0, k1;
           if (COLCH) {
-            k0 = flipd(cc[buf][b][ch0], (v0 >> b) & 1u);
-            k1 = flipd(cc[buf][b][ch1], (v1 >> b) & 1u);
+            k0 = flipd(ccoef(c, buf, b, ch0), (v0 >> b) & 1u);
+            k1 = flipd(ccoef(c, buf, b, ch1), (v1 >> b) & 1u);
           } else {
             k0 = pm1(v0, b);
             k1 = pm1(v1, b);

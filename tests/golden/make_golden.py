@@ -141,7 +141,8 @@ for i, (name, shape, ch, w) in enumerate(scd_cases):
 exp_cases = [("mat_37x70", (37, 70), -1, 40, 1.0, 0, False), ("resid_37x70", (37, 70), -1, 40, -1.0, 5, True),
              ("order3_5x7x3", (5, 7, 3), -1, 33, 1.0, 0, True), ("rgb_6x10x3", (6, 10, 3), 2, 12, -1.0, 0, True),
              ("chw_3x9x8", (3, 9, 8), 0, 9, 1.0, 2, False), ("vec_130", (130,), -1, 70, 1.0, 0, True),
-             ("wide_5x300", (5, 300), -1, 64, 1.0, 0, False), ("tall_150x3", (150, 3), -1, 31, -1.0, 0, True)]
+             ("wide_5x300", (5, 300), -1, 64, 1.0, 0, False), ("tall_150x3", (150, 3), -1, 31, -1.0, 0, True),
+             ("manych_6x20", (6, 20), 1, 40, -1.0, 3, True), ("manych_rows_12x9", (12, 9), 0, 33, 1.0, 0, True)]
 for i, (name, shape, ch, w, scale, first, base) in enumerate(exp_cases):
     fs, co = rand_factors(800 + i, shape, ch, w)
     d = fac_dict(fs, co, shape, ch)
