@@ -548,6 +548,10 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
     double acc[16] = {0};
     for (int g = 0; g < G; ++g)
       for (int i = 0; i < 16; ++i) acc[i] += static_cast<double>(hp[g * 16 + i]) / G;
+    if (!tensor)
+      std::fprintf(stderr, "[scb prof matrix] dot pass per dense pass %.0f, per delta pass %.0f cycles\n",
+                   acc[8] * G / std::max<double>(1.0, static_cast<double>(h_stats[2])) / G,
+                   acc[9] * G / std::max<double>(1.0, static_cast<double>(h_stats[3])) / G);
     if (tensor)
       std::fprintf(stderr, "[scb prof tensor] axis1 %.0f axis2 %.0f kron %.0f (slots 15, 8, 9 per dot pass)\n",
                    acc[15] / std::max<double>(1.0, static_cast<double>(h_stats[2])),

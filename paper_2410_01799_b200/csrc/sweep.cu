@@ -1856,6 +1856,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     if (prof && tid == 0) {
       const long long t = clock64();
       pacc[1] += t - t_pass0;
+      if (!p.tensor && (kind & F_DOT)) pten[(kind & F_DELTA) ? 5 : 4] += t - t_pass0;  // dense / delta split
       t_pass0 = t;
     }
     if (kind & (F_UPD | F_WB)) {
