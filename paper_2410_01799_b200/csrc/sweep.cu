@@ -2193,6 +2193,7 @@ void* kernel_for(const Variant& v) {
     SCB_K(double, 8, 2, 2)
     SCB_K(double, 8, 4, 2)
     SCB_K(double, 8, 8, 1)
+    SCB_K(double, 16, 7, 1)
   }
 #undef SCB_K
 #undef SCB_K2
@@ -2221,6 +2222,9 @@ int pick_variant(int dtype, long long pitch, Variant* v) {
     v->nw = 16; v->vpt = 5; v->rg = 1;
   } else if (dtype == 0 && nv > 2560 && nv <= 3584) {
     // rows of 10241..14336 f32 (C4's 4096 x 14336 down projection): 16 warps x 7 vectors
+    v->nw = 16; v->vpt = 7; v->rg = 1;
+  } else if (dtype == 1 && nv > 2048 && nv <= 3584) {
+    // rows of 4097..7168 f64: the same 16-warp x 7-vector tile
     v->nw = 16; v->vpt = 7; v->rg = 1;
   } else {
     // nv <= 2048: whole rows; wider: the same tile over column chunks of 2048
