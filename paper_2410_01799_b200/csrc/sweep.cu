@@ -1024,6 +1024,7 @@ struct DeltaArgs {
   long long pitch;
   unsigned rowB;
   int rows_g, nres, Q, NV, P;
+  int cpr;  // column chunks per row (1: whole rows)
 };
 
 template <typename E, int NW, int VPT>
@@ -1127,66 +1128,72 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
   }
   consumer_sync(NW * 32);
   // ---- dz over the rows whose sign flipped (ascending rows) ----
-  int vidx[VPT];
-  bool vok[VPT];
-#pragma unroll
-  for (int k = 0; k < VPT; ++k) {
-    const int v = (k * NW + warp) * 32 + lane;
-    vok[k] = v < NV;
-    vidx[k] = vok[k] ? v : 0;
-  }
-  double zacc[NE];
-#pragma unroll
-  for (int i = 0; i < NE; ++i) zacc[i] = 0.0;
+  // Rows wider than one warp tile (column chunks, cpr > 1) are covered chunk by
+  // chunk: the flipped rows are read once per chunk, each chunk's partial stored.
+  constexpr int chunkV = NW * 32 * VPT;
   bool any = false;
   const int sw = (rows_g + 31) / 32;
-  auto add_row = [&](int j, const VT (&xv)[VPT]) {
-    const double g = ((s_nxt[j >> 5] >> (j & 31)) & 1u) ? -2.0 : 2.0;
+  for (int ck = 0; ck < a.cpr; ++ck) {
+    int vidx[VPT];
+    bool vok[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
-      E x[EPV];
-      Vec<E>::split(xv[k], x);
-#pragma unroll
-      for (int e = 0; e < EPV; ++e) zacc[k * EPV + e] = fma(static_cast<double>(x[e]), g, zacc[k * EPV + e]);
+      const int v = ck * chunkV + (k * NW + warp) * 32 + lane;
+      vok[k] = v < NV;
+      vidx[k] = vok[k] ? v : 0;
     }
-  };
-  auto load_row = [&](int j, VT (&xv)[VPT]) {
-    const VT* rv = reinterpret_cast<const VT*>(row_ptr(j));
+    double zacc[NE];
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) xv[k] = j < nres ? rv[vidx[k]] : __ldcg(rv + vidx[k]);
-  };
-  int pend = -1;  // a flipped row whose loads are waiting for a partner (two rows per round trip)
-  for (int w = 0; w < sw; ++w) {
-    uint32_t f = s_nxt[w] ^ s_cur[w];
-    if (w == sw - 1 && (rows_g & 31)) f &= (1u << (rows_g & 31)) - 1u;
-    while (f) {
-      const int j = w * 32 + __ffs(f) - 1;
-      f &= f - 1;
-      any = true;
-      if (pend < 0) {
-        pend = j;
-        continue;
+    for (int i = 0; i < NE; ++i) zacc[i] = 0.0;
+    auto add_row = [&](int j, const VT (&xv)[VPT]) {
+      const double g = ((s_nxt[j >> 5] >> (j & 31)) & 1u) ? -2.0 : 2.0;
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        E x[EPV];
+        Vec<E>::split(xv[k], x);
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) zacc[k * EPV + e] = fma(static_cast<double>(x[e]), g, zacc[k * EPV + e]);
       }
-      VT x0[VPT], x1[VPT];
-      load_row(pend, x0);
-      load_row(j, x1);
-      add_row(pend, x0);  // ascending row order, as before
-      add_row(j, x1);
-      pend = -1;
+    };
+    auto load_row = [&](int j, VT (&xv)[VPT]) {
+      const VT* rv = reinterpret_cast<const VT*>(row_ptr(j));
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) xv[k] = j < nres ? rv[vidx[k]] : __ldcg(rv + vidx[k]);
+    };
+    int pend = -1;  // a flipped row whose loads are waiting for a partner (two rows per round trip)
+    for (int w = 0; w < sw; ++w) {
+      uint32_t f = s_nxt[w] ^ s_cur[w];
+      if (w == sw - 1 && (rows_g & 31)) f &= (1u << (rows_g & 31)) - 1u;
+      while (f) {
+        const int j = w * 32 + __ffs(f) - 1;
+        f &= f - 1;
+        any = true;
+        if (pend < 0) {
+          pend = j;
+          continue;
+        }
+        VT x0[VPT], x1[VPT];
+        load_row(pend, x0);
+        load_row(j, x1);
+        add_row(pend, x0);  // ascending row order, as before
+        add_row(j, x1);
+        pend = -1;
+      }
     }
-  }
-  if (pend >= 0) {
-    VT x0[VPT];
-    load_row(pend, x0);
-    add_row(pend, x0);
-  }
-  if (any) {  // uniform across the CTA (every thread walks the same bits)
+    if (pend >= 0) {
+      VT x0[VPT];
+      load_row(pend, x0);
+      add_row(pend, x0);
+    }
+    if (any) {  // uniform across the CTA (every thread walks the same bits)
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      if (vok[k]) {
+      for (int k = 0; k < VPT; ++k) {
+        if (vok[k]) {
 #pragma unroll
-        for (int e = 0; e < EPV; e += 2)
-          __stcg(reinterpret_cast<double2*>(a.zrow + vidx[k] * EPV + e), make_double2(zacc[k * EPV + e], zacc[k * EPV + e + 1]));
+          for (int e = 0; e < EPV; e += 2)
+            __stcg(reinterpret_cast<double2*>(a.zrow + static_cast<size_t>(vidx[k]) * EPV + e),
+                   make_double2(zacc[k * EPV + e], zacc[k * EPV + e + 1]));
+        }
       }
     }
   }
@@ -1776,6 +1783,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         dl.Q = p.Q;
         dl.NV = NV;
         dl.P = P;
+        dl.cpr = p.cpr;
         delta_pass<E, NW, VPT>(dl);
       } else if (p.cpr > 1) {
         da.rowB = static_cast<unsigned>(stageB);

@@ -462,7 +462,7 @@ def test_rows_8k_to_10k_whole_row_variant(engine, ref, shape, dtype):
     assert sweeps_ok(rep.sweeps, od.iterations)
 
 
-@pytest.mark.parametrize("shape,dtype", [((1024, 12000), "f32"), ((512, 16000), "f32"), ((600, 5000), "f64"),
+@pytest.mark.parametrize("shape,dtype", [((1024, 12000), "f32"), ((2048, 16384), "f32"), ((600, 5000), "f64"),
                                          ((300, 9000), "f64")])
 def test_wide_rows_with_many_sweeps(engine, ref, shape, dtype):
     """Rows past one warp tile (16-warp whole-row variants up to 14336 f32 / 7168 f64
