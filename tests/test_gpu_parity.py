@@ -332,7 +332,8 @@ def test_order3_wide_trailing_axes(engine, ref):
 
 
 # ------------------------------------------------------------ row sharding
-@pytest.mark.parametrize("shape,dtype", [((512, 1000), "f32"), ((300, 777), "f64"), ((200, 9000), "f32")])
+@pytest.mark.parametrize("shape,dtype", [((512, 1000), "f32"), ((300, 777), "f64"), ((200, 9000), "f32"),
+                                         ((300, 16384), "f32")])
 def test_sharded_world1_equals_engine(engine, ref, shape, dtype):
     """sc_greedy_decompose_sharded with one rank: the peer-memory exchange path
     (system-scope barrier off, peer tables of size 1) gives bit-identical results."""
