@@ -186,3 +186,28 @@ def test_tensor_decomposition_scd_round_trip(engine, ref):
     assert blob == ref.write_scd(a.shape, dec.factors, dec.coefficients, -1, 64)
     back = scio.read_scd(blob)
     assert (bits(engine.expand(back)) == bits(ref.accumulate_expansion(a.shape, dec.factors, dec.coefficients))).all()
+
+
+def test_around_edge_cases(engine, ref):
+    # 1 x 1 and single-row / single-column shapes through expansion, Gram and least squares
+    for shape in [(1, 1), (1, 9), (9, 1), (1,)]:
+        a = ref.fill_normal(9, int(np.prod(shape))).reshape(shape) + 0.5
+        dec, rep = engine.greedy_decompose(a, sc.DecomposeConfig(width=3, search=sc.SearchConfig(seed=2)), dtype="f64")
+        assert (bits(engine.expand(dec)) == bits(ref.accumulate_expansion(shape, dec.factors, dec.coefficients))).all()
+        g = engine.gram_matrix(dec)
+        gr, _ = ref.build_gram(a, dec.factors, dec.width())
+        assert (g == gr).all()
+        ld, lr = engine.lstsq_decompose(a, sc.DecomposeConfig(width=2, search=sc.SearchConfig(seed=2)))
+        od = ref.lstsq_decompose(a, 2, seed=2)
+        assert ld.width() == od.width
+        for x, y in zip(ld.factors, od.signs):
+            assert (x == y).all()
+    # non-finite input is rejected like the reference's DenseTensor
+    bad = np.ones((4, 5))
+    bad[2, 3] = np.nan
+    with pytest.raises(sc.InvalidArgument, match="non-finite"):
+        engine.lstsq_decompose(bad, sc.DecomposeConfig(width=1))
+    # correct_coefficients: shape mismatch like the reference
+    d = dec_of(load("gram_mat_37x70"))
+    with pytest.raises(sc.InvalidArgument, match="shape mismatch"):
+        engine.correct_coefficients(np.ones((3, 3)), d)
