@@ -35,6 +35,16 @@ sc_status put_msg(char* msg, size_t len, sc_status st, const std::string& s) {
   return st;
 }
 
+// Accumulates one call's accounting into the caller's (optional) stats.
+void add_stats(sc_op_stats* out, const sc_op_stats& st) {
+  if (out == nullptr) return;
+  out->kernel_ms += st.kernel_ms;
+  out->total_ms += st.total_ms;
+  out->h2d_bytes += st.h2d_bytes;
+  out->d2h_bytes += st.d2h_bytes;
+  out->kernel_launches += st.kernel_launches;
+}
+
 struct Timer {
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   double ms() const {
@@ -617,13 +627,7 @@ sc_status sc_accumulate_expansion(sc_ctx* ctx, const sc_factors* d, double scale
     st.kernel_ms = ms;
   }
   st.total_ms = tm.ms();
-  if (stats) {
-    stats->kernel_ms += st.kernel_ms;
-    stats->total_ms += st.total_ms;
-    stats->h2d_bytes += st.h2d_bytes;
-    stats->d2h_bytes += st.d2h_bytes;
-    stats->kernel_launches += st.kernel_launches;
-  }
+  add_stats(stats, st);
   return SC_OK;
 }
 
@@ -657,13 +661,7 @@ sc_status sc_gram_matrix(sc_ctx* ctx, const sc_factors* d, double* gram, sc_op_s
   SC_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   st.kernel_ms = ms;
   st.total_ms = tm.ms();
-  if (stats) {
-    stats->kernel_ms += st.kernel_ms;
-    stats->total_ms += st.total_ms;
-    stats->h2d_bytes += st.h2d_bytes;
-    stats->d2h_bytes += st.d2h_bytes;
-    stats->kernel_launches += st.kernel_launches;
-  }
+  add_stats(stats, st);
   return SC_OK;
 }
 
@@ -695,13 +693,7 @@ sc_status sc_contract_terms(sc_ctx* ctx, const sc_factors* d, int32_t a_dtype, c
   SC_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   st.kernel_ms = ms;
   st.total_ms = tm.ms();
-  if (stats) {
-    stats->kernel_ms += st.kernel_ms;
-    stats->total_ms += st.total_ms;
-    stats->h2d_bytes += st.h2d_bytes;
-    stats->d2h_bytes += st.d2h_bytes;
-    stats->kernel_launches += st.kernel_launches;
-  }
+  add_stats(stats, st);
   return SC_OK;
 }
 
