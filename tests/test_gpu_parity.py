@@ -496,3 +496,18 @@ def test_mistral_shapes_first_cuts_match_reference(engine, ref, idx):
         assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
     assert (rep.sweeps == od.iterations).all()
     np.testing.assert_allclose(rep._cut_values, od.cut_value, rtol=F32_TOL)
+
+
+def test_lockstep_f32_full_size_c2(engine, ref):
+    """The lockstep protocol at BASELINE config-2 size, at a cut past the f32 storage
+    divergence point (whole f32 trajectories part from the f64
+    reference around cut 23 at 4096^2): the reference's single cut on the GPU's own
+    remainder R_40 reproduces the GPU's cut 40 bit-exactly."""
+    k = 40
+    a = sc.fill_normal(1, 4096 * 4096, np.float32).reshape(4096, 4096)
+    _, _, rk = run(engine, a, k, seed=1, dtype="f32", remainder=True)
+    dec, rep, _ = run(engine, a, k + 1, seed=1, dtype="f32")
+    r = ref.signed_cut(rk.astype(np.float64), seed=ref.substream(1, k))
+    assert (dec.factors[0][k] == r["signs"][0]).all() and (dec.factors[1][k] == r["signs"][1]).all()
+    assert abs(rep._cut_values[k] - r["value"]) <= 1e-9 * abs(r["value"])
+    assert sweeps_ok(rep.sweeps[k:k + 1], [r["iterations"]])
