@@ -511,3 +511,30 @@ def test_lockstep_f32_full_size_c2(engine, ref):
     assert (dec.factors[0][k] == r["signs"][0]).all() and (dec.factors[1][k] == r["signs"][1]).all()
     assert abs(rep._cut_values[k] - r["value"]) <= 1e-9 * abs(r["value"])
     assert sweeps_ok(rep.sweeps[k:k + 1], [r["iterations"]])
+
+
+def test_c2_f64_whole_trajectory_16_cuts(engine, ref):
+    """Config 2 with f64 storage: the whole 16-cut trajectory is the reference's
+    (signs bit-identical, c and the exact residual within 1e-10)."""
+    a = sc.fill_normal(1, 4096 * 4096, np.float32).reshape(4096, 4096).astype(np.float64)
+    dec, rep, _ = run(engine, a, 16, seed=1, flush=1, dtype="f64")
+    od = ref.greedy_decompose(a, 16, seed=1, flush_width=1)
+    for i in range(2):
+        assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
+    assert np.max(np.abs(rep._cut_values - od.cut_value) / od.cut_value) <= F64_TOL
+    assert sweeps_ok(rep.sweeps, od.iterations)
+    assert abs(rep.final_residual_norm / rep.input_norm - od.final_residual_norm / od.input_norm) <= F64_TOL
+
+
+def test_c3_recipe_small_image_trajectory(engine, ref):
+    """The config-3 blob-image recipe at 400 x 300 x 3 (f32 storage): the first cuts of the
+    order-3 decomposition follow the reference's axial_run."""
+    from paper_2410_01799_b200.workloads import c3_blob_image
+
+    img = c3_blob_image(400, 300)
+    dec, rep, _ = run(engine, img, 8, seed=2, flush=1, dtype="f32")
+    od = ref.greedy_decompose(img.astype(np.float64), 8, seed=2, flush_width=1)
+    for i in range(3):
+        assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
+    assert sweeps_ok(rep.sweeps, od.iterations)
+    np.testing.assert_allclose(rep._cut_values, od.cut_value, rtol=F32_TOL)
