@@ -481,7 +481,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   kp.zstate = zstate;
   // Sparse delta passes between dense refreshes (matrices, any row length: the dz of
   // flipped rows walks every column chunk).
-  kp.delta = tensor ? 0 : static_cast<int>(env_size("SCB_DELTA", 1));
+  kp.delta = static_cast<int>(env_size("SCB_DELTA", 1));
   kp.delta_div = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_DIV", 32)));
   kp.delta_refresh = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_REFRESH", 16)));
   // Dot-pass form: the two-phase pass reads R twice per sweep but has no per-row

@@ -1271,8 +1271,8 @@ __device__ uint32_t kron_word(const KParams& p, const Ctl* ctl, const uint32_t* 
 // with a fixed butterfly -- so thousands of L2 loads are in flight instead of a
 // few warps walking the slices serially.  All index arithmetic is 32-bit.
 template <int CW>
-__device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_t* tws, Ctl* ctl, int P,
-                                      long long* tsplit) {
+__device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_t* tws, const uint32_t* tpass,
+                                      Ctl* ctl, int P, long long* tsplit) {
   constexpr int CT = CW * 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kax = p.kax;
@@ -1287,6 +1287,7 @@ __device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_
     }
   }
   double csum = 0.0;
+  if (tid == 0) ctl->nflip_next = 0;
   if (kax == 0 && tid == 0) csum = __ldcg(Z);  // order 1: c = <s_0, a> = Z[0]
   long long tprev = tsplit ? clock64() : 0;
   for (int i = 0; i < kax; ++i) {
@@ -1371,7 +1372,15 @@ __device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_
   }
   csum = warp_sum(csum);
   if (lane == 0) ctl->cred[warp] = csum;
-  for (int q = tid; q < p.Q; q += CT) tws[q] = kron_word(p, ctl, sax, q);
+  {
+    int nf = 0;  // flips of the next pass's t against this pass's (tpass, set at staging)
+    for (int q = tid; q < p.Q; q += CT) {
+      const uint32_t w = kron_word(p, ctl, sax, q);
+      nf += __popc(w ^ tpass[q]);
+      tws[q] = w;
+    }
+    if (nf) atomicAdd(&ctl->nflip_next, nf);
+  }
   consumer_sync(CT);
   if (tsplit && tid == 0) tsplit[2] += clock64() - tprev;
   if (tid == 0) {
@@ -1602,7 +1611,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       for (int j = 0; j < nls; ++j) {
         const int col = (q0 + j * GT) * 32 + lane;
         const size_t par = static_cast<size_t>(P & 1) * G * pitch + col;  // pass-parity buffer
-        if (!zmode && p.delta && lw == 0 && col < p.n) zsv[j] = __ldcg(p.zstate + col);  // issued early
+        if (p.delta && lw == 0 && col < p.n) zsv[j] = __ldcg(p.zstate + col);  // issued early
         double a = 0.0;
         for (int g0 = gs; g0 < ge; g0 += 32) {  // one round of up to 32 L2 loads in flight
           double v[32];
@@ -1626,7 +1635,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           for (int u = 0; u < 32; ++u) a += v[u];
         }
         zseg[(j * CW + lw) * 32 + lane] = a;
-        if (!zmode && p.delta && lw == 0) zst[j * 32 + lane] = (col < p.n) ? zsv[j] : 0.0;
+        if (p.delta && lw == 0) zst[j * 32 + lane] = (col < p.n) ? zsv[j] : 0.0;
       }
       psync();
       for (int j = lw; j < nls; j += NP) {
@@ -1636,7 +1645,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
 #pragma unroll
         for (int w = 0; w < NP; ++w) z += zseg[(j * CW + w) * 32 + lane];
         const bool valid = col < p.n;
-        if (!zmode && p.delta && valid) {  // z state for delta passes: dense sets it, delta adds to it
+        if (p.delta && valid) {  // z state for delta passes: dense sets it, delta adds to it
           const double zs = zst[j * 32 + lane];
           if (ctl->keep && !delta)
             z = zs;  // fixed point: z as cached
@@ -1703,7 +1712,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           tws[i] = static_cast<uint32_t>(x);
         }
       }
-      if (!p.tensor) {  // t flips since the previous pass (delta passes), counted exactly
+      {  // t flips since the previous pass (delta passes), counted exactly
         int nf = 0;
         for (int i = tid; i < p.Q; i += CT) {
           const uint32_t x = tws[i] ^ tprev[i];
@@ -1944,9 +1953,9 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     }
     if (p.tensor && (kind & F_DOT)) {  // order-k: Z = M^T s_0, then axes 1..k-1 and c
       const long long ta = prof ? clock64() : 0;
-      col_reduce(true, P, false, 0, 0);
+      col_reduce(true, P, (kind & F_DELTA) != 0, 0, 0);
       const long long tb = prof ? clock64() : 0;
-      axial_step<CW>(p, sax, tws, ctl, P, prof ? pten + 3 : nullptr);
+      axial_step<CW>(p, sax, tws, tprev, ctl, P, prof ? pten + 3 : nullptr);
       if (prof && tid == 0) {
         pten[0] += tb - ta;
         pten[1] += clock64() - tb;
@@ -2054,6 +2063,16 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
             next = F_DOT;
             if (p.tensor) {
               ctl->tsel = 0;  // next t = kron(new axes), already in tws
+              const int t = ctl->cur;  // this sweep's s_0 becomes the delta pass's previous s
+              ctl->cur = ctl->nxt;
+              ctl->nxt = t;
+              if (p.delta && ctl->since_dense + 1 < p.delta_refresh &&
+                  static_cast<long long>(ctl->nflip_next) * p.delta_div <= p.n) {
+                next |= F_DELTA;
+                ctl->since_dense += 1;
+              } else {
+                ctl->since_dense = 0;
+              }
             } else {
               const int t = ctl->cur;
               ctl->cur = ctl->nxt;

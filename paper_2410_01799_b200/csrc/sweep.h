@@ -47,6 +47,7 @@ struct Ctl {
   double ax_c;  // order-k mode: c = <s_{k-1}, v_{k-1}> of the axial step
   unsigned err_pre[4];  // error flags prefetched after the pass's grid barrier
   int nflip;            // columns of t that changed at this pass's staging (all CTAs agree)
+  int nflip_next;       // order-k: columns of the next pass's t (built by the axial step) that change
   int since_dense;      // delta passes since the last dense dot pass
   int has_dz;           // this CTA wrote a z partial in a delta pass
   int keep;             // t unchanged since the last dot pass: y, s, z stay exactly as cached

@@ -538,3 +538,20 @@ def test_c3_recipe_small_image_trajectory(engine, ref):
         assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
     assert sweeps_ok(rep.sweeps, od.iterations)
     np.testing.assert_allclose(rep._cut_values, od.cut_value, rtol=F32_TOL)
+
+
+@pytest.mark.parametrize("shape,dtype", [((200, 100, 6), "f64"), ((300, 90, 3), "f32"), ((40, 30, 20, 4), "f64")])
+def test_order_k_many_sweeps_with_delta_passes(engine, ref, shape, dtype):
+    """Order-k tensors with N(0,1) entries need many sweeps per cut, so the Kronecker t
+    changes little between late sweeps and delta passes run on the matrix view: the
+    trajectory stays the reference's axial_run."""
+    a = ref.fill_normal(77, int(np.prod(shape))).reshape(shape)
+    if dtype == "f32":
+        a = a.astype(np.float32).astype(np.float64)
+    dec, rep, _ = run(engine, a.astype(np.float32) if dtype == "f32" else a, 5, seed=6, flush=1, dtype=dtype)
+    od = ref.greedy_decompose(a, 5, seed=6, flush_width=1)
+    for i in range(len(shape)):
+        assert (dec.factors[i] == od.signs[i]).all(), f"axis {i}"
+    assert sweeps_ok(rep.sweeps, od.iterations)
+    assert max(rep.sweeps) >= 4  # several sweeps: delta passes between the dense first pass and the stop
+    np.testing.assert_allclose(rep._cut_values, od.cut_value, rtol=F32_TOL if dtype == "f32" else F64_TOL)
