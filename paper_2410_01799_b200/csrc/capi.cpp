@@ -268,6 +268,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   if (scb::pick_variant(dt, pitch, &var) != 0)
     return set_err(ctx, SC_NOT_SUPPORTED, "row length %llu exceeds the fused-kernel envelope",
                    static_cast<unsigned long long>(n));
+  var.tensor = tensor ? 1 : 0;  // order-k kernels are separate instantiations
 
   // wide rows: column chunks of one warp-tile pass (var.nw * 32 * var.vpt vectors)
   const long long tile_cols = static_cast<long long>(var.nw) * 32 * var.vpt * (dt == SC_F32 ? 4 : 2);

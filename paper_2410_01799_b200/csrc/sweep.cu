@@ -1287,7 +1287,7 @@ __device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_
     }
   }
   double csum = 0.0;
-  if (tid == 0) ctl->nflip_next = 0;
+  if (tid == 0) ctl->nflip = 0;  // recounted below for the next pass's t
   if (kax == 0 && tid == 0) csum = __ldcg(Z);  // order 1: c = <s_0, a> = Z[0]
   long long tprev = tsplit ? clock64() : 0;
   for (int i = 0; i < kax; ++i) {
@@ -1379,7 +1379,7 @@ __device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_
       nf += __popc(w ^ tpass[q]);
       tws[q] = w;
     }
-    if (nf) atomicAdd(&ctl->nflip_next, nf);
+    if (nf) atomicAdd(&ctl->nflip, nf);
   }
   consumer_sync(CT);
   if (tsplit && tid == 0) tsplit[2] += clock64() - tprev;
@@ -1391,11 +1391,27 @@ __device__ __noinline__ void axial_step(const KParams& p, uint32_t* sax, uint32_
 }
 
 // ---------------------------------------------------------------------------
+// Order-k controller step for a sweep that continues (kept out of line: the matrix
+// decision path stays compact in the instruction cache).  The next t is kron(new axes),
+// already in tws; this sweep's s_0 becomes the delta pass's previous s.
+__device__ __noinline__ int tensor_continue(Ctl* ctl, int delta, int refresh, int div, int n) {
+  ctl->tsel = 0;
+  const int t = ctl->cur;
+  ctl->cur = ctl->nxt;
+  ctl->nxt = t;
+  if (delta && ctl->since_dense + 1 < refresh && static_cast<long long>(ctl->nflip) * div <= n) {
+    ctl->since_dense += 1;
+    return F_DOT | F_DELTA;
+  }
+  ctl->since_dense = 0;
+  return F_DOT;
+}
+
 // Column ownership: consumer thread (warp w, lane l) owns the 16-byte vectors
 // v_k = (k * NW + w) * 32 + l, k < VPT, of every row (coalesced LDS.128), i.e.
 // NE = VPT * EPV elements per row, and the matching NE f64 column accumulators.
 // CPS: CTAs per SM (1, or 2 with a 112-register budget and raw lag buffers).
-template <typename E, int NW, int VPT, int RG, int CPS>
+template <typename E, int NW, int VPT, int RG, int CPS, bool TS>
 __device__ __forceinline__ void sweep_body(const KParams& p) {
   constexpr int EPV = Vec<E>::N;
   constexpr int CW = NW;       // consumer warps
@@ -1455,7 +1471,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     ctl->decided = 1;
     ctl->stored = 0;
     ctl->abort = 0;
-    ctl->pp = p.tensor ? 1 : 0;  // order-k: pp = sweep of the current pass (1-based)
+    ctl->pp = TS ? 1 : 0;  // order-k: pp = sweep of the current pass (1-based)
     for (int j = 0; j < 8; ++j) {  // read by the axial step from shared memory, not the param copy
       ctl->axn[j] = j < 7 ? p.ax_n[j] : 1;
       ctl->axoff[j] = j < 7 ? p.ax_off[j] : 0;
@@ -1697,11 +1713,11 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         const uint32_t* tw =
             p.t0 + (static_cast<size_t>(ctl->term) * p.restarts + ctl->restart) * p.t0_stride;
         for (int i = tid; i < p.Q; i += CT) tws[i] = __ldg(tw + i);
-        if (p.tensor) {  // drawn start signs of axes 1..k-1 (search.hpp:197)
+        if (TS) {  // drawn start signs of axes 1..k-1 (search.hpp:197)
           const uint32_t* aw = p.ax0 + (static_cast<size_t>(ctl->term) * p.restarts + ctl->restart) * p.axw;
           for (int i = tid; i < p.axw; i += CT) sax[i] = __ldg(aw + i);
         }
-      } else if (!p.tensor) {  // order-k: tws was rebuilt by the previous pass's axial step
+      } else if (!TS) {  // order-k: tws was rebuilt by the previous pass's axial step
         // t words were published before the last grid barrier, tagged with this pass
         const unsigned long long* tw = p.tb64 + static_cast<size_t>(ctl->tsel) * p.Q;
         for (int i = tid; i < p.Q; i += CT) {
@@ -1726,7 +1742,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       if (tid == 0)
         for (int i = 0; i < p.sw; ++i) s_nxt[i] = 0u;
     }
-    if ((kind & F_UPD) && !p.tensor) {  // order-k: uws = kron(best axes), built at term accept
+    if ((kind & F_UPD) && !TS) {  // order-k: uws = kron(best axes), built at term accept
       for (int i = tid; i < p.Q; i += CT)
         uws[i] = ctl->utsel == 2 ? __ldcg(p.tbest + i)
                                  : static_cast<uint32_t>(__ldcg(p.tb64 + static_cast<size_t>(ctl->utsel) * p.Q + i));
@@ -1737,7 +1753,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     // products: y, s' and z stay exactly as cached whatever pass form runs, so a
     // dense refresh can never nudge c by rounding there (the reference's caches
     // behave the same way outside its 16-sweep refreshes).
-    const bool keep = (kind & F_DOT) && !p.tensor && p.delta && pp >= 1 && ctl->nflip == 0;
+    const bool keep = (kind & F_DOT) && !TS && p.delta && pp >= 1 && ctl->nflip == 0;
     if (keep && !(kind & F_DELTA))
       for (int j = tid; j < rows_g; j += CT) ybak[j] = yrow[j];
 
@@ -1873,7 +1889,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     if (prof && tid == 0) {
       const long long t = clock64();
       pacc[1] += t - t_pass0;
-      if (!p.tensor && (kind & F_DOT)) pten[(kind & F_DELTA) ? 5 : 4] += t - t_pass0;  // dense / delta split
+      if (!TS && (kind & F_DOT)) pten[(kind & F_DELTA) ? 5 : 4] += t - t_pass0;  // dense / delta split
       t_pass0 = t;
     }
     if (kind & (F_UPD | F_WB)) {
@@ -1889,7 +1905,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     if (warp == 0) {
       // this CTA's c partial: sum_i s_i y_i in row order (lane-strided, fixed tree)
       double cl = 0.0;
-      if ((kind & F_DOT) && pp >= 1 && !p.tensor)
+      if ((kind & F_DOT) && pp >= 1 && !TS)
         for (int j = lane; j < rows_g; j += 32)
           cl += flipd(yrow[j], ((s_cur[j >> 5] >> (j & 31)) & 1u) << 31);
       cl = warp_sum(cl);
@@ -1951,7 +1967,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       pacc[2] += t - t_pass0;
       t_pass0 = t;
     }
-    if (p.tensor && (kind & F_DOT)) {  // order-k: Z = M^T s_0, then axes 1..k-1 and c
+    if (TS && (kind & F_DOT)) {  // order-k: Z = M^T s_0, then axes 1..k-1 and c
       const long long ta = prof ? clock64() : 0;
       col_reduce(true, P, (kind & F_DELTA) != 0, 0, 0);
       const long long tb = prof ? clock64() : 0;
@@ -1964,7 +1980,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
 
     // Matrix dot pass: owners reduce z and publish the next t right away (it does
     // not depend on the decision), taking the decision off every CTA's critical path.
-    if (!p.tensor && (kind & F_DOT) && warp >= 1)  // warp 0 runs the decision below meanwhile
+    if (!TS && (kind & F_DOT) && warp >= 1)  // warp 0 runs the decision below meanwhile
       col_reduce(false, P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
 
     // ------------------------------ decision ------------------------------
@@ -1984,13 +2000,13 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
               const int i = r0 + l;
               atomicOr(srow + (i >> 5), 1u << (i & 31));
             }
-          if (g == 0 && p.tensor) {  // axes 1..k-1 of the accepted term
+          if (g == 0 && TS) {  // axes 1..k-1 of the accepted term
             for (int i = 0; i < p.axw; ++i) p.AX_out[static_cast<size_t>(term) * p.axw + i] = sax_best[i];
           }
           if (g == 0) {
             uint32_t* trow = p.T_out + static_cast<size_t>(term) * p.t_stride;
             const int nw = min(p.t_stride, p.Q);  // words past Q are pad (zero)
-            if (p.tensor) {
+            if (TS) {
               for (int i = 0; i < nw; ++i) trow[i] = 0u;  // order-k: per-axis words are in AX_out
             } else if (ctl->best_tsel == 2) {
               for (int i = 0; i < nw; ++i) trow[i] = __ldcg(p.tbest + i);
@@ -2006,13 +2022,13 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           }
           ctl->alpha = bc / p.numel_d;  // alpha = c / numel (decompose.hpp:340)
           ctl->utsel = ctl->best_tsel;
-          ctl->kron_upd = p.tensor;  // order-k: uws = kron(best axes) after the decision
+          ctl->kron_upd = TS;  // order-k: uws = kron(best axes) after the decision
           ctl->term = static_cast<int>(term + 1);
           ctl->norm_idx = static_cast<int>(term + 1);
           if (term + 1 >= p.width) {
             return F_UPD | F_NORM | F_WB;
           } else {
-            ctl->pp = p.tensor ? 1 : 0;
+            ctl->pp = TS ? 1 : 0;
             ctl->restart = 0;
             ctl->tsel = -1;
             ctl->c_prev = -INFINITY;
@@ -2041,7 +2057,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           next = K_TERM;  // final write-back done
         } else if (!(kind & F_DOT)) {
           next = F_DOT;   // maintenance pass (initial norm / rank-1 update) -> search
-        } else if (!p.tensor && pp == 0) {
+        } else if (!TS && pp == 0) {
           const int t = ctl->cur;  // s_1 (just computed) becomes current
           ctl->cur = ctl->nxt;
           ctl->nxt = t;
@@ -2052,7 +2068,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           ctl->since_dense = 0;
         } else {
           // matrix: c = <s_pp, R t_pp> from this pass's y; order-k: c of this sweep's axial step
-          const double c = p.tensor ? ctl->ax_c : cs;
+          const double c = TS ? ctl->ax_c : cs;
           // SearchDiagnostics::sweep_values of term 0 (search.hpp:177, :207), per restart
           if (p.sweep_vals != nullptr && ctl->term == 0 && g == 0)
             p.sweep_vals[static_cast<size_t>(ctl->restart) * p.max_sweeps + (pp - 1)] = c;
@@ -2061,18 +2077,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
             ctl->c_prev = c;
             ctl->pp = pp + 1;
             next = F_DOT;
-            if (p.tensor) {
-              ctl->tsel = 0;  // next t = kron(new axes), already in tws
-              const int t = ctl->cur;  // this sweep's s_0 becomes the delta pass's previous s
-              ctl->cur = ctl->nxt;
-              ctl->nxt = t;
-              if (p.delta && ctl->since_dense + 1 < p.delta_refresh &&
-                  static_cast<long long>(ctl->nflip_next) * p.delta_div <= p.n) {
-                next |= F_DELTA;
-                ctl->since_dense += 1;
-              } else {
-                ctl->since_dense = 0;
-              }
+            if (TS) {
+              next = tensor_continue(ctl, p.delta, p.delta_refresh, p.delta_div, p.n);
             } else {
               const int t = ctl->cur;
               ctl->cur = ctl->nxt;
@@ -2089,7 +2095,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
                 ctl->since_dense = 0;
               }
             }
-          } else if (p.tensor) {
+          } else if (TS) {
             // axial_run returns the current sweep's (c, signs) (search.hpp:206, :210)
             const bool better = (ctl->restart == 0) || (c > ctl->best_c);
             if (better) {
@@ -2154,7 +2160,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       pacc[3] += t - t_pass0;
       t_pass0 = t;
     }
-    if (p.tensor && ctl->kron_upd) {  // order-k: t of the rank-1 update = kron(best axes)
+    if (TS && ctl->kron_upd) {  // order-k: t of the rank-1 update = kron(best axes)
       for (int q = tid; q < p.Q; q += CT) uws[q] = kron_word(p, ctl, sax_best, q);
       consumer_sync(CT);
       if (tid == 0) ctl->kron_upd = 0;
@@ -2179,30 +2185,33 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   }
 }
 
-template <typename E, int NW, int VPT, int RG>
+// TS: order-k (tensor) instantiation.  Matrix kernels carry no order-k code at all,
+// which keeps their per-pass serial sections compact.
+template <typename E, int NW, int VPT, int RG, bool TS>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p) {
-  sweep_body<E, NW, VPT, RG, 1>(p);
+  sweep_body<E, NW, VPT, RG, 1, TS>(p);
 }
 template <typename E, int NW, int VPT, int RG>
 __global__ void __maxnreg__(112) sweep_kernel2(const KParams p) {
-  sweep_body<E, NW, VPT, RG, 2>(p);
+  sweep_body<E, NW, VPT, RG, 2, false>(p);
 }
 
 template <typename E, int NW, int VPT, int RG, int CPS>
 struct Kern {
-  static void* fn() {
+  static void* fn(bool tensor) {
     if constexpr (CPS == 1)
-      return reinterpret_cast<void*>(&sweep_kernel<E, NW, VPT, RG>);
+      return tensor ? reinterpret_cast<void*>(&sweep_kernel<E, NW, VPT, RG, true>)
+                    : reinterpret_cast<void*>(&sweep_kernel<E, NW, VPT, RG, false>);
     else
-      return reinterpret_cast<void*>(&sweep_kernel2<E, NW, VPT, RG>);
+      return tensor ? nullptr : reinterpret_cast<void*>(&sweep_kernel2<E, NW, VPT, RG>);
   }
 };
 
 void* kernel_for(const Variant& v) {
 #define SCB_K(E, NW, VPT, RG) \
-  if (v.nw == NW && v.vpt == VPT && v.rg == RG && v.cps == 1) return Kern<E, NW, VPT, RG, 1>::fn();
+  if (v.nw == NW && v.vpt == VPT && v.rg == RG && v.cps == 1) return Kern<E, NW, VPT, RG, 1>::fn(v.tensor != 0);
 #define SCB_K2(E, NW, VPT, RG) \
-  if (v.nw == NW && v.vpt == VPT && v.rg == RG && v.cps == 2) return Kern<E, NW, VPT, RG, 2>::fn();
+  if (v.nw == NW && v.vpt == VPT && v.rg == RG && v.cps == 2) return Kern<E, NW, VPT, RG, 2>::fn(v.tensor != 0);
   if (v.dtype == 0) {
     SCB_K(float, 8, 1, 4)
     SCB_K(float, 8, 2, 2)
@@ -2236,6 +2245,7 @@ int pick_variant(int dtype, long long pitch, Variant* v) {
   const long long nv = pitch / epv;
   v->dtype = dtype;
   v->cps = 1;
+  v->tensor = 0;
   v->nw = 8;
   if (nv <= 256) {
     v->vpt = 1; v->rg = 4;

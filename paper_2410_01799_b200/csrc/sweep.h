@@ -46,8 +46,8 @@ struct Ctl {
   double alpha, c_prev, best_c, first_value;
   double ax_c;  // order-k mode: c = <s_{k-1}, v_{k-1}> of the axial step
   unsigned err_pre[4];  // error flags prefetched after the pass's grid barrier
-  int nflip;            // columns of t that changed at this pass's staging (all CTAs agree)
-  int nflip_next;       // order-k: columns of the next pass's t (built by the axial step) that change
+  int nflip;            // columns of t that changed at this pass's staging (all CTAs agree); order-k:
+                        // recounted by the axial step for the next pass's t (read by the decision)
   int since_dense;      // delta passes since the last dense dot pass
   int has_dz;           // this CTA wrote a z partial in a delta pass
   int keep;             // t unchanged since the last dot pass: y, s, z stay exactly as cached
@@ -127,6 +127,7 @@ struct Variant {
   int vpt;    // 16-byte vectors per thread per row
   int rg;     // rows per group (one dot-partial publication per group)
   int cps;    // CTAs per SM (2: 113-register budget, raw lag buffers)
+  int tensor; // order-k instantiation (set by the host after pick_variant)
 };
 
 constexpr int kRing = 4;  // dot-partial ring depth (groups)
