@@ -262,6 +262,7 @@ def main():
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                     "l2_traffic": (traffic or {}).get("l2_bytes_per_launch"),
                      "peak_source": peak_src,
                      "algorithmic_bytes": "sum_j (2*sweeps_j+1)*m*n*4 per launch (SURVEY 8d)",
                      "passes_per_launch": passes / args.steps,
@@ -269,7 +270,8 @@ def main():
                      "note": "algorithmic bytes count every half-iteration as a full read of R (the "
                              "BASELINE formula); the engine reads less: one pass per sweep, R resident in "
                              "SMEM/L2, and sparse delta passes (flipped t columns / s rows only) between "
-                             "dense refreshes, so frac can exceed 1; physical DRAM traffic is 'traffic'"},
+                             "dense refreshes, so frac can exceed 1; physical DRAM traffic is 'traffic', L2 traffic "
+                             "(lts__t_sectors x 32 B, same ncu capture) is 'l2_traffic'"},
         "sweeps_per_cut_mean": float(np.mean(sweeps)),
         "clocks": clocks,
     }

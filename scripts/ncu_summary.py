@@ -23,6 +23,7 @@ FULL_METRICS = [
     ("dram__bytes_read.sum", "DRAM bytes read"),
     ("dram__bytes_write.sum", "DRAM bytes written"),
     ("lts__t_bytes.sum", "L2 bytes (all)"),
+    ("lts__t_sectors.sum", "L2 sectors (all, x32 B)"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % of peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % of peak"),
@@ -102,6 +103,8 @@ def full(tag, dst):
         "dram_read_bytes": num("dram__bytes_read.sum", 1),
         "dram_write_bytes": num("dram__bytes_write.sum", 1),
         "duration_s_under_ncu": num("gpu__time_duration.sum", 1),
+        "l2_bytes_per_launch": (float(get["lts__t_sectors.sum"][0].replace(",", "")) * 32.0
+                                if "lts__t_sectors.sum" in get else None),
         "source": f"profiles/{os.path.basename(dst)}/sweep_kernel_full.txt",
     }
     with open(os.path.join(ROOT, "profiles", "latest_kernel_traffic.json"), "w") as f:
