@@ -118,6 +118,15 @@ typedef struct oracle_output {
 ORACLE_DECLARE(orc_)
 ORACLE_DECLARE(ref_)
 
+/* Reference-only checkers of the PPM / CSV helpers (io.hpp:294-396): the product's
+ * byte formats are compared with the reference's own streams (no restatement). */
+int ref_write_ppm(uint64_t height, uint64_t width, const double* data, uint8_t* buf, uint64_t cap, uint64_t* size);
+int ref_read_ppm(const uint8_t* buf, uint64_t size, uint64_t* height, uint64_t* width, double* data);
+int ref_write_curve_csv(uint64_t n, const uint64_t* widths, const double* rates, const double* errors, char* buf,
+                        uint64_t cap, uint64_t* size);
+int ref_read_curve_csv(const char* buf, uint64_t size, uint64_t* n, uint64_t* widths, double* rates,
+                       double* errors);
+
 #ifdef __cplusplus
 }
 #endif

@@ -338,6 +338,64 @@ class Oracle:
         return out
 
 
+# -- reference-only PPM / CSV helpers (io.hpp:294-396) --------------------------
+def _ref_extra(oracle):
+    L = oracle.lib
+    sig = {
+        "ref_write_ppm": (C.c_int, [u64, u64, P(C.c_double), P(C.c_uint8), u64, P(u64)]),
+        "ref_read_ppm": (C.c_int, [P(C.c_uint8), u64, P(u64), P(u64), P(C.c_double)]),
+        "ref_write_curve_csv": (C.c_int, [u64, P(u64), P(C.c_double), P(C.c_double), C.c_char_p, u64, P(u64)]),
+        "ref_read_curve_csv": (C.c_int, [C.c_char_p, u64, P(u64), P(u64), P(C.c_double), P(C.c_double)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    return L
+
+
+def ref_write_ppm(oracle, a) -> bytes:
+    L = _ref_extra(oracle)
+    a = np.ascontiguousarray(a, np.float64)
+    cap = 64 + a.size
+    buf = np.zeros(cap, np.uint8)
+    size = u64()
+    oracle._err(L.ref_write_ppm(a.shape[0], a.shape[1], _ptr(a, C.c_double), _ptr(buf, C.c_uint8), cap, C.byref(size)))
+    return bytes(buf[: size.value])
+
+
+def ref_read_ppm(oracle, data: bytes) -> np.ndarray:
+    L = _ref_extra(oracle)
+    buf = np.frombuffer(data, np.uint8).copy() if data else np.zeros(1, np.uint8)
+    h, w = u64(), u64()
+    oracle._err(L.ref_read_ppm(_ptr(buf, C.c_uint8), len(data), C.byref(h), C.byref(w), None))
+    out = np.zeros((h.value, w.value, 3))
+    oracle._err(L.ref_read_ppm(_ptr(buf, C.c_uint8), len(data), C.byref(h), C.byref(w), _ptr(out, C.c_double)))
+    return out
+
+
+def ref_write_curve_csv(oracle, points) -> str:
+    L = _ref_extra(oracle)
+    w = np.array([p[0] for p in points], np.uint64)
+    r = np.array([p[1] for p in points], np.float64)
+    e = np.array([p[2] for p in points], np.float64)
+    cap = 64 + 80 * len(points)
+    buf = C.create_string_buffer(cap)
+    size = u64()
+    oracle._err(L.ref_write_curve_csv(len(points), _ptr(w, u64), _ptr(r, C.c_double), _ptr(e, C.c_double), buf, cap,
+                                      C.byref(size)))
+    return buf.raw[: size.value].decode()
+
+
+def ref_read_curve_csv(oracle, text: str):
+    L = _ref_extra(oracle)
+    b = text.encode()
+    n = u64()
+    oracle._err(L.ref_read_curve_csv(b, len(b), C.byref(n), None, None, None))
+    w, r, e = np.zeros(n.value, np.uint64), np.zeros(n.value), np.zeros(n.value)
+    oracle._err(L.ref_read_curve_csv(b, len(b), C.byref(n), _ptr(w, u64), _ptr(r, C.c_double), _ptr(e, C.c_double)))
+    return [(int(a), float(x), float(y)) for a, x, y in zip(w, r, e)]
+
+
 def normal_matrix(seed: int, shape, oracle: Oracle | None = None) -> np.ndarray:
     """Row-major Xoshiro256pp(seed).next_normal() stream (inc/rng.hpp:58-71)."""
     o = oracle or Oracle("orc")

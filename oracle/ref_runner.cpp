@@ -343,4 +343,67 @@ int ref_read_raw(const uint8_t* buf, uint64_t size, int* order, uint64_t* shape,
   }
 }
 
+int ref_write_ppm(uint64_t height, uint64_t width, const double* data, uint8_t* buf, uint64_t cap, uint64_t* size) {
+  try {
+    auto t = sigcut::DenseTensor::from_raw({height, width, 3}, std::vector<double>(data, data + height * width * 3));
+    std::ostringstream os(std::ios::binary);
+    sigcut::write_ppm(os, t);
+    const std::string b = os.str();
+    *size = b.size();
+    if (b.size() > cap) throw std::invalid_argument("buffer too small");
+    std::memcpy(buf, b.data(), b.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_read_ppm(const uint8_t* buf, uint64_t size, uint64_t* height, uint64_t* width, double* data) {
+  try {
+    std::istringstream is(std::string(reinterpret_cast<const char*>(buf), size), std::ios::binary);
+    const auto t = sigcut::read_ppm(is);
+    *height = t.shape()[0];
+    *width = t.shape()[1];
+    if (data != nullptr) std::memcpy(data, t.data().data(), t.numel() * 8);
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_write_curve_csv(uint64_t n, const uint64_t* widths, const double* rates, const double* errors, char* buf,
+                        uint64_t cap, uint64_t* size) {
+  try {
+    std::vector<sigcut::CurvePoint> pts(n);
+    for (uint64_t i = 0; i < n; ++i) pts[i] = sigcut::CurvePoint{widths[i], rates[i], errors[i]};
+    std::ostringstream os;
+    sigcut::write_curve_csv(os, pts);
+    const std::string b = os.str();
+    *size = b.size();
+    if (b.size() > cap) throw std::invalid_argument("buffer too small");
+    std::memcpy(buf, b.data(), b.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_read_curve_csv(const char* buf, uint64_t size, uint64_t* n, uint64_t* widths, double* rates,
+                       double* errors) {
+  try {
+    std::istringstream is(std::string(buf, size));
+    const auto pts = sigcut::read_curve_csv(is);
+    *n = pts.size();
+    if (widths != nullptr)
+      for (std::size_t i = 0; i < pts.size(); ++i) {
+        widths[i] = pts[i].width;
+        rates[i] = pts[i].compression_rate;
+        errors[i] = pts[i].relative_error;
+      }
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
 }  // extern "C"

@@ -8,6 +8,9 @@ this module                reference (proj/include/sigcut/io.hpp)
 ``read_scd``               ``read_scd``             :168-213
 ``write_raw``              ``write_raw``            :226-246
 ``read_raw``               ``read_raw``             :250-292
+``write_ppm`` / ``read_ppm`` ``write_ppm`` / ``read_ppm`` :324-356
+``write_curve_csv`` etc.   ``write_curve_csv`` / ``read_curve_csv`` :363-396
+``emit_curve``             ``emit_curve``   (metrics.hpp:101-111)
 ``IOError_``               ``sigcut::io_error``     :22-24
 =========================  =====================================
 
@@ -19,6 +22,7 @@ compute).
 from __future__ import annotations
 
 import ctypes as C
+import re
 
 import numpy as np
 
@@ -115,3 +119,117 @@ def read_raw(data: bytes, return_source_bits: bool = False):
     if return_source_bits:
         return out, {0: 64, 1: 32, 2: 8}[dt.value]
     return out
+
+
+# ---------------------------------------------------------------------------
+# PPM (io.hpp:294-356) and CSV curve reports (io.hpp:358-396), with the curve
+# helper emit_curve (metrics.hpp:99-111).  Plain byte/text formats on the host.
+# ---------------------------------------------------------------------------
+def write_ppm(a) -> bytes:
+    """Binary P6, maxval 255; values clamped to [0, 255], halves rounded away from zero."""
+    a = np.asarray(a, np.float64)
+    if a.ndim != 3 or a.shape[2] != 3:
+        raise InvalidArgument("write_ppm: tensor must have shape m x n x 3")
+    h, w = a.shape[0], a.shape[1]
+    body = np.floor(np.clip(a, 0.0, 255.0) + 0.5).astype(np.uint8)  # lround on [0, 255]
+    return f"P6\n{w} {h}\n255\n".encode() + body.tobytes()
+
+
+def _isspace(c) -> bool:  # C isspace in the "C" locale
+    return c is not None and c in b" \t\n\v\f\r"
+
+
+def _isdigit(c) -> bool:
+    return c is not None and 48 <= c <= 57
+
+
+def _ppm_token(data: bytes, pos: int):
+    n = len(data)
+    c = data[pos] if pos < n else None
+    pos += 1
+    while c is not None and (_isspace(c) or c == ord("#")):
+        if c == ord("#"):
+            while c is not None and c != ord("\n"):
+                c = data[pos] if pos < n else None
+                pos += 1
+        c = data[pos] if pos < n else None
+        pos += 1
+    if not _isdigit(c):
+        raise IOError_("malformed PPM header")
+    value = 0
+    while _isdigit(c):
+        value = value * 10 + (c - ord("0"))
+        if value > (1 << 32):
+            raise IOError_("PPM dimension overflow")
+        c = data[pos] if pos < n else None
+        pos += 1
+    if c is not None:
+        pos -= 1  # unget
+    return value, pos
+
+
+def read_ppm(data: bytes) -> np.ndarray:
+    """height x width x 3 float64 in [0, 255] (read_ppm, io.hpp:324-340)."""
+    data = bytes(data)
+    if len(data) < 2:
+        raise IOError_("truncated payload")
+    if data[:2] != b"P6":
+        raise IOError_("not a binary P6 PPM")
+    pos = 2
+    width, pos = _ppm_token(data, pos)
+    height, pos = _ppm_token(data, pos)
+    maxval, pos = _ppm_token(data, pos)
+    if maxval != 255:
+        raise IOError_("PPM maxval must be 255")
+    if pos >= len(data) or not _isspace(data[pos]):
+        raise IOError_("malformed PPM header")
+    pos += 1
+    if width == 0 or height == 0:
+        raise IOError_("PPM with empty dimensions")
+    count = height * width * 3
+    if len(data) - pos < count:
+        raise IOError_("truncated payload")
+    px = np.frombuffer(data, np.uint8, count=count, offset=pos)
+    return px.astype(np.float64).reshape(height, width, 3)
+
+
+def emit_curve(report, shape, coeff_bits: int = 64, source_bits: int = 64, channel_axis: int = -1):
+    """(width, compression_rate, relative_error) rows from the width-0 point (0, 0, 1)."""
+    if report.input_norm == 0.0:
+        raise InvalidArgument("emit_curve: zero input norm")
+    shape = tuple(int(x) for x in shape)
+    channels = shape[channel_axis] if channel_axis >= 0 else 1
+    bits = coeff_bits * channels + sum(n for i, n in enumerate(shape) if i != channel_axis)
+    src = float(source_bits) * float(np.prod([float(x) for x in shape]))
+    pts = [(0, 0.0, 1.0)]
+    for st in report.steps:
+        pts.append((int(st.k), st.k * float(bits) / src, st.residual_norm / report.input_norm))
+    return pts
+
+
+def write_curve_csv(points) -> str:
+    """`width,compression_rate,relative_error`, full-precision decimals (%.17g)."""
+    out = ["width,compression_rate,relative_error\n"]
+    for w, rate, err in points:
+        out.append(f"{int(w)},{'%.17g' % rate},{'%.17g' % err}\n")
+    return "".join(out)
+
+
+_CSV_NUM = re.compile(r"-?(?:(?:\d+\.?\d*|\.\d+)(?:[eE][-+]?\d+)?|inf(?:inity)?|nan(?:\([0-9A-Za-z_]*\))?)",
+                      re.IGNORECASE)
+
+
+def read_curve_csv(text: str):
+    lines = text.split("\n")
+    if not lines or lines[0] != "width,compression_rate,relative_error":
+        raise IOError_("bad CSV header")
+    pts = []
+    for line in lines[1:]:
+        if not line:
+            continue
+        parts = line.split(",")
+        if len(parts) != 3 or not re.fullmatch(r"[0-9]+", parts[0]) or not _CSV_NUM.fullmatch(parts[1]) \
+                or not _CSV_NUM.fullmatch(parts[2]):
+            raise IOError_("bad CSV row")
+        pts.append((int(parts[0]), float(parts[1]), float(parts[2])))
+    return pts

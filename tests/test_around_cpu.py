@@ -202,3 +202,64 @@ def test_c3_blob_image_recipe():
     assert img.shape == (40, 30, 3) and img.dtype == np.float32
     assert img.min() >= 0.0 and img.max() <= 1.0
     assert (c3_blob_image(40, 30) == img).all()  # seeded, deterministic
+
+
+# ---------------------------------------------------------------- PPM / CSV (io.hpp:294-396)
+def _ref_only(ref):
+    if ref.which != "ref":
+        pytest.skip("reference library (oracle/_ref) not built")
+
+
+def test_ppm_bytes_identical_to_reference(ref):
+    from oracle.pyoracle import ref_read_ppm, ref_write_ppm
+
+    _ref_only(ref)
+    rng = np.random.default_rng(3)
+    for shape in [(1, 1, 3), (7, 5, 3), (16, 33, 3)]:
+        a = rng.uniform(-20, 275, size=shape)
+        a.flat[:6] = [255.7, -3.2, 100.5, 99.4, 0.0, 254.5][: a.size]
+        blob = scio.write_ppm(a)
+        assert blob == ref_write_ppm(ref, a)
+        assert (scio.read_ppm(blob) == ref_read_ppm(ref, blob)).all()
+    with pytest.raises(sc.InvalidArgument, match="m x n x 3"):
+        scio.write_ppm(np.zeros((2, 2)))
+
+
+def test_ppm_reader_like_reference(ref):
+    from oracle.pyoracle import OracleError, ref_read_ppm
+
+    _ref_only(ref)
+    good = b"P6 # comment\n# another\n2 1\n255\n" + bytes([0x7F] * 6)
+    assert (scio.read_ppm(good) == ref_read_ppm(ref, good)).all()
+    for blob in (b"P5\n2 2\n255\n....", b"P6\n1 1\n65535\n......", b"P6\n2 2\n255\nxx", b"P6\n0 2\n255\n",
+                 b"P6\n99999999999 1\n255\n", b"P6\n2 1\n255", b"P6\n2x1", b"P"):
+        with pytest.raises(scio.IOError_) as mine:
+            scio.read_ppm(blob)
+        with pytest.raises(OracleError) as theirs:
+            ref_read_ppm(ref, blob)
+        assert str(mine.value) == str(theirs.value), blob
+
+
+def test_curve_csv_like_reference(ref):
+    from oracle.pyoracle import OracleError, ref_read_curve_csv, ref_write_curve_csv
+
+    _ref_only(ref)
+    pts = [(0, 0.0, 1.0), (1, 0.03125, 0.9876543210987654), (17, 1.0 / 3.0, 1e-300), (4096, 2.5e-7, 0.1)]
+    text = scio.write_curve_csv(pts)
+    assert text == ref_write_curve_csv(ref, pts)
+    assert scio.read_curve_csv(text) == ref_read_curve_csv(ref, text) == pts
+    for bad in ("width,rate\n1,2,3\n", "width,compression_rate,relative_error\n1,2\n",
+                "width,compression_rate,relative_error\n-1,0.5,0.5\n", "width,compression_rate,relative_error\nx,1,1\n"):
+        with pytest.raises(scio.IOError_) as mine:
+            scio.read_curve_csv(bad)
+        with pytest.raises(OracleError) as theirs:
+            ref_read_curve_csv(ref, bad)
+        assert str(mine.value) == str(theirs.value)
+
+
+def test_emit_curve_uses_the_storage_model(ref):
+    rep = sc.CutReport(steps=[sc.CutStep(k, 1.0, 0.5 / k, 0.0) for k in (1, 2, 3)], input_norm=2.0)
+    pts = scio.emit_curve(rep, (37, 29), coeff_bits=32, source_bits=16)
+    assert pts[0] == (0, 0.0, 1.0)
+    for k, (w, rate, err) in zip((1, 2, 3), pts[1:]):
+        assert w == k and rate == ref.compression_rate(k, (37, 29), 32, 16) and err == 0.25 / k
