@@ -29,6 +29,7 @@ import argparse
 import json
 import os
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from typing import Callable, Dict, List, Optional, Sequence
 
@@ -109,13 +110,17 @@ def plan(jobs: Sequence[Job], world: int) -> np.ndarray:
 
 
 def run_batch(jobs: Sequence[Job], rank: int, world: int,
-              execute: Callable[[Job], Dict], gather: Optional[Callable[[list], List[list]]] = None) -> Dict:
+              execute: Callable[..., Dict], gather: Optional[Callable[[list], List[list]]] = None,
+              prepare: Optional[Callable[[Job], object]] = None) -> Dict:
     """Run this rank's share and collect every rank's summaries.
 
     ``execute(job)`` returns a dict summary (it must contain ``cuts`` and
     ``device_s``); ``gather(list) -> list of lists`` is the collective used to
     bring summaries together (``torch.distributed.all_gather_object``), None for a
-    single process.  Returns ``{"jobs": [...by index], "device_s": max over ranks,
+    single process.  With ``prepare(job)`` (host-side input synthesis), the next
+    job's input is prepared on a background thread while the device works on the
+    current one (the engine call releases the GIL), and ``execute(job, data)`` is
+    called.  Returns ``{"jobs": [...by index], "device_s": max over ranks,
     "cuts": total}``.
     """
     jobs = list(jobs)
@@ -125,11 +130,20 @@ def run_batch(jobs: Sequence[Job], rank: int, world: int,
     mine.sort(key=lambda j: (-j.cost, j.index))
     out = []
     dev = 0.0
-    for j in mine:
-        s = dict(execute(j))
+    pool = ThreadPoolExecutor(max_workers=1) if prepare is not None and mine else None
+    nxt = pool.submit(prepare, mine[0]) if pool else None
+    for k, j in enumerate(mine):
+        if pool is not None:
+            data = nxt.result()
+            nxt = pool.submit(prepare, mine[k + 1]) if k + 1 < len(mine) else None
+            s = dict(execute(j, data))
+        else:
+            s = dict(execute(j))
         s.update(index=j.index, name=j.name, rank=rank)
         dev += float(s["device_s"])
         out.append(s)
+    if pool is not None:
+        pool.shutdown()
     per_rank = gather([dev, out]) if gather is not None else [[dev, out]]
     allj = sorted((s for _, lst in per_rank for s in lst), key=lambda s: s["index"])
     return {"jobs": allj, "device_s": max(d for d, _ in per_rank), "cuts": sum(s["cuts"] for s in allj),
@@ -157,8 +171,7 @@ def _main() -> int:
     jobs = [Job(j.index, j.name, j.shape, min(j.width, args.prefix_cuts), j.seed)
             for j in mistral_jobs()[: args.jobs]]
 
-    def execute(job: Job) -> Dict:
-        a = mistral_matrix(job)
+    def execute(job: Job, a) -> Dict:
         cfg = DecomposeConfig(width=job.width, search=SearchConfig(seed=job.seed))
         dec, rep, _ = eng.run(a, cfg, dtype=args.dtype)
         return {"cuts": dec.width(), "device_s": rep.kernel_ms / 1e3,
@@ -171,7 +184,7 @@ def _main() -> int:
         return out
 
     t0 = time.perf_counter()
-    res = run_batch(jobs, rank, world, execute, gather if world > 1 else None)
+    res = run_batch(jobs, rank, world, execute, gather if world > 1 else None, prepare=mistral_matrix)
     wall = time.perf_counter() - t0
     if rank == 0:
         print(json.dumps({"metric": "batch signed cuts/sec (Mistral-shaped prefix)", "n_gpus": world,

@@ -92,3 +92,25 @@ def test_batch_driver_world2_gloo():
     per_rank = [sum(j.cost for j in jobs if bins[j.index] == r) * 1e-12 for r in range(2)]
     assert abs(res["device_s"] - max(per_rank)) <= 1e-9 * max(per_rank)
     assert res["cuts"] == sum(j.width for j in jobs)
+
+
+def test_run_batch_prefetches_inputs_in_order():
+    """prepare(job) runs one job ahead on a helper thread; execute(job, data) sees
+    exactly that job's data, in the rank's longest-first order."""
+    from paper_2410_01799_b200.batch import Job, run_batch
+
+    jobs = [Job(i, f"j{i}", (4 + i, 8), 3 + (i % 4), 100 + i) for i in range(9)]
+    seen = []
+
+    def prepare(job):
+        return ("data", job.index)
+
+    def execute(job, data):
+        assert data == ("data", job.index)
+        seen.append(job.index)
+        return {"cuts": job.width, "device_s": 0.001}
+
+    res = run_batch(jobs, 0, 1, execute, prepare=prepare)
+    assert sorted(seen) == list(range(9))
+    assert seen == [j.index for j in sorted(jobs, key=lambda j: (-j.cost, j.index))]
+    assert res["cuts"] == sum(j.width for j in jobs)
