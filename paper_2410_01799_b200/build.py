@@ -20,6 +20,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-cudart",
          "-Xptxas", "-v" if os.environ.get("SCB_PTXAS_VERBOSE") else "-O3"]
 if os.environ.get("SCB_PROFILE"):  # clock64 phase breakdown compiled in (tuning builds only)
     FLAGS += ["-DSCB_PROFILE=1"]
+FLAGS += [f"-D{d}" for d in os.environ.get("SCB_DEFINES", "").split(",") if d]  # A/B builds only
 
 
 def _stale() -> bool:

@@ -329,7 +329,8 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
                       (((w + 1) * 8 + 255) & ~size_t(255)) + 8 * 256 + 4096 +
                       ((nstart * axw64 * 8 + 255) & ~size_t(255)) +
                       ((std::max<uint64_t>(w, 1) * axw64 * 8 + 255) & ~size_t(255)) +
-                      2 * ((static_cast<size_t>(pitch) * 8 + 255) & ~size_t(255));
+                      2 * ((static_cast<size_t>(pitch) * 8 + 255) & ~size_t(255)) +
+                      env_size("SCB_ARENA_SHIFT", 0) + env_size("SCB_SYNC_SHIFT", 0) + env_size("SCB_SLOT_SHIFT", 0);
   if (need > ctx->arena_bytes) {
     if (ctx->arena) cudaFree(ctx->arena);
     ctx->arena = nullptr;
@@ -337,9 +338,13 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
     SC_CUDA(ctx, cudaMalloc(&ctx->arena, need));
     ctx->arena_bytes = need;
   }
-  char* cur = static_cast<char*>(ctx->arena);
+  // SCB_ARENA_SHIFT / SCB_SYNC_SHIFT / SCB_SLOT_SHIFT: placement probes only
+  // (scripts/layout_probe.py; DESIGN.md 5 "Placement of the exchange words")
+  char* cur = static_cast<char*>(ctx->arena) + env_size("SCB_ARENA_SHIFT", 0);
   void* dR = carve<char>(cur, m * rowB);
+  cur += env_size("SCB_SYNC_SHIFT", 0);
   double* zpart = carve<double>(cur, 2 * static_cast<size_t>(G) * pitch);  // [2][G][pitch] by pass parity
+  cur += env_size("SCB_SLOT_SHIFT", 0);
   scb::Slot* slots = carve<scb::Slot>(cur, G);
   unsigned* ctr = carve<unsigned>(cur, 8);  // [0] grid barrier, [1..3] err_pass
   unsigned long long* stats = carve<unsigned long long>(cur, 8);
