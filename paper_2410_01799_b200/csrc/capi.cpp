@@ -489,7 +489,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   // flipped rows walks every column chunk).
   kp.delta = static_cast<int>(env_size("SCB_DELTA", 1));
   kp.delta_div = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_DIV", 32)));
-  kp.delta_refresh = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_REFRESH", 16)));
+  kp.delta_refresh = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_REFRESH", 64)));
   // Dot-pass form: the two-phase pass reads R twice per sweep but has no per-row
   // serial chain -- the better choice while R stays in SMEM / L2; once R spills
   // to HBM the fused single-read pass wins (14336x4096 f32: 77.6 vs 84 us/pass).

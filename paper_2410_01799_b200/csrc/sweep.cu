@@ -1014,7 +1014,7 @@ __device__ __noinline__ void dot_pass_chunked(const DotArgs a) {
 //   s'  = sgn(y)
 //   dz  = 2 sum_{j: s flipped} s'_j R[j,:]    (this CTA's rows; owners add it to z)
 // No rows are streamed.  Dense passes refresh y and z (restart/term start, every
-// 16th sweep, or when many columns flipped), bounding the drift of the caches.
+// 64th sweep, or when many columns flipped), bounding the drift of the caches.
 struct DeltaArgs {
   unsigned res, yrow, s_cur, s_nxt, tws, txor;
   const void* Rrows;  // global row 0 of this CTA's band
@@ -1070,15 +1070,46 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
       }
     }
   }
-  if (!__any_sync(0xffffffffu, over)) {
+  // rows per warp per round trip: up to four, no more than the band needs
+  const int rpg = rows_g > 2 * NW ? 4 : (rows_g > NW ? 2 : 1);
+  const bool any_over = __any_sync(0xffffffffu, over);
+  if (!any_over && rpg < 4) {  // short bands (<= 2 rows per warp): one pair per trip
+    auto row_sum = [&](int j) -> double {
+      const E* row = row_ptr(j);
+      const bool res = j < nres;
+      double v[kMaxF];
+#pragma unroll
+      for (int k = 0; k < kMaxF; ++k)
+        v[k] = k < nf ? static_cast<double>(res ? row[fc[k]] : __ldcg(row + fc[k])) : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < kMaxF; ++k)
+        if (k < nf) acc += ((fneg >> k) & 1u) ? -v[k] : v[k];
+      return acc;
+    };
+    int j = warp;
+    for (; j + NW < rows_g; j += 2 * NW) {
+      double a0 = row_sum(j), a1 = row_sum(j + NW);
+      a0 = warp_sum(a0);
+      a1 = warp_sum(a1);
+      if (lane == 0) {
+        yrow[j] += 2.0 * a0;
+        yrow[j + NW] += 2.0 * a1;
+      }
+    }
+    if (j < rows_g) {
+      const double a0 = warp_sum(row_sum(j));
+      if (lane == 0) yrow[j] += 2.0 * a0;
+    }
+  } else if (!any_over) {
     // up to four rows per warp per L2 round trip (a band of <= 4 NW rows: one trip)
-    for (int j = warp; j < rows_g; j += 4 * NW) {
+    for (int j = warp; j < rows_g; j += rpg * NW) {
       E v[4][kMaxF];  // every load of the four rows issued before the first use (R may
                       // have been rewritten this launch: __ldcg, no __ldg)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int jr = j + r * NW;
-        const bool ok = jr < rows_g;
+        const bool ok = r < rpg && jr < rows_g;
         const E* row = row_ptr(ok ? jr : j);
         const bool res = jr < nres;
 #pragma unroll
@@ -1087,6 +1118,7 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
+        if (r >= rpg) break;  // uniform: short bands reduce only their own rows
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < kMaxF; ++k)
@@ -1098,7 +1130,7 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
   } else {
     // more than kMaxF flips in some lane: the same per-lane ascending sums, kMaxF
     // flips per round trip (each lane walks its t-XOR words with a cursor)
-    for (int j = warp; j < rows_g; j += 4 * NW) {
+    for (int j = warp; j < rows_g; j += rpg * NW) {
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       int cw = lane;
       uint32_t cx = cw < Q ? txor[cw] : 0u;
@@ -1119,7 +1151,7 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int jr = j + r * NW;
-          const bool ok = jr < rows_g;
+          const bool ok = r < rpg && jr < rows_g;
           const E* row = row_ptr(ok ? jr : j);
           const bool res = jr < nres;
 #pragma unroll
@@ -1134,6 +1166,7 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
+        if (r >= rpg) break;
         const double s = warp_sum(acc[r]);
         if (lane == 0 && j + r * NW < rows_g) yrow[j + r * NW] += 2.0 * s;
       }
@@ -1776,7 +1809,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     // A sweep whose t equals the previous pass's t is a fixed point of the cached
     // products: y, s' and z stay exactly as cached whatever pass form runs, so a
     // dense refresh can never nudge c by rounding there (the reference's caches
-    // behave the same way outside its 16-sweep refreshes).
+    // behave the same way outside their refreshes).
     const bool keep = (kind & F_DOT) && !TS && p.delta && pp >= 1 && ctl->nflip == 0;
     if (keep && !(kind & F_DELTA))
       for (int j = tid; j < rows_g; j += CT) ybak[j] = yrow[j];
@@ -2109,8 +2142,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
               ctl->nxt = t;
               ctl->tsel = (pp + 1) & 1;
               need_reduce = 1;
-              // delta pass next unless it is time to refresh the caches (every 16th
-              // sweep, as the reference) or many columns flipped last time
+              // delta pass next unless it is time to refresh the caches (every 64th
+              // sweep; the reference refreshes every 16th) or many columns flipped last time
               if (p.delta && ctl->since_dense + 1 < p.delta_refresh &&
                   static_cast<long long>(ctl->nflip) * p.delta_div <= p.n) {
                 next |= F_DELTA;

@@ -7,8 +7,10 @@ from paper_2410_01799_b200 import _native as N
 import paper_2410_01799_b200 as sc
 
 libs = [os.environ.get("SCB_LIB_A", N.LIB_PATH)] + os.environ["SCB_LIB_B"].split(",")
-a = sc.fill_normal(1, 4096 * 4096, np.float32).reshape(4096, 4096)
-cfg = sc.DecomposeConfig(width=int(os.environ.get("AB_W", 64)), search=sc.SearchConfig(seed=1))
+M, N_ = (int(x) for x in os.environ.get("AB_SHAPE", "4096,4096").split(","))
+SEED = int(os.environ.get("AB_SEED", 1))
+a = sc.fill_normal(SEED, M * N_, np.float32).reshape(M, N_)
+cfg = sc.DecomposeConfig(width=int(os.environ.get("AB_W", 64)), search=sc.SearchConfig(seed=SEED))
 res = {}
 ALL_SIGS = dict(N.SIGNATURES)
 for rnd in range(int(os.environ.get("AB_ROUNDS", 3))):

@@ -383,7 +383,7 @@ def test_fused_pass_default_beyond_l2(engine, ref):
 # ------------------------------------------------------------- delta passes
 def test_delta_passes_keep_the_trajectory(engine, ref, monkeypatch):
     """Sparse delta passes (cached y = Rt, z = R^T s updated from the flipped
-    columns / rows, dense refresh every 16 sweeps) against dense-only passes and
+    columns / rows, dense refresh every 64 sweeps) against dense-only passes and
     the reference on the same input: identical signs and sweeps, c to 1e-12."""
     a = ref.fill_normal(11, 1024 * 1024).reshape(1024, 1024).astype(np.float32)
     out = {}
@@ -411,6 +411,23 @@ def test_delta_policy_extremes(engine, ref, monkeypatch, refresh, div):
     od = ref.greedy_decompose(a, 12, seed=4)
     assert (dec.factors[0] == od.signs[0]).all() and (dec.factors[1] == od.signs[1]).all()
     assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F64_TOL
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_delta_gathers_many_flips_tall_bands(engine, monkeypatch, dtype):
+    """Delta passes with up to n flipped columns (div 1: lanes walk their flips 8 at
+    a time) on bands taller than one 4-row-per-warp group (6000 rows: 41 per CTA),
+    against dense-only passes on the same input: identical signs and sweeps."""
+    a = sc.fill_normal(21, 6000 * 1536, np.float32).reshape(6000, 1536)
+    out = {}
+    for mode, div in (("0", "32"), ("1", "1")):
+        monkeypatch.setenv("SCB_DELTA", mode)
+        monkeypatch.setenv("SCB_DELTA_DIV", div)
+        out[mode] = run(engine, a if dtype == "f32" else a.astype(np.float64), 6, seed=5, dtype=dtype)
+    (d0, r0, _), (d1, r1, _) = out["0"], out["1"]
+    assert all((x == y).all() for x, y in zip(d0.factors, d1.factors))
+    assert np.array_equal(r0.sweeps, r1.sweeps)
+    assert np.max(np.abs(r1._cut_values - r0._cut_values) / np.abs(r0._cut_values)) <= 1e-12
 
 
 # ------------------------------------------------------------ SearchDiagnostics
