@@ -322,7 +322,8 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   // ---- device arena ----
   const size_t need = ((m * rowB + 255) & ~size_t(255)) + ((2 * G * rowB * 8 / es + 255) & ~size_t(255)) +
                       ((G * sizeof(scb::Slot) + 255) & ~size_t(255)) + 4 * 256 +
-                      3 * ((tw32 * 8 + 255) & ~size_t(255)) +
+                      ((2 * static_cast<size_t>(tw32) * 8 * scb::kTbStride + 255) & ~size_t(255)) +
+                      ((tw32 * 8 + 255) & ~size_t(255)) +
                       ((nstart * wn * 8 + 255) & ~size_t(255)) +
                       ((std::max<uint64_t>(w, 1) * (wm + wn) * 8 + 511) & ~size_t(255)) +
                       ((std::max<uint64_t>(w, 1) * 8 + 255) & ~size_t(255)) * 2 +
@@ -330,7 +331,8 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
                       ((nstart * axw64 * 8 + 255) & ~size_t(255)) +
                       ((std::max<uint64_t>(w, 1) * axw64 * 8 + 255) & ~size_t(255)) +
                       2 * ((static_cast<size_t>(pitch) * 8 + 255) & ~size_t(255)) +
-                      env_size("SCB_ARENA_SHIFT", 0) + env_size("SCB_SYNC_SHIFT", 0) + env_size("SCB_SLOT_SHIFT", 0);
+                      env_size("SCB_ARENA_SHIFT", 0) + env_size("SCB_SYNC_SHIFT", 0) + env_size("SCB_SLOT_SHIFT", 0) +
+                      env_size("SCB_TB_SHIFT", 0) + env_size("SCB_ZS_SHIFT", 0);
   if (need > ctx->arena_bytes) {
     if (ctx->arena) cudaFree(ctx->arena);
     ctx->arena = nullptr;
@@ -338,7 +340,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
     SC_CUDA(ctx, cudaMalloc(&ctx->arena, need));
     ctx->arena_bytes = need;
   }
-  // SCB_ARENA_SHIFT / SCB_SYNC_SHIFT / SCB_SLOT_SHIFT: placement probes only
+  // SCB_ARENA/SYNC/SLOT/TB/ZS_SHIFT: placement probes only
   // (scripts/layout_probe.py; DESIGN.md 5 "Placement of the exchange words")
   char* cur = static_cast<char*>(ctx->arena) + env_size("SCB_ARENA_SHIFT", 0);
   void* dR = carve<char>(cur, m * rowB);
@@ -348,7 +350,8 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   scb::Slot* slots = carve<scb::Slot>(cur, G);
   unsigned* ctr = carve<unsigned>(cur, 8);  // [0] grid barrier, [1..3] err_pass
   unsigned long long* stats = carve<unsigned long long>(cur, 8);
-  unsigned long long* tb64 = carve<unsigned long long>(cur, 2 * static_cast<size_t>(tw32));
+  cur += env_size("SCB_TB_SHIFT", 0);
+  unsigned long long* tb64 = carve<unsigned long long>(cur, 2 * static_cast<size_t>(tw32) * scb::kTbStride);
   unsigned* ctr_g = ctr;  // the grid's barrier / error words (rank 0's when sharded)
   if (sh) {  // exchange buffers live in the peer-mapped shard region (reset by sc_shard_reset)
     if (sh->pitch != pitch || sh->dtype != dt || sh->n != n)
@@ -370,6 +373,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   uint64_t* ax0 = carve<uint64_t>(cur, std::max<uint64_t>(nstart * axw64, 1));
   uint64_t* AX_out = carve<uint64_t>(cur, std::max<uint64_t>(std::max<uint64_t>(w, 1) * axw64, 1));
   double* zfull = carve<double>(cur, static_cast<size_t>(pitch));
+  cur += env_size("SCB_ZS_SHIFT", 0);
   double* zstate = carve<double>(cur, static_cast<size_t>(pitch));
 
   // ---- host staging (pinned) for the start vectors ----
@@ -432,7 +436,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
     SC_CUDA(ctx, cudaMemsetAsync(ctr, 0, 4, st));
     SC_CUDA(ctx, cudaMemsetAsync(ctr + 1, 0xff, 12, st));
     SC_CUDA(ctx, cudaMemsetAsync(slots, 0, static_cast<size_t>(G) * sizeof(scb::Slot), st));
-    SC_CUDA(ctx, cudaMemsetAsync(tb64, 0, 2 * static_cast<size_t>(tw32) * 8, st));
+    SC_CUDA(ctx, cudaMemsetAsync(tb64, 0, 2 * static_cast<size_t>(tw32) * 8 * scb::kTbStride, st));
   }
   SC_CUDA(ctx, cudaMemsetAsync(tbest, 0, static_cast<size_t>(tw32) * 4, st));
   SC_CUDA(ctx, cudaMemsetAsync(stats, 0, 64, st));
@@ -697,7 +701,7 @@ sc_status sc_shard_open(sc_ctx* ctx, const sc_shard_config* cfg, void* handle_ou
   S.off_zpart = 0;
   S.off_slots = al(2 * static_cast<size_t>(S.G) * S.pitch * 8);
   S.off_tb64 = S.off_slots + al(static_cast<size_t>(S.G) * sizeof(scb::Slot));
-  S.off_ctr = S.off_tb64 + al(2 * static_cast<size_t>(S.tw32) * 8);
+  S.off_ctr = S.off_tb64 + al(2 * static_cast<size_t>(S.tw32) * 8 * scb::kTbStride);
   S.exch_bytes = S.off_ctr + 256;
   SC_CUDA(ctx, cudaMalloc(&S.exch, S.exch_bytes));
   cudaIpcMemHandle_t h;

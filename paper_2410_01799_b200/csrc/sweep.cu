@@ -1673,7 +1673,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         asm volatile("bar.sync 2, %0;" ::"r"(NP * 32) : "memory");
     };
     double zsv[4];  // warp 0: z state of its word slices, parked in zst before the combine
-    unsigned long long* tout = p.tb64 + static_cast<size_t>(tbuf) * p.Q;
+    unsigned long long* tout = p.tb64 + static_cast<size_t>(tbuf) * p.Q * kTbStride;
     const unsigned long long tag = static_cast<unsigned long long>(P + 1) << 32;
     // owners by global CTA index: the CTAs of all ranks share the column words
     const int GT = p.GT, gg = p.rank * G + g;
@@ -1733,9 +1733,9 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           const unsigned word = __ballot_sync(0xffffffffu, valid && z < 0.0);
           if (p.world > 1) {  // every rank stages t from its own copy
             if (lane < p.world)
-              st_relaxed64_sys(p.tb64_pe[lane] + static_cast<size_t>(tbuf) * p.Q + qq, tag | word);
+              st_relaxed64_sys(p.tb64_pe[lane] + (static_cast<size_t>(tbuf) * p.Q + qq) * kTbStride, tag | word);
           } else if (lane == 0) {
-            st_relaxed64(tout + qq, tag | word);
+            st_relaxed64(tout + static_cast<size_t>(qq) * kTbStride, tag | word);
           }
         }
       }
@@ -1776,11 +1776,11 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         }
       } else if (!TS) {  // order-k: tws was rebuilt by the previous pass's axial step
         // t words were published before the last grid barrier, tagged with this pass
-        const unsigned long long* tw = p.tb64 + static_cast<size_t>(ctl->tsel) * p.Q;
+        const unsigned long long* tw = p.tb64 + static_cast<size_t>(ctl->tsel) * p.Q * kTbStride;
         for (int i = tid; i < p.Q; i += CT) {
           unsigned long long x;
           do {
-            x = p.world > 1 ? ld_relaxed64_sys(tw + i) : ld_relaxed64(tw + i);
+            x = p.world > 1 ? ld_relaxed64_sys(tw + i * kTbStride) : ld_relaxed64(tw + i * kTbStride);
           } while (static_cast<int>(static_cast<unsigned>(x >> 32) - static_cast<unsigned>(P)) < 0);
           tws[i] = static_cast<uint32_t>(x);
         }
@@ -1802,7 +1802,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     if ((kind & F_UPD) && !TS) {  // order-k: uws = kron(best axes), built at term accept
       for (int i = tid; i < p.Q; i += CT)
         uws[i] = ctl->utsel == 2 ? __ldcg(p.tbest + i)
-                                 : static_cast<uint32_t>(__ldcg(p.tb64 + static_cast<size_t>(ctl->utsel) * p.Q + i));
+                                 : static_cast<uint32_t>(__ldcg(p.tb64 + (static_cast<size_t>(ctl->utsel) * p.Q + i) * kTbStride));
     }
     consumer_sync(CT);
     if (prof && tid == 0) pacc[5] += clock64() - t_pass0;
@@ -2068,8 +2068,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
             } else if (ctl->best_tsel == 2) {
               for (int i = 0; i < nw; ++i) trow[i] = __ldcg(p.tbest + i);
             } else {
-              const unsigned long long* src = p.tb64 + static_cast<size_t>(ctl->best_tsel) * p.Q;
-              for (int i = 0; i < nw; ++i) trow[i] = static_cast<uint32_t>(__ldcg(src + i));
+              const unsigned long long* src = p.tb64 + static_cast<size_t>(ctl->best_tsel) * p.Q * kTbStride;
+              for (int i = 0; i < nw; ++i) trow[i] = static_cast<uint32_t>(__ldcg(src + i * kTbStride));
             }
             for (int i = nw; i < p.t_stride; ++i) trow[i] = 0u;
             p.c_out[term] = bc;
@@ -2183,8 +2183,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
               for (int i = 0; i < p.sw; ++i) sbest[i] = s_cur[i];
               if (ctl->restart + 1 < p.restarts) {
                 if (g == 0) {
-                  const unsigned long long* src = p.tb64 + static_cast<size_t>(pp & 1) * p.Q;
-                  for (int i = 0; i < p.Q; ++i) p.tbest[i] = static_cast<uint32_t>(__ldcg(src + i));
+                  const unsigned long long* src = p.tb64 + static_cast<size_t>(pp & 1) * p.Q * kTbStride;
+                  for (int i = 0; i < p.Q; ++i) p.tbest[i] = static_cast<uint32_t>(__ldcg(src + i * kTbStride));
                 }
                 ctl->best_tsel = 2;
               } else {

@@ -31,6 +31,10 @@ struct Slot {
 };
 
 constexpr int kMaxStages = 16;
+// Tagged t words sit one per 128-byte line: all CTAs poll them while the owners
+// publish, and packing 16 per line made the pass time depend on which L2 slices
+// those few lines hash to ("Placement of the exchange words").
+constexpr int kTbStride = 16;
 
 // Per-CTA controller block in shared memory.
 struct Ctl {
@@ -70,7 +74,8 @@ struct KParams {
   int rows_max;        // max rows per CTA
   const uint32_t* t0;  // [width][restarts][t0_stride] start vectors (u32 view)
   int t0_stride;       // u32 words per start vector (= 2 * ceil(n/64))
-  unsigned long long* tb64;  // [2][Q] t words tagged with the consuming pass: (P << 32) | word
+  unsigned long long* tb64;  // [2][Q] t words tagged with the consuming pass: (P << 32) | word,
+                             // one per kTbStride u64s (a 128-byte line each)
   uint32_t* tbest;     // [Q] t of the best restart so far (restarts > 1)
   double* zpart;       // [2][G][pitch] per-CTA column partials, by pass parity
   Slot* slots;         // [G] c / ||R||^2 partials

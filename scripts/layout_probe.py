@@ -39,6 +39,8 @@ if os.environ.get("PROBE_SHIFTS"):  # one engine, the arena carve shifted per ru
         os.environ["SCB_ARENA_SHIFT"] = "0"
         os.environ["SCB_SYNC_SHIFT"] = "0"
         os.environ["SCB_SLOT_SHIFT"] = "0"
+        os.environ["SCB_TB_SHIFT"] = "0"
+        os.environ["SCB_ZS_SHIFT"] = "0"
         for kv in spec.split(","):
             k, v = kv.split("=")
             os.environ[k] = v
