@@ -10,6 +10,9 @@ libs = [os.environ.get("SCB_LIB_A", N.LIB_PATH)] + os.environ["SCB_LIB_B"].split
 M, N_ = (int(x) for x in os.environ.get("AB_SHAPE", "4096,4096").split(","))
 SEED = int(os.environ.get("AB_SEED", 1))
 a = sc.fill_normal(SEED, M * N_, np.float32).reshape(M, N_)
+if os.environ.get("AB_C3"):  # config 3: the order-3 blob image, search seed 2
+    from paper_2410_01799_b200 import workloads as wl
+    a, SEED = wl.c3_blob_image(), 2
 cfg = sc.DecomposeConfig(width=int(os.environ.get("AB_W", 64)), search=sc.SearchConfig(seed=SEED))
 res = {}
 ALL_SIGS = dict(N.SIGNATURES)
