@@ -7,10 +7,18 @@ import numpy as np
 import paper_2410_01799_b200 as sc
 
 shapes = [(4096, 4096, 64, 1), (1024, 1024, 256, 0)]
+if os.environ.get("DS_C3"):  # config 3 (order 3) instead: the blob image, search seed 2
+    shapes = [("c3", None, int(os.environ.get("DS_W", 128)), 2)]
 pol = [(32, 16), (16, 16), (8, 16), (4, 16), (2, 16), (32, 32), (8, 32), (8, 64), (4, 64)]
+if os.environ.get("DS_POL"):
+    pol = [tuple(int(x) for x in q.split(":")) for q in os.environ["DS_POL"].split(",")]
 eng = sc.Engine(0)
 for m, n, w, seed in shapes:
-    a = sc.fill_normal(1 if seed else 0, m * n, np.float32).reshape(m, n)
+    if m == "c3":
+        from paper_2410_01799_b200 import workloads as wl
+        a = wl.c3_blob_image()
+    else:
+        a = sc.fill_normal(1 if seed else 0, m * n, np.float32).reshape(m, n)
     cfg = sc.DecomposeConfig(width=w, search=sc.SearchConfig(seed=seed))
     base = None
     for div, ref in pol:
@@ -23,5 +31,5 @@ for m, n, w, seed in shapes:
         if base is None:
             base = sig
         same = all((x == y).all() for x, y in zip(sig, base))
-        print(f"{m}x{n} w={w} div={div} refresh={ref}: {min(ms):.2f} ms passes {rep.passes} "
+        print(f"{a.shape} w={w} div={div} refresh={ref}: {min(ms):.2f} ms passes {rep.passes} "
               f"same_signs={same} rel={rep.final_residual_norm / rep.input_norm:.9f}", flush=True)
