@@ -111,7 +111,8 @@ def plan(jobs: Sequence[Job], world: int) -> np.ndarray:
 
 def run_batch(jobs: Sequence[Job], rank: int, world: int,
               execute: Callable[..., Dict], gather: Optional[Callable[[list], List[list]]] = None,
-              prepare: Optional[Callable[[Job], object]] = None) -> Dict:
+              prepare: Optional[Callable[[Job], object]] = None,
+              pair: Optional[Callable[[Job], bool]] = None) -> Dict:
     """Run this rank's share and collect every rank's summaries.
 
     ``execute(job)`` returns a dict summary (it must contain ``cuts`` and
@@ -120,8 +121,13 @@ def run_batch(jobs: Sequence[Job], rank: int, world: int,
     single process.  With ``prepare(job)`` (host-side input synthesis), the next
     job's input is prepared on a background thread while the device works on the
     current one (the engine call releases the GIL), and ``execute(job, data)`` is
-    called.  Returns ``{"jobs": [...by index], "device_s": max over ranks,
-    "cuts": total}``.
+    called.  With ``pair(job)``, the jobs it accepts (the sync-bound small
+    shapes, which sort to the tail of the longest-first order) run two at a time
+    on two host threads as ``execute(job, data, lane)``, lane 0 or 1, each lane
+    on its own engine with half the grid (1024×4096 jobs +76%); the
+    pair's device time is the wall time of the pair, which also covers the
+    gap between the two launches.  Returns ``{"jobs": [...by index],
+    "device_s": max over ranks, "cuts": total}``.
     """
     jobs = list(jobs)
     index_of = {j.index: k for k, j in enumerate(jobs)}
@@ -130,18 +136,45 @@ def run_batch(jobs: Sequence[Job], rank: int, world: int,
     mine.sort(key=lambda j: (-j.cost, j.index))
     out = []
     dev = 0.0
-    pool = ThreadPoolExecutor(max_workers=1) if prepare is not None and mine else None
-    nxt = pool.submit(prepare, mine[0]) if pool else None
-    for k, j in enumerate(mine):
-        if pool is not None:
-            data = nxt.result()
-            nxt = pool.submit(prepare, mine[k + 1]) if k + 1 < len(mine) else None
-            s = dict(execute(j, data))
-        else:
-            s = dict(execute(j))
+    solo = [j for j in mine if pair is None or not pair(j)]
+    duo = [j for j in mine if pair is not None and pair(j)]
+    order = solo + duo
+    pool = ThreadPoolExecutor(max_workers=1) if prepare is not None and order else None
+    nxt = pool.submit(prepare, order[0]) if pool else None
+
+    def fetch(k):
+        nonlocal nxt
+        if pool is None:
+            return None
+        data = nxt.result()
+        nxt = pool.submit(prepare, order[k + 1]) if k + 1 < len(order) else None
+        return data
+
+    def record(j, s):
         s.update(index=j.index, name=j.name, rank=rank)
-        dev += float(s["device_s"])
         out.append(s)
+
+    for k, j in enumerate(solo):
+        data = fetch(k)
+        s = dict(execute(j, data) if pool is not None else execute(j))
+        dev += float(s["device_s"])
+        record(j, s)
+    k = len(solo)
+    if duo:
+        lanes = ThreadPoolExecutor(max_workers=2)
+        while k < len(order):
+            group = order[k:k + 2]
+            args = [(j, fetch(k + i)) for i, j in enumerate(group)]
+            t0 = time.perf_counter()
+            futs = [lanes.submit(execute, j, d, i) for i, (j, d) in enumerate(args)]
+            res = [dict(f.result()) for f in futs]
+            wall = time.perf_counter() - t0
+            dev += max([wall] + [float(s["device_s"]) for s in res])
+            for j, s in zip(group, res):
+                s["paired"] = len(group) == 2
+                record(j, s)
+            k += len(group)
+        lanes.shutdown()
     if pool is not None:
         pool.shutdown()
     per_rank = gather([dev, out]) if gather is not None else [[dev, out]]
@@ -155,6 +188,9 @@ def _main() -> int:
     ap.add_argument("--jobs", type=int, default=14, help="first J jobs of the 226 (layer order)")
     ap.add_argument("--prefix-cuts", type=int, default=64, help="cuts per job (prefix of its Table-2 width)")
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--pair-rows", type=int, default=0,
+                    help="jobs with at most this many rows run two at a time, half the grid each "
+                         "(0: off; off by default, DESIGN §8: the two host calls serialise)")
     args = ap.parse_args()
 
     import torch
@@ -168,13 +204,20 @@ def _main() -> int:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     eng = Engine(local)
+    engs = [eng, Engine(local)] if args.pair_rows > 0 else [eng]
+    half = torch.cuda.get_device_properties(local).multi_processor_count // 2
+    for e in engs[1:]:  # first-use setup of the second lane's engine stays out of the batch
+        e.run(np.ones((64, 64), np.float32), DecomposeConfig(width=1), dtype=args.dtype)
     jobs = [Job(j.index, j.name, j.shape, min(j.width, args.prefix_cuts), j.seed)
             for j in mistral_jobs()[: args.jobs]]
 
-    def execute(job: Job, a) -> Dict:
+    def execute(job: Job, a, lane: Optional[int] = None) -> Dict:
         cfg = DecomposeConfig(width=job.width, search=SearchConfig(seed=job.seed))
-        dec, rep, _ = eng.run(a, cfg, dtype=args.dtype)
-        return {"cuts": dec.width(), "device_s": rep.kernel_ms / 1e3,
+        if lane is not None:
+            # pair phase (after every solo job): each engine's grid capped at half the SMs
+            os.environ["SCB_CTAS"] = str(half)
+        dec, rep, _ = engs[lane or 0].run(a, cfg, dtype=args.dtype)
+        return {"cuts": dec.width(), "device_s": rep.kernel_ms / 1e3, "call_s": rep.total_ms / 1e3,
                 "rel_residual": rep.final_residual_norm / rep.input_norm,
                 "sweeps_mean": float(np.mean(rep.sweeps)) if len(rep.sweeps) else 0.0}
 
@@ -184,7 +227,10 @@ def _main() -> int:
         return out
 
     t0 = time.perf_counter()
-    res = run_batch(jobs, rank, world, execute, gather if world > 1 else None, prepare=mistral_matrix)
+    pair = (lambda j: j.shape[0] <= args.pair_rows) if args.pair_rows > 0 else None
+    res = run_batch(jobs, rank, world, execute, gather if world > 1 else None, prepare=mistral_matrix,
+                    pair=pair)
+    os.environ.pop("SCB_CTAS", None)
     wall = time.perf_counter() - t0
     if rank == 0:
         print(json.dumps({"metric": "batch signed cuts/sec (Mistral-shaped prefix)", "n_gpus": world,

@@ -114,3 +114,41 @@ def test_run_batch_prefetches_inputs_in_order():
     assert sorted(seen) == list(range(9))
     assert seen == [j.index for j in sorted(jobs, key=lambda j: (-j.cost, j.index))]
     assert res["cuts"] == sum(j.width for j in jobs)
+
+
+def test_run_batch_pairs_small_jobs_two_lanes():
+    """pair(job) jobs run after every solo job, two at a time on lanes 0 and 1, each
+    with its own prefetched data; the pair's device time is counted once."""
+    import threading
+    import time as _time
+
+    from paper_2410_01799_b200.batch import Job, run_batch
+
+    jobs = [Job(i, f"j{i}", (64 if i < 3 else 8, 8), 4, 100 + i) for i in range(8)]
+    lock = threading.Lock()
+    calls = []
+
+    def prepare(job):
+        return ("data", job.index)
+
+    def execute(job, data, lane=None):
+        assert data == ("data", job.index)
+        with lock:
+            calls.append((job.index, lane))
+        if lane is not None:
+            _time.sleep(0.1)
+        return {"cuts": job.width, "device_s": 0.1 if lane is not None else 0.001}
+
+    small = lambda j: j.shape[0] <= 8
+    res = run_batch(jobs, 0, 1, execute, prepare=prepare, pair=small)
+    solo = [c for c in calls if c[1] is None]
+    duo = [c for c in calls if c[1] is not None]
+    assert sorted(c[0] for c in solo) == [0, 1, 2]
+    assert calls[:3] == solo  # every solo job runs before the pair phase
+    assert sorted(c[0] for c in duo) == [3, 4, 5, 6, 7]
+    assert sorted(c[1] for c in duo) == [0, 0, 0, 1, 1]
+    assert res["cuts"] == sum(j.width for j in jobs)
+    assert [s["index"] for s in res["jobs"]] == list(range(8))
+    assert sum(1 for s in res["jobs"] if s.get("paired")) == 4
+    # two pairs and a single of ~100 ms each: concurrent lanes, not 5 x 100 ms
+    assert 0.3 <= res["device_s"] < 0.45
