@@ -2,18 +2,23 @@
 
 nvcc compiles the CUDA kernels and the C++ host driver into one shared
 library next to this file so it travels with the repo snapshot to the GPU box.
+Every translation unit is compiled to an object in parallel (the kernel
+families live in separate sweep_k_*.cu units), then linked once.
 """
 from __future__ import annotations
 
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsigcut_b200.so")
-SOURCES = ["sweep.cu", "ops.cu", "capi.cpp", "ops.cpp"]
-HEADERS = ["sweep.h", "rng.h", "ops.h", "ctx.h"]
+SOURCES = ["sweep.cu", "sweep_k_f32m.cu", "sweep_k_f32t.cu", "sweep_k_f64m.cu", "sweep_k_f64t.cu",
+           "ops.cu", "capi.cpp", "ops.cpp"]
+HEADERS = ["sweep.h", "sweep_impl.cuh", "rng.h", "ops.h", "ctx.h"]
+OBJDIR = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-cudart", "static",
@@ -36,16 +41,27 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    srcs = [os.path.join(CSRC, f) for f in SOURCES]
+    os.makedirs(OBJDIR, exist_ok=True)
+
+    def compile_one(f):
+        obj = os.path.join(OBJDIR, f + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", "-o", obj, os.path.join(CSRC, f)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {f} ({r.returncode}):\n{r.stdout}\n{r.stderr}")
+        if verbose and r.stderr:
+            print(r.stderr, file=sys.stderr)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", tmp, *srcs]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
-    if verbose and r.stderr:
-        print(r.stderr, file=sys.stderr)
+        raise RuntimeError(f"nvcc link failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
     return LIB
 
