@@ -125,6 +125,12 @@ typedef struct sc_result {
    * max_sweeps values.  n_sweep_values receives their count (= sweeps[0]). */
   double* sweep_values;
   uint64_t n_sweep_values;
+  /* filled by the call: dot passes by form, and the bytes the kernel moved through
+   * L2 / HBM (streamed rows of R, delta-pass gathers at sector granularity, rank-1
+   * update write-backs, column-partial exchange; shared-memory-resident rows excluded) */
+  uint64_t dense_passes;
+  uint64_t delta_passes;
+  uint64_t device_bytes;
 } sc_result;
 
 const char* sc_version(void);
@@ -248,11 +254,15 @@ sc_status sc_read_dten(const uint8_t* in, uint64_t size, double* data, char* msg
 /* Row-sharded decomposition of ONE matrix over `world` GPUs (one process and
  * one context per GPU).  Rank r owns the contiguous row band
  * [row0, row0 + local rows) of the m_global x n matrix.  The persistent kernel
- * of every rank joins one grid: per pass the z partials and the c / ||R||^2
- * partials of all ranks' CTAs are reduced in the same fixed order through
- * peer-mapped buffers (CUDA IPC over NVLink), owner CTAs publish the next t to
- * every rank, and one system-scope barrier separates the passes -- the
- * allreduce of R^T s and of the objective is fused into the kernel.
+ * of every rank joins one grid.  Per pass each rank reduces its CTAs' column
+ * partials of R^T s into one rank partial (n f64) and its c / ||R||^2 partials
+ * into one rank slot behind a rank-local barrier; after one system-scope
+ * barrier the owner CTA of every 32-column word adds the world rank partials in
+ * rank order through peer-mapped buffers (CUDA IPC over NVLink) and publishes
+ * the next t to every rank, and every CTA adds the world rank slots -- the
+ * allreduce of R^T s and of the objective is fused into the kernel.  Every
+ * cross-rank spin is bounded: after timeout_ms (or when any rank has set the
+ * shared abort word) the kernel stops and the call returns SC_RUNTIME_ERROR.
  * Protocol (all ranks):
  *   1. sc_shard_open(ctx, cfg, handle)   allocate + export this rank's buffers
  *   2. all-gather the world handles      (e.g. torch.distributed)
@@ -269,6 +279,7 @@ typedef struct sc_shard_config {
   uint64_t n;        /* columns */
   int32_t dtype;     /* sc_dtype */
   int32_t ctas;      /* CTAs per rank, identical on all ranks; 0 = min(SMs, m_global / world) */
+  uint32_t timeout_ms; /* bound of every cross-rank spin in the kernel; 0 = 30000 */
 } sc_shard_config;
 
 sc_status sc_shard_open(sc_ctx* ctx, const sc_shard_config* cfg, void* handle_out);
@@ -277,6 +288,22 @@ sc_status sc_shard_reset(sc_ctx* ctx);
 sc_status sc_greedy_decompose_sharded(sc_ctx* ctx, const sc_problem* local, const sc_shard_config* cfg,
                                       sc_result* result);
 void sc_shard_close(sc_ctx* ctx);
+/* The same row-sharded protocol with `world` VIRTUAL ranks on this context's one
+ * device, for machines with fewer GPUs than ranks: the ranks' kernels wait on
+ * one another, so they run as ONE cooperative launch (CTA block r plays rank r
+ * with rank r's band, parameters and exchange region; peer pointers are the
+ * other ranks' regions on the same device).  `problem` is the WHOLE matrix; the
+ * result is the gathered one (global row signs, t, c, curve), after checking
+ * that every rank took the same decisions.  opts == NULL: world 1. */
+typedef struct sc_shard_emulation {
+  int32_t world;       /* virtual ranks, 1..8 */
+  int32_t ctas;        /* CTAs per rank; 0 = SMs / world */
+  uint32_t timeout_ms; /* as sc_shard_config::timeout_ms */
+  int32_t dead_rank;   /* test hook: this rank's CTAs exit at once (a rank that never
+                          joins; the others time out -> SC_RUNTIME_ERROR); -1 = none */
+} sc_shard_emulation;
+sc_status sc_greedy_decompose_sharded_emulated(sc_ctx* ctx, const sc_problem* problem,
+                                               const sc_shard_emulation* opts, sc_result* result);
 
 #ifdef __cplusplus
 }

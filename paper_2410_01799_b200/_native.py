@@ -59,6 +59,9 @@ class ScResult(C.Structure):
         ("kernel_launches", C.c_int32),
         ("sweep_values", P(C.c_double)),
         ("n_sweep_values", u64),
+        ("dense_passes", u64),
+        ("delta_passes", u64),
+        ("device_bytes", u64),
     ]
 
 
@@ -71,6 +74,16 @@ class ScShardConfig(C.Structure):
         ("n", u64),
         ("dtype", C.c_int32),
         ("ctas", C.c_int32),
+        ("timeout_ms", C.c_uint32),
+    ]
+
+
+class ScShardEmulation(C.Structure):
+    _fields_ = [
+        ("world", C.c_int32),
+        ("ctas", C.c_int32),
+        ("timeout_ms", C.c_uint32),
+        ("dead_rank", C.c_int32),
     ]
 
 
@@ -117,6 +130,7 @@ SIGNATURES = {
     "sc_shard_reset": (C.c_int, [C.c_void_p]),
     "sc_greedy_decompose_sharded": (C.c_int, [C.c_void_p, P(ScProblem), P(ScShardConfig), P(ScResult)]),
     "sc_shard_close": (None, [C.c_void_p]),
+    "sc_greedy_decompose_sharded_emulated": (C.c_int, [C.c_void_p, P(ScProblem), P(ScShardEmulation), P(ScResult)]),
     "sc_accumulate_expansion": (C.c_int, [C.c_void_p, P(ScFactors), C.c_double, u64, u64, C.c_void_p, C.c_int32,
                                           C.c_int32, P(ScOpStats)]),
     "sc_gram_matrix": (C.c_int, [C.c_void_p, P(ScFactors), P(C.c_double), P(ScOpStats)]),

@@ -125,6 +125,9 @@ class CutReport:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     kernel_launches: int = 0
+    dense_passes: int = 0
+    delta_passes: int = 0
+    device_bytes: int = 0  # bytes the kernel moved through L2 / HBM (sc_result::device_bytes)
 
 
 @dataclass
@@ -211,7 +214,8 @@ class Engine:
 
     # -- core call -----------------------------------------------------------
     def run(self, a, cfg: DecomposeConfig, *, dtype: Optional[str] = None, seed_mode: int = N.SC_SEED_PER_TERM,
-            want_remainder: bool = False, shard=None, diag: Optional[SearchDiagnostics] = None):
+            want_remainder: bool = False, shard=None, diag: Optional[SearchDiagnostics] = None,
+            emulate=None):
         """Runs the device decomposition; returns (CutDecomposition, CutReport, remainder|None).
 
         ``a`` is a numpy array (host path) or a CUDA torch tensor (device path,
@@ -278,14 +282,19 @@ class Engine:
         sv = np.zeros(max(int(cfg.search.max_sweeps), 1)) if diag is not None else None
         if sv is not None:
             res.sweep_values = sv.ctypes.data_as(C.POINTER(C.c_double))
-        if shard is None:
+        if emulate is not None:  # row sharding over virtual ranks on this device (sharded.emulated)
+            self._check(self.lib.sc_greedy_decompose_sharded_emulated(self.handle, C.byref(prob), C.byref(emulate),
+                                                                      C.byref(res)))
+        elif shard is None:
             self._check(self.lib.sc_greedy_decompose(self.handle, C.byref(prob), C.byref(res)))
         else:  # this rank's band of a row-sharded matrix (sharded.py)
             self._check(self.lib.sc_greedy_decompose_sharded(self.handle, C.byref(prob), C.byref(shard), C.byref(res)))
         del keep
         wd = int(res.width_done)
-        numel = float(np.prod([float(d) for d in shape])) if shard is None else float(shard.m_global) * shape[1]
-        bits_per_term = 64 + sum(int(d) for d in shape)
+        # the global shape: a row-sharded rank holds only its band of the m_global rows
+        gshape = tuple(int(d) for d in shape) if shard is None else (int(shard.m_global), int(shape[1]))
+        numel = float(np.prod([float(d) for d in gshape]))
+        bits_per_term = 64 + sum(gshape)
         steps = []
         if cfg.record_curve:
             steps = [CutStep(k + 1, float(cut[k]), float(rn[k]), (k + 1) * bits_per_term / (64.0 * numel))
@@ -295,7 +304,8 @@ class Engine:
                         residual_norm_exact=rne[:wd].copy(), sweeps=sweeps[:wd].copy(), passes=int(res.passes),
                         kernel_ms=float(res.kernel_ms), total_ms=float(res.total_ms),
                         h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes),
-                        kernel_launches=int(res.kernel_launches))
+                        kernel_launches=int(res.kernel_launches), dense_passes=int(res.dense_passes),
+                        delta_passes=int(res.delta_passes), device_bytes=int(res.device_bytes))
         rep._cut_values = cut[:wd].copy()
         if diag is not None:
             diag.sweep_values = sv[: int(res.n_sweep_values)].tolist()
@@ -451,7 +461,8 @@ class Engine:
                         residual_norm_exact=rne[:wd].copy(), sweeps=sweeps[:wd].copy(), passes=int(res.passes),
                         kernel_ms=float(res.kernel_ms), total_ms=float(res.total_ms),
                         h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes),
-                        kernel_launches=int(res.kernel_launches))
+                        kernel_launches=int(res.kernel_launches), dense_passes=int(res.dense_passes),
+                        delta_passes=int(res.delta_passes), device_bytes=int(res.device_bytes))
         rep._cut_values = cut[:wd].copy()
         return dec, rep
 

@@ -15,7 +15,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsigcut_b200.so")
-SOURCES = ["sweep.cu", "sweep_k_f32m.cu", "sweep_k_f32t.cu", "sweep_k_f64m.cu", "sweep_k_f64t.cu",
+SOURCES = ["sweep.cu", "sweep_k_f32m.cu", "sweep_k_f32t.cu", "sweep_k_f64m.cu", "sweep_k_f64t.cu", "sweep_k_vr.cu",
            "ops.cu", "capi.cpp", "ops.cpp"]
 HEADERS = ["sweep.h", "sweep_impl.cuh", "rng.h", "ops.h", "ctx.h"]
 OBJDIR = os.path.join(HERE, "build")

@@ -143,9 +143,11 @@ void sc_destroy(sc_ctx* ctx) {
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   scb::pool_release(ctx);
-  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
-  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (!ctx->borrowed) {
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  }
   delete ctx;
 }
 
@@ -208,6 +210,31 @@ void sc_lpt_schedule(const double* costs, uint64_t count, uint32_t bins, uint32_
 }
 
 namespace {
+// Everything finish_run needs after the launch (prepare_run fills it).
+struct RunState {
+  std::chrono::steady_clock::time_point t_start;
+  scb::Variant var{};
+  scb::KParams kp{};
+  size_t smem = 0;
+  bool tensor = false, prof = false;
+  int kax = 0, G = 0, res_rows = 0, stages = 0;
+  int ax_off[7] = {0, 0, 0, 0, 0, 0, 0};
+  uint64_t axw64 = 0, m = 0, n = 0, w = 0, wm = 0, wn = 0, h2d = 0, d2h = 0;
+  size_t es = 0, rowB = 0;
+  double numel = 0.0;  // global element count (row-sharded: m_global * n)
+  void* dR = nullptr;
+  unsigned* ctr_g = nullptr;
+  unsigned long long* stats = nullptr;
+  double* norm2 = nullptr;
+  uint64_t *S_out = nullptr, *T_out = nullptr, *AX_out = nullptr;
+  double* c_out = nullptr;
+  uint32_t* sweeps_out = nullptr;
+  double* dsweeps = nullptr;
+  unsigned long long* dprof = nullptr;
+};
+sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc_ctx::Shard* sh, RunState& S,
+                      bool vr);
+sc_status finish_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, RunState& S);
 sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc_ctx::Shard* sh);
 
 // CTAs for m rows (the engine and the sharded path agree, so world-1 sharding is
@@ -228,6 +255,17 @@ sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res) 
 
 namespace {
 sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc_ctx::Shard* sh) {
+  RunState S;
+  if (sc_status st = prepare_run(ctx, p, res, sh, S, false); st != SC_OK) return st;
+  SC_CUDA(ctx, scb::set_smem_limit(S.var, S.smem));
+  SC_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  SC_CUDA(ctx, scb::launch_sweep(S.var, S.kp, S.smem, ctx->stream));
+  SC_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+  return finish_run(ctx, p, res, S);
+}
+
+sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc_ctx::Shard* sh, RunState& S,
+                      bool vr) {
   const auto t_start = std::chrono::steady_clock::now();
   if (ctx == nullptr) return SC_INVALID_ARGUMENT;
   if (res == nullptr) return set_err(ctx, SC_INVALID_ARGUMENT, "sc_result: null");
@@ -269,6 +307,8 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
     return set_err(ctx, SC_NOT_SUPPORTED, "row length %llu exceeds the fused-kernel envelope",
                    static_cast<unsigned long long>(n));
   var.tensor = tensor ? 1 : 0;  // order-k kernels are separate instantiations
+  if (vr && !scb::has_vr(var))
+    return set_err(ctx, SC_NOT_SUPPORTED, "emulated row sharding: no virtual-rank kernel for rows of %llu", static_cast<unsigned long long>(n));
 
   // wide rows: column chunks of one warp-tile pass (var.nw * 32 * var.vpt vectors)
   const long long tile_cols = static_cast<long long>(var.nw) * 32 * var.vpt * (dt == SC_F32 ? 4 : 2);
@@ -356,6 +396,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   if (sh) {  // exchange buffers live in the peer-mapped shard region (reset by sc_shard_reset)
     if (sh->pitch != pitch || sh->dtype != dt || sh->n != n)
       return set_err(ctx, SC_INVALID_ARGUMENT, "sc_greedy_decompose_sharded: problem does not match the shard");
+    if (sh->G != G) return set_err(ctx, SC_INVALID_ARGUMENT, "sc_greedy_decompose_sharded: CTA count mismatch");
     char* ex = static_cast<char*>(sh->exch);
     zpart = reinterpret_cast<double*>(ex + sh->off_zpart);
     slots = reinterpret_cast<scb::Slot*>(ex + sh->off_slots);
@@ -440,6 +481,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   }
   SC_CUDA(ctx, cudaMemsetAsync(tbest, 0, static_cast<size_t>(tw32) * 4, st));
   SC_CUDA(ctx, cudaMemsetAsync(stats, 0, 64, st));
+  if (!sh) SC_CUDA(ctx, cudaMemsetAsync(ctr + 4, 0xff, 4, st));
   if (w > 0) SC_CUDA(ctx, cudaMemsetAsync(S_out, 0, w * wm * 8, st));
 
   scb::KParams kp{};
@@ -508,10 +550,14 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   kp.GT = G * kp.world;
   for (int r = 0; r < kp.world; ++r) {
     char* ex = sh ? static_cast<char*>(sh->peers[r]) : nullptr;
-    kp.zpart_pe[r] = sh ? reinterpret_cast<double*>(ex + sh->off_zpart) : zpart;
-    kp.slots_pe[r] = sh ? reinterpret_cast<scb::Slot*>(ex + sh->off_slots) : slots;
+    kp.zr_pe[r] = sh ? reinterpret_cast<double*>(ex + sh->off_zr) : nullptr;
+    kp.rslot_pe[r] = sh ? reinterpret_cast<scb::Slot*>(ex + sh->off_rslot) : nullptr;
     kp.tb64_pe[r] = sh ? reinterpret_cast<unsigned long long*>(ex + sh->off_tb64) : tb64;
   }
+  kp.bar_local = ctr + 5;  // this rank's own counter
+  kp.abort_word = ctr_g + 6;
+  kp.timeout_ns = static_cast<long long>(sh && sh->timeout_ms ? sh->timeout_ms : 30000u) * 1000000ll;
+  kp.fault = sh ? sh->fault : 0;
   kp.chunk_cols = cpr > 1 ? static_cast<int>(tile_cols) : static_cast<int>(pitch);
 
   const bool prof = std::getenv("SCB_PROF") != nullptr;
@@ -532,20 +578,73 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
     SC_CUDA(ctx, cudaMemsetAsync(dsweeps, 0, nb, st));
   }
   kp.sweep_vals = dsweeps;
-  SC_CUDA(ctx, scb::set_smem_limit(var, smem));
-  SC_CUDA(ctx, cudaEventRecord(ctx->ev0, st));
-  SC_CUDA(ctx, scb::launch_sweep(var, kp, smem, st));
-  SC_CUDA(ctx, cudaEventRecord(ctx->ev1, st));
+  S.t_start = t_start;
+  S.var = var;
+  S.kp = kp;
+  S.smem = smem;
+  S.tensor = tensor;
+  S.prof = prof;
+  S.kax = kax;
+  S.G = G;
+  S.res_rows = res_rows;
+  S.stages = stages;
+  std::copy(ax_off, ax_off + 7, S.ax_off);
+  S.axw64 = axw64;
+  S.m = m;
+  S.n = n;
+  S.w = w;
+  S.wm = wm;
+  S.wn = wn;
+  S.h2d = h2d;
+  S.d2h = d2h;
+  S.es = es;
+  S.rowB = rowB;
+  S.numel = kp.numel_d;
+  S.dR = dR;
+  S.ctr_g = ctr_g;
+  S.stats = stats;
+  S.norm2 = norm2;
+  S.S_out = S_out;
+  S.T_out = T_out;
+  S.AX_out = AX_out;
+  S.c_out = c_out;
+  S.sweeps_out = sweeps_out;
+  S.dsweeps = dsweeps;
+  S.dprof = dprof;
+  return SC_OK;
+}
+
+sc_status finish_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, RunState& S) {
+  const auto t_start = S.t_start;
+  const scb::Variant& var = S.var;
+  const bool tensor = S.tensor, prof = S.prof;
+  const int kax = S.kax, G = S.G, res_rows = S.res_rows, stages = S.stages;
+  const int* ax_off = S.ax_off;
+  const uint64_t axw64 = S.axw64, m = S.m, n = S.n, w = S.w, wm = S.wm, wn = S.wn;
+  uint64_t h2d = S.h2d, d2h = S.d2h;
+  const size_t es = S.es, rowB = S.rowB, smem = S.smem;
+  void* dR = S.dR;
+  unsigned* ctr_g = S.ctr_g;
+  unsigned long long* stats = S.stats;
+  double* norm2 = S.norm2;
+  uint64_t *S_out = S.S_out, *T_out = S.T_out, *AX_out = S.AX_out;
+  double* c_out = S.c_out;
+  uint32_t* sweeps_out = S.sweeps_out;
+  double* dsweeps = S.dsweeps;
+  unsigned long long* dprof = S.dprof;
+  cudaStream_t st = ctx->stream;
+  const long long pitch = S.kp.pitch;
+  (void)pitch;
 
   // ---- results ----
-  unsigned h_ctr[4];
+  unsigned h_ctr[8];
   unsigned long long h_stats[8];
   std::vector<double> h_norm2(w + 1);
-  SC_CUDA(ctx, cudaMemcpyAsync(h_ctr, ctr_g, 16, cudaMemcpyDeviceToHost, st));
+  SC_CUDA(ctx, cudaMemcpyAsync(h_ctr, ctr_g, 32, cudaMemcpyDeviceToHost, st));
   SC_CUDA(ctx, cudaMemcpyAsync(h_stats, stats, 64, cudaMemcpyDeviceToHost, st));
   SC_CUDA(ctx, cudaMemcpyAsync(h_norm2.data(), norm2, (w + 1) * 8, cudaMemcpyDeviceToHost, st));
   SC_CUDA(ctx, cudaStreamSynchronize(st));
-  d2h += 16 + 32 + (w + 1) * 8;
+  d2h += 32 + 64 + (w + 1) * 8;
   float kms = 0.f;
   cudaEventElapsedTime(&kms, ctx->ev0, ctx->ev1);
   res->kernel_ms = kms;
@@ -611,6 +710,10 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
                  acc[1] / std::max<double>(1.0, static_cast<double>(h_stats[1])),
                  static_cast<unsigned long long>(h_stats[1]));
   }
+  if (S.kp.world > 1 && h_ctr[4] != 0xffffffffu)
+    return set_err(ctx, SC_RUNTIME_ERROR,
+                   "row-sharded exchange: a rank did not arrive within %lld ms (pass %u); run aborted",
+                   S.kp.timeout_ns / 1000000, h_ctr[4]);
   if (h_ctr[3] != 0xffffffffu) return set_err(ctx, SC_INVALID_ARGUMENT, "DenseTensor: non-finite value");
   if (h_ctr[1] != 0xffffffffu || h_ctr[2] != 0xffffffffu)
     return set_err(ctx, SC_INVALID_ARGUMENT, "sgn_vector: non-finite entry");
@@ -618,6 +721,9 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   const uint64_t wd = h_stats[0];
   res->width_done = wd;
   res->passes = h_stats[1];
+  res->dense_passes = h_stats[2];
+  res->delta_passes = h_stats[3];
+  res->device_bytes = h_stats[5];
   if (wd > 0) {
     SC_CUDA(ctx, cudaMemcpyAsync(res->sign_words[0], S_out, wd * wm * 8, cudaMemcpyDeviceToHost, st));
     if (!tensor) {
@@ -654,7 +760,7 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   SC_CUDA(ctx, cudaStreamSynchronize(st));
 
   // ---- CutReport reconstruction (decompose.hpp:317-359) ----
-  const double N = static_cast<double>(m * n);
+  const double N = S.numel;  // m_global * n when row-sharded (the kernel's alpha divisor)
   res->input_norm = std::sqrt(h_norm2[0]);
   double resid_sq = h_norm2[0];
   for (uint64_t k = 0; k < wd; ++k) {
@@ -678,6 +784,33 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
 
 // ---------------------------------------------------------------------------
 // Row-sharded decomposition of one matrix over `world` GPUs.
+namespace {
+// This rank's exchange region: [zpart (local column partials) | zr (rank partial,
+// read by peers) | slots | rank slot (read by peers) | tagged t words (written by
+// peers) | counters].  Counters: [0] cross-rank barrier (rank 0's is used),
+// [1..3] first failing pass per error class, [4] first pass of a cross-rank
+// timeout, [5] this rank's local barrier, [6] abort word (rank 0's is used).
+sc_status shard_alloc(sc_ctx* ctx, const sc_shard_config* cfg) {
+  auto& S = ctx->shard;
+  S.pitch = static_cast<long long>((cfg->n + 31) / 32 * 32);
+  const uint64_t min_band = cfg->m_global / cfg->world;  // bands are floor/ceil of m/world
+  S.G = cfg->ctas > 0 ? cfg->ctas : static_cast<int>(auto_ctas(ctx->num_sms, 1, min_band));
+  const int Q = static_cast<int>(S.pitch / 32);
+  S.tw32 = std::max(Q, static_cast<int>(2 * words64(cfg->n)));
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  S.off_zpart = 0;
+  S.off_zr = al(2 * static_cast<size_t>(S.G) * S.pitch * 8);
+  S.off_slots = S.off_zr + al(2 * static_cast<size_t>(S.pitch) * 8);
+  S.off_rslot = S.off_slots + al(static_cast<size_t>(S.G) * sizeof(scb::Slot));
+  S.off_tb64 = S.off_rslot + al(sizeof(scb::Slot));
+  S.off_ctr = S.off_tb64 + al(2 * static_cast<size_t>(S.tw32) * 8 * scb::kTbStride);
+  S.exch_bytes = S.off_ctr + 256;
+  SC_CUDA(ctx, cudaMalloc(&S.exch, S.exch_bytes));
+  S.peers[S.rank] = S.exch;
+  return SC_OK;
+}
+}  // namespace
+
 sc_status sc_shard_open(sc_ctx* ctx, const sc_shard_config* cfg, void* handle_out) {
   if (!ctx || !cfg || !handle_out) return SC_INVALID_ARGUMENT;
   if (cfg->world < 1 || cfg->world > 8 || cfg->rank < 0 || cfg->rank >= cfg->world || cfg->n == 0 ||
@@ -692,22 +825,11 @@ sc_status sc_shard_open(sc_ctx* ctx, const sc_shard_config* cfg, void* handle_ou
   S.m_global = cfg->m_global;
   S.row0 = cfg->row0;
   S.n = cfg->n;
-  S.pitch = static_cast<long long>((cfg->n + 31) / 32 * 32);
-  const uint64_t min_band = cfg->m_global / cfg->world;  // bands are floor/ceil of m/world
-  S.G = cfg->ctas > 0 ? cfg->ctas : static_cast<int>(auto_ctas(ctx->num_sms, 1, min_band));
-  const int Q = static_cast<int>(S.pitch / 32);
-  S.tw32 = std::max(Q, static_cast<int>(2 * words64(cfg->n)));
-  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  S.off_zpart = 0;
-  S.off_slots = al(2 * static_cast<size_t>(S.G) * S.pitch * 8);
-  S.off_tb64 = S.off_slots + al(static_cast<size_t>(S.G) * sizeof(scb::Slot));
-  S.off_ctr = S.off_tb64 + al(2 * static_cast<size_t>(S.tw32) * 8 * scb::kTbStride);
-  S.exch_bytes = S.off_ctr + 256;
-  SC_CUDA(ctx, cudaMalloc(&S.exch, S.exch_bytes));
+  S.timeout_ms = cfg->timeout_ms;
+  if (sc_status st = shard_alloc(ctx, cfg); st != SC_OK) return st;
   cudaIpcMemHandle_t h;
   SC_CUDA(ctx, cudaIpcGetMemHandle(&h, S.exch));
   std::memcpy(handle_out, &h, sizeof h);
-  S.peers[S.rank] = S.exch;
   return sc_shard_reset(ctx);
 }
 
@@ -730,9 +852,9 @@ sc_status sc_shard_reset(sc_ctx* ctx) {
   SC_CUDA(ctx, cudaSetDevice(ctx->device));
   auto& S = ctx->shard;
   char* ex = static_cast<char*>(S.exch);
-  SC_CUDA(ctx, cudaMemset(ex + S.off_slots, 0, S.off_ctr - S.off_slots));  // slots + tagged t words
-  SC_CUDA(ctx, cudaMemset(ex + S.off_ctr, 0, 4));                          // grid barrier counter
-  SC_CUDA(ctx, cudaMemset(ex + S.off_ctr + 4, 0xff, 12));                  // no error seen
+  SC_CUDA(ctx, cudaMemset(ex + S.off_slots, 0, S.off_ctr - S.off_slots));  // slots, rank slot, tagged t words
+  SC_CUDA(ctx, cudaMemset(ex + S.off_ctr, 0, 32));                         // barrier counters, abort word
+  SC_CUDA(ctx, cudaMemset(ex + S.off_ctr + 4, 0xff, 16));                  // no error / timeout seen
   SC_CUDA(ctx, cudaDeviceSynchronize());
   return SC_OK;
 }
@@ -749,12 +871,211 @@ sc_status sc_greedy_decompose_sharded(sc_ctx* ctx, const sc_problem* local, cons
   return run_decompose(ctx, local, res, &S);
 }
 
+// Row sharding emulated on one device: `world` virtual ranks, each with its own
+// child context (arena, exchange region, band of rows), launched as ONE
+// cooperative kernel (sweep_kernel_vr) so that ranks that wait on one another are
+// co-resident.  The peer pointers are the siblings' exchange regions.
+sc_status sc_greedy_decompose_sharded_emulated(sc_ctx* ctx, const sc_problem* p, const sc_shard_emulation* opt,
+                                               sc_result* res) {
+  const auto t_start = std::chrono::steady_clock::now();
+  if (ctx == nullptr) return SC_INVALID_ARGUMENT;
+  if (res == nullptr) return set_err(ctx, SC_INVALID_ARGUMENT, "sc_result: null");
+  std::string msg;
+  if (validate(p, &msg) != SC_OK) return set_err(ctx, SC_INVALID_ARGUMENT, "%s", msg.c_str());
+  if (p->order != 2) return set_err(ctx, SC_NOT_SUPPORTED, "emulated row sharding: matrices only");
+  if (res->sign_words[0] == nullptr || res->sign_words[1] == nullptr || res->cut_value == nullptr)
+    return set_err(ctx, SC_INVALID_ARGUMENT, "sc_result: sign_words of every axis and cut_value are required");
+  const int world = opt ? opt->world : 1;
+  if (world < 1 || world > scb::kMaxVRanks)
+    return set_err(ctx, SC_INVALID_ARGUMENT, "sc_shard_emulation: world must be in [1, %d]", scb::kMaxVRanks);
+  SC_CUDA(ctx, cudaSetDevice(ctx->device));
+  const uint64_t m = p->shape[0], n = p->shape[1];
+  const int G = (opt && opt->ctas > 0) ? opt->ctas : ctx->num_sms / world;
+  if (G < 1 || static_cast<long long>(G) * world > ctx->num_sms)
+    return set_err(ctx, SC_NOT_SUPPORTED, "emulated row sharding: %d ranks x %d CTAs exceed %d SMs", world, G,
+                   ctx->num_sms);
+  if (m / world < static_cast<uint64_t>(G))
+    return set_err(ctx, SC_NOT_SUPPORTED, "emulated row sharding: bands of %llu rows are smaller than %d CTAs",
+                   static_cast<unsigned long long>(m / world), G);
+  const size_t es = p->dtype == SC_F32 ? 4 : 8;
+  const uint64_t wmax = std::max<uint64_t>(p->width, 1), wn = words64(n);
+
+  struct Rank {
+    sc_ctx* kid = nullptr;
+    uint64_t row0 = 0, rows = 0;
+    uint64_t shape[2] = {0, 0};
+    sc_problem prob{};
+    sc_result res{};
+    std::vector<uint64_t> s_words, t_words;
+    std::vector<double> alpha, cut, rn, rne;
+    std::vector<uint32_t> sweeps;
+    RunState S;
+  };
+  std::vector<Rank> R(world);
+  auto cleanup = [&]() {
+    for (auto& r : R) {
+      if (!r.kid) continue;
+      sc_destroy(r.kid);  // borrowed stream/events survive; arena, pinned, exchange region freed
+      r.kid = nullptr;
+    }
+  };
+  auto fail = [&](sc_status st) {
+    const std::string e = ctx->err;
+    cleanup();
+    ctx->err = e;
+    return st;
+  };
+  for (int r = 0; r < world; ++r) {
+    Rank& k = R[r];
+    k.kid = new sc_ctx();
+    sc_ctx* c = k.kid;
+    c->device = ctx->device;
+    c->num_sms = ctx->num_sms;
+    c->smem_optin = ctx->smem_optin;
+    c->smem_per_sm = ctx->smem_per_sm;
+    c->stream = ctx->stream;
+    c->ev0 = ctx->ev0;
+    c->ev1 = ctx->ev1;
+    c->borrowed = true;
+    k.row0 = static_cast<uint64_t>(r) * m / world;
+    k.rows = static_cast<uint64_t>(r + 1) * m / world - k.row0;
+    sc_shard_config cfg{};
+    cfg.rank = r;
+    cfg.world = world;
+    cfg.m_global = m;
+    cfg.row0 = k.row0;
+    cfg.n = n;
+    cfg.dtype = p->dtype;
+    cfg.ctas = G;
+    auto& S = c->shard;
+    S.world = world;
+    S.rank = r;
+    S.dtype = p->dtype;
+    S.m_global = m;
+    S.row0 = k.row0;
+    S.n = n;
+    S.ipc = false;
+    S.timeout_ms = opt ? opt->timeout_ms : 0;
+    S.fault = (opt && opt->dead_rank == r) ? 1 : 0;
+    if (sc_status st = shard_alloc(c, &cfg); st != SC_OK) {
+      ctx->err = c->err;
+      return fail(st);
+    }
+  }
+  for (int r = 0; r < world; ++r) {
+    auto& S = R[r].kid->shard;
+    for (int q = 0; q < world; ++q) S.peers[q] = R[q].kid->shard.exch;
+    S.connected = true;
+    if (sc_status st = sc_shard_reset(R[r].kid); st != SC_OK) {
+      ctx->err = R[r].kid->err;
+      return fail(st);
+    }
+  }
+  for (int r = 0; r < world; ++r) {
+    Rank& k = R[r];
+    k.shape[0] = k.rows;
+    k.shape[1] = n;
+    k.prob = *p;
+    k.prob.shape = k.shape;
+    k.prob.data = static_cast<const char*>(p->data) + k.row0 * n * es;
+    k.s_words.assign(wmax * words64(k.rows), 0);
+    k.t_words.assign(wmax * wn, 0);
+    k.alpha.assign(wmax, 0.0);
+    k.cut.assign(wmax, 0.0);
+    k.rn.assign(wmax, 0.0);
+    k.rne.assign(wmax, 0.0);
+    k.sweeps.assign(wmax, 0);
+    k.res.sign_words[0] = k.s_words.data();
+    k.res.sign_words[1] = k.t_words.data();
+    k.res.alpha = k.alpha.data();
+    k.res.cut_value = k.cut.data();
+    k.res.resid_norm = k.rn.data();
+    k.res.resid_norm_exact = k.rne.data();
+    k.res.sweeps = k.sweeps.data();
+    k.res.remainder = res->remainder ? static_cast<char*>(res->remainder) + k.row0 * n * es : nullptr;
+    if (sc_status st = prepare_run(k.kid, &k.prob, &k.res, &k.kid->shard, k.S, true); st != SC_OK) {
+      ctx->err = k.kid->err;
+      return fail(st);
+    }
+  }
+  scb::KParamsVR pv{};
+  pv.world = world;
+  size_t smem = 0;
+  for (int r = 0; r < world; ++r) {
+    if (R[r].S.var.nw != R[0].S.var.nw || R[r].S.var.vpt != R[0].S.var.vpt || R[r].S.var.rg != R[0].S.var.rg ||
+        R[r].S.G != G)
+      return fail(set_err(ctx, SC_RUNTIME_ERROR, "emulated row sharding: ranks chose different kernels"));
+    pv.r[r] = R[r].S.kp;
+    smem = std::max(smem, R[r].S.smem);
+  }
+  if (static_cast<size_t>(smem) > ctx->smem_optin)
+    return fail(set_err(ctx, SC_NOT_SUPPORTED, "emulated row sharding: %zu bytes of shared memory", smem));
+  if (cudaError_t e = scb::set_smem_limit_vr(R[0].S.var, smem); e != cudaSuccess)
+    return fail(set_err(ctx, SC_CUDA_ERROR, "set_smem_limit_vr: %s", cudaGetErrorString(e)));
+  cudaEventRecord(ctx->ev0, ctx->stream);
+  if (cudaError_t e = scb::launch_sweep_vr(R[0].S.var, pv, G, smem, ctx->stream); e != cudaSuccess)
+    return fail(set_err(ctx, SC_CUDA_ERROR, "launch_sweep_vr: %s", cudaGetErrorString(e)));
+  cudaEventRecord(ctx->ev1, ctx->stream);
+  for (int r = 0; r < world; ++r) {
+    if (sc_status st = finish_run(R[r].kid, &R[r].prob, &R[r].res, R[r].S); st != SC_OK) {
+      ctx->err = R[r].kid->err;
+      return fail(st);
+    }
+  }
+  // gather: every rank must hold the same t, c and sweeps (one decision everywhere)
+  const uint64_t wd = R[0].res.width_done;
+  for (int r = 1; r < world; ++r) {
+    const Rank& k = R[r];
+    if (k.res.width_done != wd || std::memcmp(k.t_words.data(), R[0].t_words.data(), wd * wn * 8) != 0 ||
+        std::memcmp(k.cut.data(), R[0].cut.data(), wd * 8) != 0 ||
+        std::memcmp(k.sweeps.data(), R[0].sweeps.data(), wd * 4) != 0)
+      return fail(set_err(ctx, SC_RUNTIME_ERROR, "emulated row sharding: rank %d disagrees with rank 0", r));
+  }
+  const uint64_t wm = words64(m);
+  for (uint64_t t = 0; t < wd; ++t) {
+    uint64_t* dst = res->sign_words[0] + t * wm;
+    std::fill(dst, dst + wm, uint64_t{0});
+    for (int r = 0; r < world; ++r) {
+      const Rank& k = R[r];
+      const uint64_t* src = k.s_words.data() + t * words64(k.rows);
+      for (uint64_t i = 0; i < k.rows; ++i)
+        if ((src[i / 64] >> (i % 64)) & 1u) dst[(k.row0 + i) / 64] |= uint64_t{1} << ((k.row0 + i) % 64);
+    }
+  }
+  std::memcpy(res->sign_words[1], R[0].t_words.data(), wd * wn * 8);
+  std::memcpy(res->cut_value, R[0].cut.data(), wd * 8);
+  if (res->alpha) std::memcpy(res->alpha, R[0].alpha.data(), wd * 8);
+  if (res->resid_norm) std::memcpy(res->resid_norm, R[0].rn.data(), wd * 8);
+  if (res->resid_norm_exact) std::memcpy(res->resid_norm_exact, R[0].rne.data(), wd * 8);
+  if (res->sweeps) std::memcpy(res->sweeps, R[0].sweeps.data(), wd * 4);
+  res->width_done = wd;
+  res->input_norm = R[0].res.input_norm;
+  res->final_residual_norm = R[0].res.final_residual_norm;
+  res->passes = R[0].res.passes;
+  res->dense_passes = R[0].res.dense_passes;
+  res->delta_passes = R[0].res.delta_passes;
+  res->device_bytes = 0;
+  for (const auto& k : R) res->device_bytes += k.res.device_bytes;
+  res->kernel_ms = R[0].res.kernel_ms;
+  res->kernel_launches = 1;
+  res->n_sweep_values = 0;
+  res->h2d_bytes = 0;
+  res->d2h_bytes = 0;
+  for (const auto& k : R) {
+    res->h2d_bytes += k.res.h2d_bytes;
+    res->d2h_bytes += k.res.d2h_bytes;
+  }
+  cleanup();
+  res->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  return SC_OK;
+}
+
 void sc_shard_close(sc_ctx* ctx) {
   if (!ctx) return;
   auto& S = ctx->shard;
   cudaSetDevice(ctx->device);
   for (int r = 0; r < 8; ++r)
-    if (S.peers[r] && r != S.rank) cudaIpcCloseMemHandle(S.peers[r]);
+    if (S.ipc && S.peers[r] && r != S.rank) cudaIpcCloseMemHandle(S.peers[r]);
   if (S.exch) cudaFree(S.exch);
   S = sc_ctx::Shard{};
 }

@@ -19,6 +19,7 @@ struct sc_ctx {
   size_t smem_per_sm = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool borrowed = false;  // stream / events belong to a parent context (emulated ranks)
   std::string err;
   // cached device arena and pinned staging
   void* arena = nullptr;
@@ -32,9 +33,12 @@ struct sc_ctx {
     int tw32 = 0;
     uint64_t m_global = 0, row0 = 0, n = 0;
     void* exch = nullptr;
-    size_t exch_bytes = 0, off_zpart = 0, off_slots = 0, off_tb64 = 0, off_ctr = 0;
+    size_t exch_bytes = 0, off_zpart = 0, off_zr = 0, off_slots = 0, off_rslot = 0, off_tb64 = 0, off_ctr = 0;
     void* peers[8] = {};
     bool connected = false;
+    bool ipc = true;          // peers opened with cudaIpcOpenMemHandle (false: emulated ranks, same device)
+    uint32_t timeout_ms = 0;  // bound of the kernel's cross-rank spins (0 = 30 s)
+    int fault = 0;            // test hook (emulation): this rank's CTAs exit at once
   } shard;
   // auxiliary ops (expansion, Gram system, least squares): named grow-only
   // device buffers, so a driver can hold several at once

@@ -13,6 +13,7 @@ void* kernel_f32m(const Variant& v);
 void* kernel_f32t(const Variant& v);
 void* kernel_f64m(const Variant& v);
 void* kernel_f64t(const Variant& v);
+void* kernel_vr(const Variant& v);
 
 namespace {
 void* kernel_for(const Variant& v) {
@@ -85,6 +86,24 @@ cudaError_t launch_sweep(const Variant& v, const KParams& p, size_t smem_bytes, 
   KParams copy = p;
   void* args[] = {&copy};
   return cudaLaunchCooperativeKernel(f, dim3(p.G), dim3((v.nw + 1) * 32), args, smem_bytes, st);
+}
+
+bool has_vr(const Variant& v) { return kernel_vr(v) != nullptr; }
+
+cudaError_t set_smem_limit_vr(const Variant& v, size_t bytes) {
+  void* f = kernel_vr(v);
+  if (!f) return cudaErrorInvalidValue;
+  const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+
+cudaError_t launch_sweep_vr(const Variant& v, const KParamsVR& p, int G, size_t smem_bytes, cudaStream_t st) {
+  void* f = kernel_vr(v);
+  if (!f) return cudaErrorInvalidValue;
+  KParamsVR copy = p;
+  void* args[] = {&copy};
+  return cudaLaunchCooperativeKernel(f, dim3(G * p.world), dim3((v.nw + 1) * 32), args, smem_bytes, st);
 }
 
 }  // namespace scb

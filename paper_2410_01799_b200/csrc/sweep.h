@@ -21,6 +21,7 @@ enum PassFlags : int {
 };
 
 enum ErrSlot : int { ERR_Y = 0, ERR_Z = 1, ERR_INPUT = 2 };
+// err_pass[3] (world > 1): first pass at which a cross-rank spin timed out or saw the abort word
 
 // Per-CTA scalar partials of a pass, double-buffered by pass parity (a CTA can
 // run at most one pass ahead of the slowest reader).
@@ -43,6 +44,7 @@ struct Ctl {
   volatile int decided;  // kinds of passes [0, decided) are published
   volatile int stored;   // global-R writes of passes [0, stored) are complete
   volatile int abort;
+  volatile int aborted;  // world > 1: a cross-rank spin of this CTA timed out / saw the abort word
   volatile int kind_ring[4];
   // controller state (thread 0 writes, consumers read after a named barrier)
   int kind, pp, term, restart, tsel, utsel, best_tsel, best_sweeps, best_restart;
@@ -54,7 +56,9 @@ struct Ctl {
                         // recounted by the axial step for the next pass's t (read by the decision)
   int since_dense;      // delta passes since the last dense dot pass
   int has_dz;           // this CTA wrote a z partial in a delta pass
+  int nfrows;           // this CTA's flipped streamed rows in the last delta pass
   int keep;             // t unchanged since the last dot pass: y, s, z stay exactly as cached
+  unsigned rank_dz;     // world > 1: ranks whose rank partial holds a delta-pass dz
   double cred[64];  // per-warp partials (axial step: 4 outputs x up to 16 warps)
   int axn[8], axoff[8];  // order-k: n_1..n_{k-1} and their axis-word offsets (shared-memory copies)
   double nred[32];
@@ -88,7 +92,9 @@ struct KParams {
   double* c_out;       // [width]
   uint32_t* sweeps_out;  // [width]
   double* norm2_out;   // [width + 1]: [0] = ||A||^2, [k+1] = ||R after term k||^2
-  unsigned long long* stats;  // [0] width_done, [1] passes, [2]/[3] dense/delta dot passes, [4] term 0's winning restart
+  unsigned long long* stats;  // [0] width_done, [1] passes, [2]/[3] dense/delta dot passes, [4] term 0's winning restart,
+                              // [5] bytes moved through L2 / HBM by the kernel (R streaming, delta gathers,
+                              //     rank-1 update writes, column-partial exchange)
   double* sweep_vals;  // [restarts][max_sweeps] c of every sweep of term 0 (SearchDiagnostics) or nullptr
   long long width, restarts, max_sweeps;
   double min_frac;
@@ -118,11 +124,28 @@ struct KParams {
   // kernel on its row band with the same G; the exchange buffers of all ranks are
   // peer-mapped (CUDA IPC over NVLink) and the CTAs of all ranks form one grid:
   // global CTA gg = rank * G + g, GT = world * G.  world == 1: the local buffers.
+  // Per pass each rank first reduces its own G column partials into one rank
+  // partial (zr, n f64) and its G slots into one rank slot, behind a rank-local
+  // barrier; only those cross NVLink (n f64 + 3 f64 per rank and pass).
   int world, rank, GT;
-  double* zpart_pe[8];               // per-rank [2][G][pitch] column partials
-  Slot* slots_pe[8];                 // per-rank [G] slots
+  double* zr_pe[8];                  // per-rank [2][pitch] rank column partials (by pass parity)
+  Slot* rslot_pe[8];                 // per-rank rank slot (c, ||R||^2, any dz), by pass parity
   unsigned long long* tb64_pe[8];    // per-rank [2][Q] tagged t words (owners write all)
+  unsigned* bar_local;               // this rank's local barrier counter (world > 1)
+  unsigned* abort_word;              // rank 0's: set by any CTA whose spin timed out (world > 1)
+  long long timeout_ns;              // bound of every cross-rank spin (world > 1)
+  int fault;                         // test hook: 1 = this rank's CTAs exit at once (a dead rank)
   unsigned long long* prof;  // [G][16] clock64 breakdown or nullptr
+};
+
+// Virtual ranks (row-sharding emulated on one GPU): ONE cooperative launch of
+// world * G CTAs; CTA block r plays rank r with its own parameters.  The ranks
+// wait on one another, so they must be one launch (co-resident), never separate
+// kernels on one device.
+constexpr int kMaxVRanks = 8;
+struct KParamsVR {
+  KParams r[kMaxVRanks];
+  int world;
 };
 
 // Kernel variant: consumer warps and per-thread register tiles.
@@ -189,5 +212,9 @@ int pick_variant(int dtype, long long pitch, Variant* v);
 cudaError_t set_smem_limit(const Variant& v, size_t bytes);
 int blocks_per_sm(const Variant& v, size_t smem_bytes);  // co-resident CTAs at this smem
 cudaError_t launch_sweep(const Variant& v, const KParams& p, size_t smem_bytes, cudaStream_t st);
+// virtual-rank launch (world * G CTAs); false from has_vr: no such instantiation
+bool has_vr(const Variant& v);
+cudaError_t set_smem_limit_vr(const Variant& v, size_t bytes);
+cudaError_t launch_sweep_vr(const Variant& v, const KParamsVR& p, int G, size_t smem_bytes, cudaStream_t st);
 
 }  // namespace scb

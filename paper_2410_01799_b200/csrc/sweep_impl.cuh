@@ -119,11 +119,49 @@ __device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void grid_barrier_sys(unsigned* bar, unsigned target) {
-  asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-  while (static_cast<int>(ld_relaxed_sys(bar) - target) < 0) {
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Bounded spin of the row-sharded (world > 1) exchange: every 256 polls it checks
+// the shared abort word (rank 0's) and the elapsed time; a timeout sets the abort
+// word so every other waiting CTA of every rank gives up too.  Returns false then.
+struct SpinBound {
+  unsigned* abort_word;
+  long long timeout_ns;
+  unsigned long long t0;
+  unsigned it;
+  __device__ __forceinline__ bool ok() {
+    if ((++it & 255u) != 0u) return true;
+    if (ld_relaxed_sys(abort_word) != 0u) return false;
+    const unsigned long long t = global_ns();
+    if (t0 == 0) {
+      t0 = t;
+    } else if (static_cast<long long>(t - t0) > timeout_ns) {
+      atomicExch_system(abort_word, 1u);
+      return false;
+    }
+    return true;
   }
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
+};
+// Cross-rank barrier (counter on rank 0, reached over NVLink) and the rank-local
+// one of a sharded run, both bounded by the abort word / timeout.
+template <bool SYS>
+__device__ __noinline__ bool grid_barrier_bounded(unsigned* bar, unsigned target, unsigned* abort_word,
+                                                  long long timeout_ns) {
+  if (SYS)
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+  else
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+  SpinBound sb{abort_word, timeout_ns, 0ull, 0u};
+  while (static_cast<int>((SYS ? ld_relaxed_sys(bar) : ld_relaxed(bar)) - target) < 0)
+    if (!sb.ok()) return false;
+  if (SYS)
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  return true;
 }
 __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
   unsigned long long v;
@@ -1023,6 +1061,7 @@ struct DeltaArgs {
   double* zrow;       // this CTA's z partial row of this pass
   unsigned* errp;
   int* has_dz;
+  int* nfrows;        // flipped rows read from global memory (streamed rows; byte accounting)
   long long pitch;
   unsigned rowB;
   int rows_g, nres, Q, NV, P;
@@ -1190,6 +1229,7 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
   // chunk: the flipped rows are read once per chunk, each chunk's partial stored.
   constexpr int chunkV = NW * 32 * VPT;
   bool any = false;
+  int nfg = 0;  // flipped streamed rows (read from L2 / HBM), counted once
   const int sw = (rows_g + 31) / 32;
   for (int ck = 0; ck < a.cpr; ++ck) {
     int vidx[VPT];
@@ -1227,6 +1267,7 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
         const int j = w * 32 + __ffs(f) - 1;
         f &= f - 1;
         any = true;
+        if (ck == 0 && j >= nres) ++nfg;
         if (pend < 0) {
           pend = j;
           continue;
@@ -1256,7 +1297,10 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
       }
     }
   }
-  if (tid == 0) *a.has_dz = any ? 1 : 0;
+  if (tid == 0) {
+    *a.has_dz = any ? 1 : 0;
+    *a.nfrows = nfg;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1471,7 +1515,7 @@ __device__ __noinline__ int tensor_continue(Ctl* ctl, int delta, int refresh, in
 // NE = VPT * EPV elements per row, and the matching NE f64 column accumulators.
 // CPS: CTAs per SM (1, or 2 with a 112-register budget and raw lag buffers).
 template <typename E, int NW, int VPT, int RG, int CPS, bool TS>
-__device__ __forceinline__ void sweep_body(const KParams& p) {
+__device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
   constexpr int EPV = Vec<E>::N;
   constexpr int CW = NW;       // consumer warps
   constexpr int CT = CW * 32;  // consumer threads
@@ -1484,8 +1528,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int g = blockIdx.x;
   const int G = p.G;
+  if (p.fault) return;  // test hook: a rank that never joins (the others must time out, not hang)
   const long long pitch = p.pitch;
   const size_t rowB = static_cast<size_t>(pitch) * sizeof(E);
   const int NV = static_cast<int>(pitch / EPV);
@@ -1530,6 +1574,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     ctl->decided = 1;
     ctl->stored = 0;
     ctl->abort = 0;
+    ctl->aborted = 0;
+    ctl->rank_dz = 0;
     ctl->pp = TS ? 1 : 0;  // order-k: pp = sweep of the current pass (1-based)
     for (int j = 0; j < 8; ++j) {  // read by the axial step from shared memory, not the param copy
       ctl->axn[j] = j < 7 ? p.ax_n[j] : 1;
@@ -1648,7 +1694,9 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   int qs = 0, qph = 0;     // stage / phase of this pass's first streamed row
   unsigned gcount = 0;     // dot-partial groups published in earlier passes
   unsigned epoch = 0;      // grid barriers passed (thread 0)
+  unsigned lepoch = 0;     // rank-local barriers passed (thread 0, world > 1)
   unsigned long long dot_passes[2] = {0, 0};  // CTA 0: dense, delta dot passes (-> stats[2], [3])
+  unsigned long long phys = 0;  // thread 0: bytes this CTA moved through L2 / HBM (-> stats[5])
   int vidx[VPT];           // owned vectors (clamped to a valid address when out of range)
   bool vok[VPT];
 #pragma unroll
@@ -1659,14 +1707,17 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
   }
 
   // Owner CTAs sum the G column partials of their 32-column words in a fixed
-  // order; matrix mode publishes sgn(z) as tagged t words, order-k mode stores
-  // z itself.  Ends with a grid barrier.
+  // order.  mode 0 (one GPU, matrix): publish sgn(z) as tagged t words; mode 1
+  // (order-k): store z itself; mode 2 (row-sharded, world > 1): store the RANK
+  // partial zr of the column (this rank's G partials), which the global owners
+  // combine after the cross-rank barrier (col_reduce_global).  Mode 1 ends with
+  // a grid barrier.
   // tbuf: the tb64 buffer the next pass reads ((pp + 1) & 1); the decision may
   // still stop the restart -- then these words are simply never read (the kept
   // triple's t lives in the other buffer).
   // Warps w0..CW-1 take part (w0 = 1: warp 0 runs the controller decision meanwhile
   // and the participants synchronise on named barrier 2).
-  auto col_reduce = [&](bool zmode, int P, bool delta, int tbuf, int w0) {
+  auto col_reduce = [&](int mode, int P, bool delta, int tbuf, int w0) {
     const int NP = CW - w0, lw = warp - w0;
     auto psync = [&]() {
       if (w0 == 0)
@@ -1674,53 +1725,47 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       else
         asm volatile("bar.sync 2, %0;" ::"r"(NP * 32) : "memory");
     };
+    const bool zstate_here = p.delta && mode != 2;  // z state kept by the owners (one GPU; order-k too)
     double zsv[4];  // warp 0: z state of its word slices, parked in zst before the combine
     unsigned long long* tout = p.tb64 + static_cast<size_t>(tbuf) * p.Q * kTbStride;
     const unsigned long long tag = static_cast<unsigned long long>(P + 1) << 32;
-    // owners by global CTA index: the CTAs of all ranks share the column words
-    const int GT = p.GT, gg = p.rank * G + g;
-    const int gs = (lw * GT) / NP, ge = ((lw + 1) * GT) / NP;
-    for (int q0 = gg; q0 < p.Q; q0 += GT * p.zl) {
+    const int gs = (lw * G) / NP, ge = ((lw + 1) * G) / NP;
+    for (int q0 = g; q0 < p.Q; q0 += G * p.zl) {
       int nls = 0;
-      for (int j = 0; j < p.zl && q0 + j * GT < p.Q; ++j) nls = j + 1;
+      for (int j = 0; j < p.zl && q0 + j * G < p.Q; ++j) nls = j + 1;
       for (int j = 0; j < nls; ++j) {
-        const int col = (q0 + j * GT) * 32 + lane;
+        const int col = (q0 + j * G) * 32 + lane;
         const size_t par = static_cast<size_t>(P & 1) * G * pitch + col;  // pass-parity buffer
-        if (p.delta && lw == 0 && col < p.n) zsv[j] = __ldcg(p.zstate + col);  // issued early
+        if (zstate_here && lw == 0 && col < p.n) zsv[j] = __ldcg(p.zstate + col);  // issued early
         double a = 0.0;
+        const double* zb = p.zpart + par;
         for (int g0 = gs; g0 < ge; g0 += 32) {  // one round of up to 32 L2 loads in flight
           double v[32];
-          if (p.world > 1) {  // partials of every rank through the peer mappings
 #pragma unroll
-            for (int u = 0; u < 32; ++u) {
-              const int gp = g0 + u;
-              const bool take = gp < ge && (!delta || ((dzmask[gp >> 5] >> (gp & 31)) & 1u));
-              v[u] = take ? __ldcg(p.zpart_pe[gp / G] + static_cast<size_t>(gp % G) * pitch + par) : 0.0;
-            }
-          } else {  // single GPU: no per-load division or parameter-array indexing
-            const double* zb = p.zpart + par;
-#pragma unroll
-            for (int u = 0; u < 32; ++u) {
-              const int gp = g0 + u;
-              const bool take = gp < ge && (!delta || ((dzmask[gp >> 5] >> (gp & 31)) & 1u));
-              v[u] = take ? __ldcg(zb + static_cast<size_t>(gp) * pitch) : 0.0;
-            }
+          for (int u = 0; u < 32; ++u) {
+            const int gp = g0 + u;
+            const bool take = gp < ge && (!delta || ((dzmask[gp >> 5] >> (gp & 31)) & 1u));
+            v[u] = take ? __ldcg(zb + static_cast<size_t>(gp) * pitch) : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < 32; ++u) a += v[u];
         }
         zseg[(j * CW + lw) * 32 + lane] = a;
-        if (p.delta && lw == 0) zst[j * 32 + lane] = (col < p.n) ? zsv[j] : 0.0;
+        if (zstate_here && lw == 0) zst[j * 32 + lane] = (col < p.n) ? zsv[j] : 0.0;
       }
       psync();
       for (int j = lw; j < nls; j += NP) {
-        const int qq = q0 + j * GT;
+        const int qq = q0 + j * G;
         const int col = qq * 32 + lane;
         double z = 0.0;
 #pragma unroll
         for (int w = 0; w < NP; ++w) z += zseg[(j * CW + w) * 32 + lane];
         const bool valid = col < p.n;
-        if (p.delta && valid) {  // z state for delta passes: dense sets it, delta adds to it
+        if (mode == 2) {  // rank partial: combined and checked by the global owners
+          if (valid) __stcg(p.zr_pe[p.rank] + static_cast<size_t>(P & 1) * pitch + col, z);
+          continue;
+        }
+        if (zstate_here && valid) {  // z state for delta passes: dense sets it, delta adds to it
           const double zs = zst[j * 32 + lane];
           if (ctl->keep && !delta)
             z = zs;  // fixed point: z as cached
@@ -1729,16 +1774,11 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
           __stcg(p.zstate + col, z);
         }
         if (valid && !isfinite(z)) atomicMin(const_cast<unsigned*>(errp) + ERR_Z, static_cast<unsigned>(P));
-        if (zmode) {  // order-k: Z = M^T s_0 for the axial step
+        if (mode == 1) {  // order-k: Z = M^T s_0 for the axial step
           if (valid) __stcg(p.zfull + col, z);
         } else {
           const unsigned word = __ballot_sync(0xffffffffu, valid && z < 0.0);
-          if (p.world > 1) {  // every rank stages t from its own copy
-            if (lane < p.world)
-              st_relaxed64_sys(p.tb64_pe[lane] + (static_cast<size_t>(tbuf) * p.Q + qq) * kTbStride, tag | word);
-          } else if (lane == 0) {
-            st_relaxed64(tout + static_cast<size_t>(qq) * kTbStride, tag | word);
-          }
+          if (lane == 0) st_relaxed64(tout + static_cast<size_t>(qq) * kTbStride, tag | word);
         }
       }
       psync();
@@ -1748,11 +1788,47 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     // pass-tagged t words, and zpart / slots / tb64 are reused only two passes
     // later, i.e. after the next pass's grid barrier, which every CTA reaches
     // only after finishing this reduction.
-    if (zmode) {
+    if (mode == 1) {
       const long long tz = prof ? clock64() : 0;
       if (tid == 0) grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
       consumer_sync(CT);
       if (prof && tid == 0) pten[2] += clock64() - tz;
+    }
+  };
+  // Row-sharded (world > 1), after the cross-rank barrier: the owner of a 32-column
+  // word (by global CTA index over all ranks) adds the world rank partials in rank
+  // order (in delta passes only the ranks that had a flipped row), keeps the z state,
+  // and publishes sgn(z) to every rank.  One warp per word; no cross-warp combine.
+  auto col_reduce_global = [&](int P, bool delta, int tbuf, int w0) {
+    const int NP = CW - w0, lw = warp - w0;
+    const int GT = p.GT, gg = p.rank * G + g;
+    const unsigned long long tag = static_cast<unsigned long long>(P + 1) << 32;
+    const unsigned rdz = ctl->rank_dz;
+    int k = 0;
+    for (int qq = gg; qq < p.Q; qq += GT, ++k) {
+      if (k % NP != lw) continue;
+      const int col = qq * 32 + lane;
+      const bool valid = col < p.n;
+      const size_t off = static_cast<size_t>(P & 1) * pitch + col;
+      const double zs = (p.delta && valid) ? __ldcg(p.zstate + col) : 0.0;
+      double v[kMaxVRanks];
+#pragma unroll
+      for (int r = 0; r < kMaxVRanks; ++r)
+        v[r] = (r < p.world && valid && (!delta || ((rdz >> r) & 1u))) ? __ldcg(p.zr_pe[r] + off) : 0.0;
+      double z = 0.0;
+#pragma unroll
+      for (int r = 0; r < kMaxVRanks; ++r) z += v[r];
+      if (p.delta && valid) {
+        if (ctl->keep && !delta)
+          z = zs;
+        else if (delta)
+          z = zs + z;
+        __stcg(p.zstate + col, z);
+      }
+      if (valid && !isfinite(z)) atomicMin(const_cast<unsigned*>(errp) + ERR_Z, static_cast<unsigned>(P));
+      const unsigned word = __ballot_sync(0xffffffffu, valid && z < 0.0);
+      if (lane < p.world)  // every rank stages t from its own copy
+        st_relaxed64_sys(p.tb64_pe[lane] + (static_cast<size_t>(tbuf) * p.Q + qq) * kTbStride, tag | word);
     }
   };
 
@@ -1779,12 +1855,29 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       } else if (!TS) {  // order-k: tws was rebuilt by the previous pass's axial step
         // t words were published before the last grid barrier, tagged with this pass
         const unsigned long long* tw = p.tb64 + static_cast<size_t>(ctl->tsel) * p.Q * kTbStride;
-        for (int i = tid; i < p.Q; i += CT) {
-          unsigned long long x;
-          do {
-            x = p.world > 1 ? ld_relaxed64_sys(tw + i * kTbStride) : ld_relaxed64(tw + i * kTbStride);
-          } while (static_cast<int>(static_cast<unsigned>(x >> 32) - static_cast<unsigned>(P)) < 0);
-          tws[i] = static_cast<uint32_t>(x);
+        if (p.world > 1) {  // published by owners on every rank: bounded spin
+          SpinBound sb{p.abort_word, p.timeout_ns, 0ull, 0u};
+          for (int i = tid; i < p.Q; i += CT) {
+            unsigned long long x;
+            bool ok = true;
+            do {
+              x = ld_relaxed64_sys(tw + i * kTbStride);
+            } while (static_cast<int>(static_cast<unsigned>(x >> 32) - static_cast<unsigned>(P)) < 0 && (ok = sb.ok()));
+            if (!ok) {
+              ctl->aborted = 1;
+              atomicMin(const_cast<unsigned*>(errp) + 3, static_cast<unsigned>(P));
+              break;
+            }
+            tws[i] = static_cast<uint32_t>(x);
+          }
+        } else {
+          for (int i = tid; i < p.Q; i += CT) {
+            unsigned long long x;
+            do {
+              x = ld_relaxed64(tw + i * kTbStride);
+            } while (static_cast<int>(static_cast<unsigned>(x >> 32) - static_cast<unsigned>(P)) < 0);
+            tws[i] = static_cast<uint32_t>(x);
+          }
         }
       }
       {  // t flips since the previous pass (delta passes), counted exactly
@@ -1807,6 +1900,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
                                  : static_cast<uint32_t>(__ldcg(p.tb64 + (static_cast<size_t>(ctl->utsel) * p.Q + i) * kTbStride));
     }
     consumer_sync(CT);
+    if (p.world > 1 && ctl->aborted) break;  // uniform: set before the barrier
     if (prof && tid == 0) pacc[5] += clock64() - t_pass0;
     // A sweep whose t equals the previous pass's t is a fixed point of the cached
     // products: y, s' and z stay exactly as cached whatever pass form runs, so a
@@ -1860,6 +1954,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
         dl.zrow = da.zrow;
         dl.errp = da.errp;
         dl.has_dz = &ctl->has_dz;
+        dl.nfrows = &ctl->nfrows;
         dl.pitch = pitch;
         dl.rowB = static_cast<unsigned>(rowB);
         dl.rows_g = rows_g;
@@ -1944,6 +2039,25 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       qs = t % D;
     }
 
+    // Physical traffic of this pass (thread 0; R reads from SMEM-resident rows are on chip
+    // and not counted): streamed rows (twice for the two-phase pass), delta gathers at
+    // 32-byte sector granularity plus the flipped streamed rows, the rank-1 update's
+    // write-back, and the column-partial row this CTA stores.
+    if (tid == 0) {
+      const unsigned long long sbytes = static_cast<unsigned long long>(nstream) * rowB;
+      const unsigned long long zbytes = static_cast<unsigned long long>(pitch) * 8ull;
+      if (kind & F_DOT) {
+        if (kind & F_DELTA) {
+          phys += static_cast<unsigned long long>(ctl->nflip) * nstream * 32ull +
+                  static_cast<unsigned long long>(ctl->nfrows) * rowB + (ctl->has_dz ? zbytes : 0ull);
+        } else {
+          phys += sbytes * (p.two_phase ? 2ull : 1ull) + zbytes;
+        }
+      } else {
+        phys += sbytes * ((kind & F_UPD) ? 2ull : 1ull) +
+                ((kind & F_WB) ? static_cast<unsigned long long>(nres) * rowB : 0ull);
+      }
+    }
     // ------------------------------ pass end ------------------------------
     if (prof && tid == 0) {
       const long long t = clock64();
@@ -1990,19 +2104,24 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     }
     if (tid == 0) {
       const long long tb0 = prof ? clock64() : 0;
-      if (p.world > 1)
-        grid_barrier_sys(p.bar, ++epoch * static_cast<unsigned>(p.GT));
-      else
+      if (p.world > 1) {  // rank-local barrier first (the rank partials need this rank's partials)
+        if (!grid_barrier_bounded<false>(p.bar_local, ++lepoch * static_cast<unsigned>(G), p.abort_word,
+                                         p.timeout_ns)) {
+          ctl->aborted = 1;
+          atomicMin(const_cast<unsigned*>(errp) + 3, static_cast<unsigned>(P));
+        }
+      } else {
         grid_barrier(p.bar, ++epoch * static_cast<unsigned>(G));
+      }
       if (prof) pacc[6] += clock64() - tb0;  // barrier (incl. waiting for the last CTA)
     }
     consumer_sync(CT);
+    if (p.world > 1 && ctl->aborted) break;
     {
-      // every CTA (of every rank) reduces the GT partials in the same fixed order
+      // every CTA reduces the G partials of its rank in the same fixed order
       double cs = 0.0, ns = 0.0;
-      const bool multi = p.world > 1;
-      for (int i = tid; i < p.GT; i += CT) {
-        const Slot* s = multi ? p.slots_pe[i / G] + (i % G) : p.slots + i;
+      for (int i = tid; i < G; i += CT) {
+        const Slot* s = p.slots + i;
         cs += __ldcg(&s->c[P & 1]);
         ns += __ldcg(&s->n[P & 1]);
         if ((kind & F_DELTA) && __ldcg(&s->dz[P & 1]) != 0.0) atomicOr(&dzmask[i >> 5], 1u << (i & 31));
@@ -2021,6 +2140,73 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
       }
     }
     consumer_sync(CT);
+    if (tid == 0 && g == 0 && (kind & F_DOT)) {  // owners' reads of the column partials (grid total)
+      unsigned long long parts = static_cast<unsigned long long>(G);
+      if (kind & F_DELTA) {
+        parts = 0;
+        for (int i = 0; i < 64; ++i) parts += __popc(dzmask[i]);
+      }
+      phys += (parts + (p.world > 1 ? 1ull : 0ull)) * static_cast<unsigned long long>(pitch) * 8ull;
+    }
+    if (p.world > 1) {
+      // Rank stage: this rank's column partials -> one rank partial zr (local
+      // owners), its slots -> one rank slot; then the cross-rank barrier, after
+      // which every CTA of every rank combines the world rank slots in rank order.
+      if (!TS && (kind & F_DOT)) col_reduce(2, P, (kind & F_DELTA) != 0, 0, 0);
+      if (tid == 0) {
+        double cs = 0.0, ns = 0.0;
+        for (int w = 0; w < CW; ++w) {
+          cs += ctl->cred[w];
+          ns += ctl->nred[w];
+        }
+        unsigned anydz = 0;
+        for (int i = 0; i < 64; ++i) anydz |= dzmask[i];
+        if (g == 0) {
+          Slot* rs = p.rslot_pe[p.rank];
+          __stcg(&rs->c[P & 1], cs);
+          __stcg(&rs->n[P & 1], ns);
+          __stcg(&rs->dz[P & 1], ((kind & F_DELTA) && anydz) ? 1.0 : 0.0);
+        }
+      }
+      consumer_sync(CT);
+      if (tid == 0) {
+        if (!grid_barrier_bounded<true>(p.bar, ++epoch * static_cast<unsigned>(p.GT), p.abort_word,
+                                        p.timeout_ns)) {
+          ctl->aborted = 1;
+          atomicMin(const_cast<unsigned*>(errp) + 3, static_cast<unsigned>(P));
+        }
+      }
+      consumer_sync(CT);
+      if (ctl->aborted) break;
+      if (warp == 0) {
+        double c = 0.0, n2 = 0.0, dz = 0.0;
+        if (lane < p.world) {
+          const Slot* rs = p.rslot_pe[lane];
+          c = __ldcg(&rs->c[P & 1]);
+          n2 = __ldcg(&rs->n[P & 1]);
+          dz = __ldcg(&rs->dz[P & 1]);
+        }
+        const unsigned rdz = __ballot_sync(0xffffffffu, dz != 0.0);
+        double cs = 0.0, ns = 0.0;  // rank order
+        for (int r = 0; r < p.world; ++r) {
+          cs += __shfl_sync(0xffffffffu, c, r);
+          ns += __shfl_sync(0xffffffffu, n2, r);
+        }
+        if (lane == 0) {
+          ctl->rank_dz = rdz;
+          ctl->cred[0] = cs;
+          ctl->nred[0] = ns;
+          for (int w = 1; w < CW; ++w) {
+            ctl->cred[w] = 0.0;
+            ctl->nred[w] = 0.0;
+          }
+          ctl->err_pre[0] = __ldcg(errp + ERR_Y);  // rank 0's words: every rank's errors so far
+          ctl->err_pre[1] = __ldcg(errp + ERR_INPUT);
+          ctl->err_pre[2] = __ldcg(errp + ERR_Z);
+        }
+      }
+      consumer_sync(CT);
+    }
     if (prof && tid == 0) {
       const long long t = clock64();
       pacc[2] += t - t_pass0;
@@ -2028,7 +2214,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     }
     if (TS && (kind & F_DOT)) {  // order-k: Z = M^T s_0, then axes 1..k-1 and c
       const long long ta = prof ? clock64() : 0;
-      col_reduce(true, P, (kind & F_DELTA) != 0, 0, 0);
+      col_reduce(1, P, (kind & F_DELTA) != 0, 0, 0);
       const long long tb = prof ? clock64() : 0;
       axial_step<CW>(p, sax, tws, tprev, ctl, P, prof ? pten + 3 : nullptr);
       if (prof && tid == 0) {
@@ -2039,8 +2225,12 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
 
     // Matrix dot pass: owners reduce z and publish the next t right away (it does
     // not depend on the decision), taking the decision off every CTA's critical path.
-    if (!TS && (kind & F_DOT) && warp >= 1)  // warp 0 runs the decision below meanwhile
-      col_reduce(false, P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
+    if (!TS && (kind & F_DOT) && warp >= 1) {  // warp 0 runs the decision below meanwhile
+      if (p.world > 1)
+        col_reduce_global(P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
+      else
+        col_reduce(0, P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
+    }
 
     // ------------------------------ decision ------------------------------
     if (tid == 0) {
@@ -2228,7 +2418,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
     // --------------------- column reduction: t' = sgn(z) ---------------------
     if (prof && tid == 0) pacc[4] += clock64() - t_pass0;
   }
-  if (tid == 0) ctl->abort = 1;  // release a producer still waiting on an unconsumed stage
+  if (tid == 0) {
+    ctl->abort = 1;  // release a producer still waiting on an unconsumed stage
+    atomicAdd(p.stats + 5, phys);
+  }
   if (g == 0 && tid == 0) {
     p.stats[2] = dot_passes[0];
     p.stats[3] = dot_passes[1];
@@ -2248,11 +2441,20 @@ __device__ __forceinline__ void sweep_body(const KParams& p) {
 // which keeps their per-pass serial sections compact.
 template <typename E, int NW, int VPT, int RG, bool TS>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel(const KParams p) {
-  sweep_body<E, NW, VPT, RG, 1, TS>(p);
+  sweep_body<E, NW, VPT, RG, 1, TS>(p, blockIdx.x);
 }
 template <typename E, int NW, int VPT, int RG>
 __global__ void __maxnreg__(112) sweep_kernel2(const KParams p) {
-  sweep_body<E, NW, VPT, RG, 2, false>(p);
+  sweep_body<E, NW, VPT, RG, 2, false>(p, blockIdx.x);
+}
+// Row sharding emulated on one GPU (KParamsVR): CTA block r of the one
+// cooperative launch runs rank r's band with rank r's parameters and exchange
+// region; the code path is the multi-rank one (rank partials, bounded barriers).
+template <typename E, int NW, int VPT, int RG>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel_vr(const __grid_constant__ KParamsVR pv) {
+  const int G = pv.r[0].G;
+  const int rank = static_cast<int>(blockIdx.x) / G;
+  sweep_body<E, NW, VPT, RG, 1, false>(pv.r[rank], static_cast<int>(blockIdx.x) - rank * G);
 }
 
 

@@ -10,8 +10,9 @@ the objective happens inside the kernel, over peer memory, instead of as NCCL
 calls between kernel launches.  Every rank therefore holds the same t, α and
 curve; the row signs s are distributed like the rows and gathered at the end.
 
-C5 input (65536² f32): row block b (``C5_BLOCK`` rows) is drawn from
-``Xoshiro256pp(substream(4, b))`` so every rank generates only its own rows.
+C5 input (65536² f32): row block b of ``workloads.C5_BLOCK`` (1024) rows is drawn
+from ``Xoshiro256pp(substream(4, b))`` so every rank generates only its own rows
+(workloads.c5_rows, the single C5 generator).
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \\
         -m paper_2410_01799_b200.sharded --m 65536 --n 65536 --cuts 4
@@ -28,9 +29,6 @@ from typing import Callable, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _native as N
-
-C5_BLOCK = 256
-
 
 def bands(m: int, world: int) -> List[Tuple[int, int]]:
     """(row0, rows) of every rank: balanced contiguous bands (floor / ceil of m / world)."""
@@ -60,18 +58,25 @@ def assemble_signs(local_words: Sequence[np.ndarray], band_list: Sequence[Tuple[
     return out
 
 
-def c5_rows(row0: int, rows: int, n: int, base_seed: int = 4) -> np.ndarray:
-    """Rows [row0, row0+rows) of the C5 matrix (f32), generated block by block."""
-    from .api import fill_normal
-    from .batch import substream
+def c5_rows(row0: int, rows: int, n: int = 65536, base_seed: int = 4) -> np.ndarray:
+    """Rows [row0, row0+rows) of the C5 matrix (f32): the one generator, workloads.c5_rows."""
+    from .workloads import c5_rows as _c5
 
-    out = np.empty((rows, n), np.float32)
-    b0, b1 = row0 // C5_BLOCK, (row0 + rows - 1) // C5_BLOCK
-    for b in range(b0, b1 + 1):
-        blk = fill_normal(substream(base_seed, b), C5_BLOCK * n, np.float32).reshape(C5_BLOCK, n)
-        lo, hi = max(row0, b * C5_BLOCK), min(row0 + rows, (b + 1) * C5_BLOCK)
-        out[lo - row0: hi - row0] = blk[lo - b * C5_BLOCK: hi - b * C5_BLOCK]
-    return out
+    return _c5(row0, rows, n, seed=base_seed)
+
+
+def emulated(a, cfg, world: int, dtype: Optional[str] = None, ctas: int = 0, timeout_ms: int = 0,
+             dead_rank: int = -1, engine=None, want_remainder: bool = False):
+    """The row-sharded protocol with ``world`` virtual ranks on ONE GPU (one
+    cooperative launch over all ranks' bands; sc_greedy_decompose_sharded_emulated).
+    ``a`` is the whole matrix; returns the gathered (CutDecomposition, CutReport,
+    remainder) like Engine.run.  For testing the multi-rank exchange where fewer
+    GPUs than ranks are available."""
+    from .api import Engine
+
+    eng = engine or Engine(0)
+    opt = N.ScShardEmulation(world, ctas, timeout_ms, dead_rank)
+    return eng.run(a, cfg, dtype=dtype, emulate=opt, want_remainder=want_remainder)
 
 
 class ShardedEngine:
@@ -80,7 +85,7 @@ class ShardedEngine:
 
     def __init__(self, m_global: int, n: int, dtype: str = "f32", rank: int = 0, world: int = 1,
                  device: Optional[int] = None, allgather: Optional[Callable] = None,
-                 barrier: Optional[Callable] = None, ctas: int = 0):
+                 barrier: Optional[Callable] = None, ctas: int = 0, timeout_ms: int = 0):
         from .api import Engine
 
         self.m_global, self.n, self.dtype, self.rank, self.world = m_global, n, dtype, rank, world
@@ -89,7 +94,7 @@ class ShardedEngine:
         self._allgather = allgather or (lambda x: [x])
         self._barrier = barrier or (lambda: None)
         self.cfg = N.ScShardConfig(rank, world, m_global, self.band[0], n,
-                                   N.SC_F32 if dtype == "f32" else N.SC_F64, ctas)
+                                   N.SC_F32 if dtype == "f32" else N.SC_F64, ctas, timeout_ms)
         h = C.create_string_buffer(N.SC_IPC_HANDLE_BYTES)
         self.eng._check(self.eng.lib.sc_shard_open(self.eng.handle, C.byref(self.cfg), h))
         handles = self._allgather(h.raw)  # rank order

@@ -86,13 +86,21 @@ def c3_blob_image(height: int = 4000, width: int = 3000, blobs: int = 8, seed: i
     return np.clip(img, 0.0, 1.0).astype(np.float32)
 
 
-def c5_rows(row0: int, rows: int, n: int = 65536, block: int = 1024, seed: int = 4) -> np.ndarray:
-    """Rows [row0, row0 + rows) of C5 (row0, rows multiples of the block)."""
+C5_BLOCK = 1024
+
+
+def c5_rows(row0: int, rows: int, n: int = 65536, block: int = C5_BLOCK, seed: int = 4) -> np.ndarray:
+    """Rows [row0, row0 + rows) of C5 (any range): row block b of ``block`` rows is
+    fill_normal(substream(seed, b)), so ranks generate only their own bands."""
     out = np.empty((rows, n), np.float32)
-    for b in range(rows // block):
-        gb = row0 // block + b
-        out[b * block:(b + 1) * block] = fill_normal(substream(seed, gb), block * n, np.float32).reshape(block, n)
+    if rows <= 0:
+        return out
+    b0, b1 = row0 // block, (row0 + rows - 1) // block
+    for b in range(b0, b1 + 1):
+        lo, hi = max(row0, b * block), min(row0 + rows, (b + 1) * block)
+        blk = fill_normal(substream(seed, b), (hi - b * block) * n, np.float32).reshape(-1, n)
+        out[lo - row0: hi - row0] = blk[lo - b * block:]
     return out
 
 
-__all__ = ["Xoshiro256pp", "c1", "c2", "c3_blob_image", "c5_rows", "mix64", "substream"]
+__all__ = ["C5_BLOCK", "Xoshiro256pp", "c1", "c2", "c3_blob_image", "c5_rows", "mix64", "substream"]

@@ -33,11 +33,15 @@ def test_assemble_signs_ragged_bands():
 
 
 def test_c5_rows_are_the_block_seeded_stream(orc):
-    n = 40
-    full = np.concatenate([orc.fill_normal(orc.substream(4, b), sharded.C5_BLOCK * n).astype(np.float32)
-                           .reshape(sharded.C5_BLOCK, n) for b in range(3)])
-    for r0, rows in [(0, 10), (250, 20), (300, 400), (511, 257)]:
+    """One C5 generator (workloads.c5_rows, 1024-row blocks), any row range."""
+    from paper_2410_01799_b200 import workloads
+
+    n, B = 40, workloads.C5_BLOCK
+    full = np.concatenate([orc.fill_normal(orc.substream(4, b), B * n).astype(np.float32)
+                           .reshape(B, n) for b in range(3)])
+    for r0, rows in [(0, 10), (250, 20), (300, 1400), (1023, 1025), (2047, 1)]:
         assert np.array_equal(sharded.c5_rows(r0, rows, n), full[r0:r0 + rows])
+        assert np.array_equal(workloads.c5_rows(r0, rows, n), full[r0:r0 + rows])
 
 
 def _free_port():
