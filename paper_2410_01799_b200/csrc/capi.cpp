@@ -534,6 +534,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   // Sparse delta passes between dense refreshes (matrices, any row length: the dz of
   // flipped rows walks every column chunk).
   kp.delta = static_cast<int>(env_size("SCB_DELTA", 1));
+  kp.fuse_update = static_cast<int>(env_size("SCB_FUSE_UPDATE", 1));
   kp.delta_div = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_DIV", 32)));
   kp.delta_refresh = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_REFRESH", 64)));
   // Dot-pass form: the two-phase pass reads R twice per sweep but has no per-row
@@ -554,6 +555,8 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
     kp.rslot_pe[r] = sh ? reinterpret_cast<scb::Slot*>(ex + sh->off_rslot) : nullptr;
     kp.tb64_pe[r] = sh ? reinterpret_cast<unsigned long long*>(ex + sh->off_tb64) : tb64;
   }
+  kp.zr_own = kp.zr_pe[kp.rank];
+  kp.rslot_own = kp.rslot_pe[kp.rank];
   kp.bar_local = ctr + 5;  // this rank's own counter
   kp.abort_word = ctr_g + 6;
   kp.timeout_ns = static_cast<long long>(sh && sh->timeout_ms ? sh->timeout_ms : 30000u) * 1000000ll;
@@ -723,7 +726,34 @@ sc_status finish_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, RunState&
   res->passes = h_stats[1];
   res->dense_passes = h_stats[2];
   res->delta_passes = h_stats[3];
-  res->device_bytes = h_stats[5];
+  {
+    // Bytes the kernel moved through L2 / HBM, from the pass counts and the kernel's
+    // traffic counters (SMEM-resident rows are on chip and not counted): streamed
+    // rows per read (two-phase dot passes read twice), rank-1 write-backs, delta
+    // gathers at 32-byte sectors (flipped columns x streamed rows) plus the flipped
+    // streamed rows, and the column-partial rows written and read by the owners.
+    const scb::KParams& kp = S.kp;
+    uint64_t srows = 0, rrows = 0;
+    for (int g = 0; g < kp.G; ++g) {
+      const uint64_t rg = static_cast<uint64_t>(kp.rows_base + (g < kp.rows_rem ? 1 : 0));
+      const uint64_t nr = std::min<uint64_t>(rg, static_cast<uint64_t>(kp.res_rows));
+      rrows += nr;
+      srows += rg - nr;
+    }
+    const double sb = static_cast<double>(srows) * rowB, zb = static_cast<double>(kp.pitch) * 8.0;
+    const uint64_t dense = h_stats[2], delta = h_stats[3], maint = h_stats[1] - dense - delta;
+    const uint64_t upd_terms = wd == 0 ? 0 : std::min<uint64_t>(wd, static_cast<uint64_t>(w) - 1);
+    const uint64_t fused = kp.fuse_update ? upd_terms : 0;
+    const uint64_t maint_upd = (kp.fuse_update ? 0 : upd_terms) + (wd == w && wd > 0 ? 1 : 0);
+    double bytes = 0.0;
+    bytes += static_cast<double>(dense - fused) * (sb * (kp.two_phase ? 2.0 : 1.0) + 2.0 * zb * kp.G);
+    bytes += static_cast<double>(fused) * (sb * 3.0 + 2.0 * zb * kp.G);
+    bytes += static_cast<double>(maint) * sb + static_cast<double>(maint_upd) * sb + static_cast<double>(rrows) * rowB;
+    bytes += static_cast<double>(h_stats[7]) * static_cast<double>(srows) * 32.0 +
+             static_cast<double>(h_stats[5]) * rowB + static_cast<double>(h_stats[6]) * 2.0 * zb;
+    if (kp.world > 1) bytes += static_cast<double>(dense + delta) * 2.0 * zb;  // rank partials
+    res->device_bytes = static_cast<uint64_t>(bytes);
+  }
   if (wd > 0) {
     SC_CUDA(ctx, cudaMemcpyAsync(res->sign_words[0], S_out, wd * wm * 8, cudaMemcpyDeviceToHost, st));
     if (!tensor) {

@@ -12,7 +12,7 @@ namespace scb {
 // producer through shared memory.
 enum PassFlags : int {
   F_DOT = 1,     // y = R t, s' = sgn(y), z = R^T s', c = <s, y>
-  F_UPD = 2,     // R -= alpha s t^T applied while streaming (fused rank-1 update)
+  F_UPD = 2,     // R -= alpha s t^T applied while streaming (with F_DOT: fused into the term's first dot pass)
   F_NORM = 4,    // ||R||_F^2 accumulated (f64)
   F_WB = 8,      // write SMEM-resident rows back to global (end of run)
   F_CHECK = 16,  // reject non-finite input values (first pass)
@@ -37,6 +37,16 @@ constexpr int kMaxStages = 16;
 // those few lines hash to ("Placement of the exchange words").
 constexpr int kTbStride = 16;
 
+// Operands of the rank-1 update fused into a term's first dot pass (written by
+// thread 0 at the pass's staging; read by the dot pass from shared memory).
+struct UpdArgs {
+  double alpha;
+  void* Rband;      // global row 0 of the CTA's band
+  long long pitch;
+  int n;
+  unsigned uws, s_upd;  // smem offsets: t of the update (Q words), s of the update (band words)
+};
+
 // Per-CTA controller block in shared memory.
 struct Ctl {
   unsigned long long full[kMaxStages];   // TMA -> dot warps
@@ -45,6 +55,8 @@ struct Ctl {
   volatile int stored;   // global-R writes of passes [0, stored) are complete
   volatile int abort;
   volatile int aborted;  // world > 1: a cross-rank spin of this CTA timed out / saw the abort word
+  volatile int upd_done;  // fused-update dot pass P: phase A's write-back is complete (P + 1)
+  UpdArgs ua;
   volatile int kind_ring[4];
   // controller state (thread 0 writes, consumers read after a named barrier)
   int kind, pp, term, restart, tsel, utsel, best_tsel, best_sweeps, best_restart;
@@ -56,7 +68,7 @@ struct Ctl {
                         // recounted by the axial step for the next pass's t (read by the decision)
   int since_dense;      // delta passes since the last dense dot pass
   int has_dz;           // this CTA wrote a z partial in a delta pass
-  int nfrows;           // this CTA's flipped streamed rows in the last delta pass
+  int nfrows, ndz;      // run totals: flipped streamed rows read by delta passes, dz partials written
   int keep;             // t unchanged since the last dot pass: y, s, z stay exactly as cached
   unsigned rank_dz;     // world > 1: ranks whose rank partial holds a delta-pass dz
   double cred[64];  // per-warp partials (axial step: 4 outputs x up to 16 warps)
@@ -93,8 +105,8 @@ struct KParams {
   uint32_t* sweeps_out;  // [width]
   double* norm2_out;   // [width + 1]: [0] = ||A||^2, [k+1] = ||R after term k||^2
   unsigned long long* stats;  // [0] width_done, [1] passes, [2]/[3] dense/delta dot passes, [4] term 0's winning restart,
-                              // [5] bytes moved through L2 / HBM by the kernel (R streaming, delta gathers,
-                              //     rank-1 update writes, column-partial exchange)
+                              // traffic counters: [5] flipped streamed rows read by delta passes, [6] delta
+                              //     dz partials written, [7] t flips summed over delta passes (CTA 0)
   double* sweep_vals;  // [restarts][max_sweeps] c of every sweep of term 0 (SearchDiagnostics) or nullptr
   long long width, restarts, max_sweeps;
   double min_frac;
@@ -113,6 +125,7 @@ struct KParams {
   double* zfull;       // [pitch] reduced z (order-k mode)
   int two_phase;       // 1: dot pass as (A) y = R t, (B) z = R^T s' (rows streamed twice)
   int delta;           // 1: sparse delta passes between dense refreshes (matrix mode)
+  int fuse_update;     // 1: the rank-1 update rides on the next term's first dot pass (else its own pass)
   int delta_div;       // delta pass only if the last sweep flipped <= n / delta_div columns
   int delta_refresh;   // dense refresh every delta_refresh sweeps
   double* zstate;      // [pitch] z = R^T s of the previous pass (owners' columns)
@@ -130,6 +143,8 @@ struct KParams {
   int world, rank, GT;
   double* zr_pe[8];                  // per-rank [2][pitch] rank column partials (by pass parity)
   Slot* rslot_pe[8];                 // per-rank rank slot (c, ||R||^2, any dz), by pass parity
+  double* zr_own;                    // = zr_pe[rank]
+  Slot* rslot_own;                   // = rslot_pe[rank]
   unsigned long long* tb64_pe[8];    // per-rank [2][Q] tagged t words (owners write all)
   unsigned* bar_local;               // this rank's local barrier counter (world > 1)
   unsigned* abort_word;              // rank 0's: set by any CTA whose spin timed out (world > 1)

@@ -306,6 +306,14 @@ struct DotArgs {
   int wmul;  // 1 << 29 (run-time value)
   unsigned long long* prof;  // [4] thread-0 cycle sums (SCB_PROFILE builds): stage waits, A, B, C
   int cpr, chunk_cols;       // wide rows: column chunks per row (stage = one chunk)
+  // Fused rank-1 update (the first dot pass of a term, north-star kernel 3): before
+  // its dot, every row is deflated R -= alpha s t^T with the previous term's (s, t)
+  // (flush_pending with one term, decompose.hpp:200-214) and written back (resident
+  // rows in SMEM, streamed rows to global R); ||R_new||^2 is accumulated.  The
+  // update's operands sit in shared memory (Ctl::ua; DotArgs stays small enough to
+  // be passed in registers).
+  int upd;                   // 1: apply the update in phase A
+  unsigned ctl;              // smem offset of the Ctl block
 #ifdef SCB_TIMING
   unsigned long long* tprof;  // [blocks][warps][8] section cycle sums (dotbench only)
 #endif
@@ -645,8 +653,29 @@ __device__ __noinline__ void dot_pass(const DotArgs a) {
 // (C) z = R^T s' streams the rows again (SMEM-resident ones from SMEM, the rest
 // re-streamed by the producer) as a pure accumulate.  Rows are read twice, but
 // they live in SMEM / L2; what this removes is the per-row serial chain.
+// Deflation of one loaded row segment by the previous term (fused update): the
+// reference's flush arithmetic data += flip(-alpha, s_i ^ t_j), rounded to the
+// storage type, on the columns < n; returns the segment's ||.||^2 contribution.
+template <typename E, int EPV, int VPT>
+__device__ __forceinline__ double deflate(E* x, const uint32_t* um, uint32_t sneg, double alpha, const int* colv,
+                                          const bool* vok, int n) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    if (!vok[k]) continue;
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) {
+      const int i = k * EPV + e;
+      if (colv[k] + e < n) x[i] = Vec<E>::narrow(static_cast<double>(x[i]) + flipd(-alpha, sneg ^ um[i]));
+      const double d = static_cast<double>(x[i]);
+      acc += d * d;
+    }
+  }
+  return acc;
+}
+
 template <typename E, int NW, int VPT, bool FULL>
-__device__ __forceinline__ void dot_pass_2ph_impl(const DotArgs& a) {
+__device__ __forceinline__ double dot_pass_2ph_impl(const DotArgs& a) {
   constexpr int EPV = Vec<E>::N;
   constexpr int NE = VPT * EPV;
   using VT = typename Vec<E>::T;
@@ -684,6 +713,39 @@ __device__ __forceinline__ void dot_pass_2ph_impl(const DotArgs& a) {
   uint32_t fm[NE];
 #pragma unroll
   for (int i = 0; i < NE; ++i) fm[i] = bitmask(tbits, i);
+  // fused update: the update's t bits of the owned columns, and their columns
+#ifdef SCB_NO_FUSE
+  const bool upd = false;
+#else
+  const bool upd = a.upd != 0;
+#endif
+  Ctl* ctl = reinterpret_cast<Ctl*>(smem + a.ctl);
+  const UpdArgs& ua = ctl->ua;
+  uint32_t um[NE];
+  int colv[VPT];
+  double nacc = 0.0;
+  {
+    const uint32_t* uws = reinterpret_cast<const uint32_t*>(smem + ua.uws);
+    uint32_t ub = 0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      colv[k] = vidx[k] * EPV;
+      if (upd && vok[k]) ub |= ((uws[colv[k] >> 5] >> (colv[k] & 31)) & ((1u << EPV) - 1u)) << (k * EPV);
+    }
+#pragma unroll
+    for (int i = 0; i < NE; ++i) um[i] = bitmask(ub, i);
+  }
+  const uint32_t* s_upd = reinterpret_cast<const uint32_t*>(smem + ua.s_upd);
+  // phase A: deflate the loaded row (when fused) and write it back where it lives
+  auto upd_row = [&](int j, const VT* rp, E (&x)[NE]) {
+    const uint32_t sneg = ((s_upd[j >> 5] >> (j & 31)) & 1u) << 31;
+    nacc += deflate<E, EPV, VPT>(x, um, sneg, ua.alpha, colv, vok, ua.n);
+    VT* dst = j < nres ? const_cast<VT*>(rp)
+                       : reinterpret_cast<VT*>(static_cast<E*>(ua.Rband) + static_cast<size_t>(j) * ua.pitch);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k)
+      if (vok[k]) dst[vidx[k]] = Vec<E>::join(&x[k * EPV]);
+  };
 
   long long twait = 0;
   auto rowptr = [&](int j, int& sl) -> const VT* {
@@ -748,6 +810,11 @@ __device__ __forceinline__ void dot_pass_2ph_impl(const DotArgs& a) {
     E x0[NE], x1[NE];
     ld(p0, x0);
     ld(p1, x1);
+    if (upd) {
+      upd_row(j, p0, x0);
+      upd_row(j + 1, p1, x1);
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // before the stages go back to the TMA producer
+    }
     double v0 = partial(x0), v1 = partial(x1);
     release(s0);
     release(s1);
@@ -767,13 +834,19 @@ __device__ __forceinline__ void dot_pass_2ph_impl(const DotArgs& a) {
     const VT* p0 = rowptr(j, s0);
     E x0[NE];
     ld(p0, x0);
+    if (upd) {
+      upd_row(j, p0, x0);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     double v0 = partial(x0);
     release(s0);
     v0 = warp_sum(v0);
     if (lane == 0) ypart[j * NW + warp] = v0;
   }
   const long long tB = clock64();
+  if (upd) __threadfence();
   consumer_sync(NW * 32);
+  if (upd && tid == 0) ctl->upd_done = a.P + 1;  // the producer may now stream the updated rows for (C)
   // ---- (B) y and s' of every row, fixed warp order ----
   for (int jb = 0; jb < rows_g; jb += NW * 32) {
     const int jj = jb + tid;
@@ -846,19 +919,21 @@ __device__ __forceinline__ void dot_pass_2ph_impl(const DotArgs& a) {
         __stcg(reinterpret_cast<double2*>(a.zrow + vidx[k] * EPV + e), make_double2(zacc[k * EPV + e], zacc[k * EPV + e + 1]));
     }
   }
+  return nacc;
 }
 
+// Returns this thread's ||R_new||^2 contribution (fused update passes; else 0).
 template <typename E, int NW, int VPT>
-__device__ __noinline__ void dot_pass_2ph(const DotArgs a) {
+__device__ __noinline__ double dot_pass_2ph(const DotArgs a) {
   // warp-uniform: does every vector this warp owns lie inside the row?
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   bool full = true;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) full = full && ((k * NW + warp) * 32 + lane) < a.NV;
   if (__all_sync(0xffffffffu, full))
-    dot_pass_2ph_impl<E, NW, VPT, true>(a);
+    return dot_pass_2ph_impl<E, NW, VPT, true>(a);
   else
-    dot_pass_2ph_impl<E, NW, VPT, false>(a);
+    return dot_pass_2ph_impl<E, NW, VPT, false>(a);
 }
 // ---------------------------------------------------------------------------
 // Wide rows (cpr > 1): the two-phase pass over column chunks.  Every (row,
@@ -913,11 +988,24 @@ struct PieceCursor {
 
 // phase A over one chunk: every row's partial against this chunk's t, reduced in
 // the warp and accumulated into ypart[j][warp]
-template <typename E, int NW, int VPT, bool FULL>
+// Fused update (DotArgs::upd) of the chunk's pieces: deflate, write back to global R.
+struct ChunkUpd {
+  const uint32_t* s_upd;
+  const uint32_t* um;  // [NE] update t masks of this chunk's owned columns
+  const int* colv;     // [VPT] first column of each owned vector
+  double alpha;
+  void* Rband;
+  long long pitch;
+  int n, vbase;        // vbase: first vector of the chunk within the row
+  double nacc;
+};
+
+template <typename E, int NW, int VPT, bool FULL, bool UPD>
 __device__ __forceinline__ void chunk_dot(PieceCursor& cur, int rows_g, int k, unsigned toff, const int (&vloc)[VPT],
                                           const bool (&vok)[VPT], const uint32_t (&fm)[VPT * Vec<E>::N],
-                                          double* ypart) {
+                                          double* ypart, ChunkUpd& cu) {
   using VT = typename Vec<E>::T;
+  constexpr int EPV = Vec<E>::N;
   constexpr int NE = VPT * Vec<E>::N;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   auto partial = [&](const E (&x)[NE]) -> double {
@@ -931,6 +1019,15 @@ __device__ __forceinline__ void chunk_dot(PieceCursor& cur, int rows_g, int k, u
     const VT* rp = reinterpret_cast<const VT*>(cur.next(sl));
     E x[NE];
     ld_piece<E, NW, VPT, FULL>(rp, toff, vloc, vok, x);
+    if constexpr (UPD) {
+      const uint32_t sneg = ((cu.s_upd[j >> 5] >> (j & 31)) & 1u) << 31;
+      cu.nacc += deflate<E, EPV, VPT>(x, cu.um, sneg, cu.alpha, cu.colv, vok, cu.n);
+      VT* dst = reinterpret_cast<VT*>(static_cast<E*>(cu.Rband) + static_cast<size_t>(j) * cu.pitch) + cu.vbase;
+#pragma unroll
+      for (int q = 0; q < VPT; ++q)
+        if (vok[q]) dst[vloc[q]] = Vec<E>::join(&x[q * EPV]);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     double v = partial(x);
     cur.release(sl);
     v = warp_sum(v);
@@ -969,7 +1066,7 @@ __device__ __forceinline__ void chunk_z(PieceCursor& cur, int rows_g, unsigned t
 }
 
 template <typename E, int NW, int VPT>
-__device__ __noinline__ void dot_pass_chunked(const DotArgs a) {
+__device__ __noinline__ double dot_pass_chunked(const DotArgs a) {
   constexpr int EPV = Vec<E>::N;
   constexpr int NE = VPT * EPV;
   constexpr int chunkV = NW * 32 * VPT;  // vectors per chunk
@@ -995,24 +1092,47 @@ __device__ __noinline__ void dot_pass_chunked(const DotArgs a) {
     }
     return __all_sync(0xffffffffu, ok);
   };
-  // ---- (A) y partials, chunk-major ----
+  // ---- (A) y partials, chunk-major (fused update: deflate + write back first) ----
+  Ctl* ctl = reinterpret_cast<Ctl*>(smem + a.ctl);
+  const UpdArgs& ua = ctl->ua;
+  const uint32_t* uws = reinterpret_cast<const uint32_t*>(smem + ua.uws);
+  ChunkUpd cu{reinterpret_cast<const uint32_t*>(smem + ua.s_upd), nullptr, nullptr, ua.alpha, ua.Rband, ua.pitch,
+              ua.n, 0, 0.0};
   for (int k = 0; k < cpr; ++k) {
     const bool full = setup(k);
-    uint32_t tbits = 0;
+    uint32_t tbits = 0, ub = 0;
+    int colv[VPT];
 #pragma unroll
     for (int q = 0; q < VPT; ++q) {
       const int col0 = (k * chunkV + vloc[q]) * EPV;
+      colv[q] = col0;
       if (vok[q]) tbits |= ((tws[col0 >> 5] >> (col0 & 31)) & ((1u << EPV) - 1u)) << (q * EPV);
+      if (a.upd && vok[q]) ub |= ((uws[col0 >> 5] >> (col0 & 31)) & ((1u << EPV) - 1u)) << (q * EPV);
     }
-    uint32_t fm[NE];
+    uint32_t fm[NE], um[NE];
 #pragma unroll
-    for (int i = 0; i < NE; ++i) fm[i] = bitmask(tbits, i);
-    if (full)
-      chunk_dot<E, NW, VPT, true>(cur, rows_g, k, toff, vloc, vok, fm, ypart);
-    else
-      chunk_dot<E, NW, VPT, false>(cur, rows_g, k, toff, vloc, vok, fm, ypart);
+    for (int i = 0; i < NE; ++i) {
+      fm[i] = bitmask(tbits, i);
+      um[i] = bitmask(ub, i);
+    }
+    cu.um = um;
+    cu.colv = colv;
+    cu.vbase = k * chunkV;
+    if (a.upd) {
+      if (full)
+        chunk_dot<E, NW, VPT, true, true>(cur, rows_g, k, toff, vloc, vok, fm, ypart, cu);
+      else
+        chunk_dot<E, NW, VPT, false, true>(cur, rows_g, k, toff, vloc, vok, fm, ypart, cu);
+    } else {
+      if (full)
+        chunk_dot<E, NW, VPT, true, false>(cur, rows_g, k, toff, vloc, vok, fm, ypart, cu);
+      else
+        chunk_dot<E, NW, VPT, false, false>(cur, rows_g, k, toff, vloc, vok, fm, ypart, cu);
+    }
   }
+  if (a.upd) __threadfence();
   consumer_sync(NW * 32);
+  if (a.upd && tid == 0) ctl->upd_done = P + 1;  // the producer may now stream the updated pieces for (C)
   // ---- (B) y and s' of every row, fixed warp order ----
   for (int jb = 0; jb < rows_g; jb += NW * 32) {
     const int jj = jb + tid;
@@ -1043,6 +1163,7 @@ __device__ __noinline__ void dot_pass_chunked(const DotArgs a) {
     else
       chunk_z<E, NW, VPT, false>(cur, rows_g, toff, vloc, vok, s_nxt, zc);
   }
+  return cu.nacc;
 }
 
 // ---------------------------------------------------------------------------
@@ -1061,7 +1182,7 @@ struct DeltaArgs {
   double* zrow;       // this CTA's z partial row of this pass
   unsigned* errp;
   int* has_dz;
-  int* nfrows;        // flipped rows read from global memory (streamed rows; byte accounting)
+  int* nfrows;        // [2] run totals: flipped streamed rows read from global, dz partials written
   long long pitch;
   unsigned rowB;
   int rows_g, nres, Q, NV, P;
@@ -1299,7 +1420,8 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
   }
   if (tid == 0) {
     *a.has_dz = any ? 1 : 0;
-    *a.nfrows = nfg;
+    a.nfrows[0] += nfg;       // totals over the run (traffic accounting)
+    a.nfrows[1] += any ? 1 : 0;
   }
 }
 
@@ -1575,6 +1697,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     ctl->stored = 0;
     ctl->abort = 0;
     ctl->aborted = 0;
+    ctl->upd_done = 0;
     ctl->rank_dz = 0;
     ctl->pp = TS ? 1 : 0;  // order-k: pp = sweep of the current pass (1-based)
     for (int j = 0; j < 8; ++j) {  // read by the axial step from shared memory, not the param copy
@@ -1583,6 +1706,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     }
     ctl->kron_upd = 0;
     ctl->nflip = 0;
+    ctl->nfrows = 0;
+    ctl->ndz = 0;
     ctl->since_dense = 0;
     ctl->has_dz = 0;
     ctl->keep = 0;
@@ -1638,9 +1763,17 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         }
         // the two-phase dot pass reads the streamed rows twice (y, then z); wide
         // rows go as column chunks, chunk-major in dot passes, row-major otherwise
-        const bool dotp = (kind & F_DOT) && p.two_phase;
+        // (the first dot pass of a term carries the fused rank-1 update: always two-phase)
+        const bool dotp = (kind & F_DOT) && (p.two_phase || (kind & F_UPD));
         const int reps = (kind & F_DELTA) ? 0 : (dotp ? 2 : 1);  // delta passes stream nothing
         for (int rep = 0; rep < reps; ++rep) {
+          if (rep == 1 && (kind & F_UPD)) {  // phase C re-reads rows that phase A rewrote
+            while (ctl->upd_done <= P) {
+              if (ctl->abort) goto drain;
+              __nanosleep(32);
+            }
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
           int row = 0, chunk = 0;  // piece cursor: chunk-major in dot passes, row-major otherwise
           for (int idx = 0; idx < npieces; ++idx, ++q) {
             const int s = ps;
@@ -1696,7 +1829,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
   unsigned epoch = 0;      // grid barriers passed (thread 0)
   unsigned lepoch = 0;     // rank-local barriers passed (thread 0, world > 1)
   unsigned long long dot_passes[2] = {0, 0};  // CTA 0: dense, delta dot passes (-> stats[2], [3])
-  unsigned long long phys = 0;  // thread 0: bytes this CTA moved through L2 / HBM (-> stats[5])
+  unsigned long long nflip_sum = 0;  // CTA 0, thread 32: t flips over the delta passes (-> stats[7])
   int vidx[VPT];           // owned vectors (clamped to a valid address when out of range)
   bool vok[VPT];
 #pragma unroll
@@ -1762,7 +1895,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         for (int w = 0; w < NP; ++w) z += zseg[(j * CW + w) * 32 + lane];
         const bool valid = col < p.n;
         if (mode == 2) {  // rank partial: combined and checked by the global owners
-          if (valid) __stcg(p.zr_pe[p.rank] + static_cast<size_t>(P & 1) * pitch + col, z);
+          if (valid) __stcg(p.zr_own + static_cast<size_t>(P & 1) * pitch + col, z);
           continue;
         }
         if (zstate_here && valid) {  // z state for delta passes: dense sets it, delta adds to it
@@ -1827,8 +1960,13 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       }
       if (valid && !isfinite(z)) atomicMin(const_cast<unsigned*>(errp) + ERR_Z, static_cast<unsigned>(P));
       const unsigned word = __ballot_sync(0xffffffffu, valid && z < 0.0);
-      if (lane < p.world)  // every rank stages t from its own copy
-        st_relaxed64_sys(p.tb64_pe[lane] + (static_cast<size_t>(tbuf) * p.Q + qq) * kTbStride, tag | word);
+      // every rank stages t from its own copy (lane r stores rank r's; constant-index
+      // selects keep the kernel-parameter tables out of local memory)
+      unsigned long long* dst = nullptr;
+#pragma unroll
+      for (int r = 0; r < kMaxVRanks; ++r)
+        if (lane == r) dst = p.tb64_pe[r];
+      if (lane < p.world) st_relaxed64_sys(dst + (static_cast<size_t>(tbuf) * p.Q + qq) * kTbStride, tag | word);
     }
   };
 
@@ -1894,6 +2032,14 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       if (tid == 0)
         for (int i = 0; i < p.sw; ++i) s_nxt[i] = 0u;
     }
+    if ((kind & F_UPD) && (kind & F_DOT) && tid == 0) {  // operands of the fused update (smem)
+      ctl->ua.uws = static_cast<unsigned>(L.uws);
+      ctl->ua.s_upd = static_cast<unsigned>(reinterpret_cast<const unsigned char*>(s_upd) - smem);
+      ctl->ua.alpha = alpha;
+      ctl->ua.Rband = R + static_cast<size_t>(r0) * pitch;
+      ctl->ua.pitch = pitch;
+      ctl->ua.n = p.n;
+    }
     if ((kind & F_UPD) && !TS) {  // order-k: uws = kron(best axes), built at term accept
       for (int i = tid; i < p.Q; i += CT)
         uws[i] = ctl->utsel == 2 ? __ldcg(p.tbest + i)
@@ -1901,6 +2047,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     }
     consumer_sync(CT);
     if (p.world > 1 && ctl->aborted) break;  // uniform: set before the barrier
+    if (g == 0 && tid == 32 && (kind & F_DELTA)) nflip_sum += static_cast<unsigned>(ctl->nflip);
     if (prof && tid == 0) pacc[5] += clock64() - t_pass0;
     // A sweep whose t equals the previous pass's t is a fixed point of the cached
     // products: y, s' and z stay exactly as cached whatever pass form runs, so a
@@ -1942,6 +2089,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       da.prof = prof ? prof + g * 16 + 8 : nullptr;
       da.cpr = p.cpr;
       da.chunk_cols = p.chunk_cols;
+      da.upd = (kind & F_UPD) ? 1 : 0;
+      da.ctl = static_cast<unsigned>(L.ctl);
       if (kind & F_DELTA) {
         DeltaArgs dl;
         dl.res = static_cast<unsigned>(L.res);
@@ -1966,9 +2115,9 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         delta_pass<E, NW, VPT>(dl);
       } else if (p.cpr > 1) {
         da.rowB = static_cast<unsigned>(stageB);
-        dot_pass_chunked<E, NW, VPT>(da);
-      } else if (p.two_phase) {
-        dot_pass_2ph<E, NW, VPT>(da);
+        nacc += dot_pass_chunked<E, NW, VPT>(da);
+      } else if (p.two_phase || (kind & F_UPD)) {
+        nacc += dot_pass_2ph<E, NW, VPT>(da);
       } else {
         dot_pass<E, NW, VPT, RG, CPS>(da);
       }
@@ -2034,30 +2183,11 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       }
     }
     if (D > 0) {  // advance the stage ring past this pass's streamed rows
-      const int t = qs + npieces * ((kind & F_DELTA) ? 0 : (((kind & F_DOT) && p.two_phase) ? 2 : 1));
+      const int t = qs + npieces * ((kind & F_DELTA) ? 0 : (((kind & F_DOT) && (p.two_phase || (kind & F_UPD))) ? 2 : 1));
       qph ^= (t / D) & 1;
       qs = t % D;
     }
 
-    // Physical traffic of this pass (thread 0; R reads from SMEM-resident rows are on chip
-    // and not counted): streamed rows (twice for the two-phase pass), delta gathers at
-    // 32-byte sector granularity plus the flipped streamed rows, the rank-1 update's
-    // write-back, and the column-partial row this CTA stores.
-    if (tid == 0) {
-      const unsigned long long sbytes = static_cast<unsigned long long>(nstream) * rowB;
-      const unsigned long long zbytes = static_cast<unsigned long long>(pitch) * 8ull;
-      if (kind & F_DOT) {
-        if (kind & F_DELTA) {
-          phys += static_cast<unsigned long long>(ctl->nflip) * nstream * 32ull +
-                  static_cast<unsigned long long>(ctl->nfrows) * rowB + (ctl->has_dz ? zbytes : 0ull);
-        } else {
-          phys += sbytes * (p.two_phase ? 2ull : 1ull) + zbytes;
-        }
-      } else {
-        phys += sbytes * ((kind & F_UPD) ? 2ull : 1ull) +
-                ((kind & F_WB) ? static_cast<unsigned long long>(nres) * rowB : 0ull);
-      }
-    }
     // ------------------------------ pass end ------------------------------
     if (prof && tid == 0) {
       const long long t = clock64();
@@ -2140,14 +2270,6 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       }
     }
     consumer_sync(CT);
-    if (tid == 0 && g == 0 && (kind & F_DOT)) {  // owners' reads of the column partials (grid total)
-      unsigned long long parts = static_cast<unsigned long long>(G);
-      if (kind & F_DELTA) {
-        parts = 0;
-        for (int i = 0; i < 64; ++i) parts += __popc(dzmask[i]);
-      }
-      phys += (parts + (p.world > 1 ? 1ull : 0ull)) * static_cast<unsigned long long>(pitch) * 8ull;
-    }
     if (p.world > 1) {
       // Rank stage: this rank's column partials -> one rank partial zr (local
       // owners), its slots -> one rank slot; then the cross-rank barrier, after
@@ -2162,7 +2284,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         unsigned anydz = 0;
         for (int i = 0; i < 64; ++i) anydz |= dzmask[i];
         if (g == 0) {
-          Slot* rs = p.rslot_pe[p.rank];
+          Slot* rs = p.rslot_own;
           __stcg(&rs->c[P & 1], cs);
           __stcg(&rs->n[P & 1], ns);
           __stcg(&rs->dz[P & 1], ((kind & F_DELTA) && anydz) ? 1.0 : 0.0);
@@ -2180,8 +2302,11 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       if (ctl->aborted) break;
       if (warp == 0) {
         double c = 0.0, n2 = 0.0, dz = 0.0;
+        const Slot* rs = nullptr;
+#pragma unroll
+        for (int r = 0; r < kMaxVRanks; ++r)
+          if (lane == r) rs = p.rslot_pe[r];
         if (lane < p.world) {
-          const Slot* rs = p.rslot_pe[lane];
           c = __ldcg(&rs->c[P & 1]);
           n2 = __ldcg(&rs->n[P & 1]);
           dz = __ldcg(&rs->dz[P & 1]);
@@ -2281,7 +2406,13 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
             ctl->restart = 0;
             ctl->tsel = -1;
             ctl->c_prev = -INFINITY;
-            return F_UPD | F_NORM;  // deflate, then search the next term
+            // the next term's first dot pass deflates R by this term as it streams it
+            // (north-star kernel 3): sweeps + 1 passes per cut, no maintenance pass
+#ifdef SCB_NO_FUSE
+            return F_UPD | F_NORM;
+#else
+            return p.fuse_update ? (F_DOT | F_UPD | F_NORM) : (F_UPD | F_NORM);
+#endif
           }
         } else {
           // min_value_fraction stop (decompose.hpp:337-338): nothing appended
@@ -2420,8 +2551,11 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
   }
   if (tid == 0) {
     ctl->abort = 1;  // release a producer still waiting on an unconsumed stage
-    atomicAdd(p.stats + 5, phys);
+    // traffic counters (the host turns them into bytes, sc_result::device_bytes)
+    atomicAdd(p.stats + 5, static_cast<unsigned long long>(ctl->nfrows));
+    atomicAdd(p.stats + 6, static_cast<unsigned long long>(ctl->ndz));
   }
+  if (g == 0 && tid == 32) p.stats[7] = nflip_sum;
   if (g == 0 && tid == 0) {
     p.stats[2] = dot_passes[0];
     p.stats[3] = dot_passes[1];
