@@ -329,7 +329,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   const size_t rowB = static_cast<size_t>(pitch) * es;
   const size_t stageB = cpr > 1 ? static_cast<size_t>(tile_cols) * es : rowB;  // one row or one chunk
   auto smem_for = [&](int st_, int res_) {
-    return scb::make_layout(stageB, st_, res_, var.rg, var.nw, rows_max, Q, zl, sw, axw).total;
+    return scb::make_layout(stageB, st_, res_, var.rg, var.nw, rows_max, Q, zl, sw, axw, G).total;
   };
   // per-CTA shared memory: the opt-in maximum, or an even split of the SM's
   // 228 KB (minus the 1 KB the runtime reserves per CTA) when two CTAs share an SM
@@ -371,6 +371,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
                       ((nstart * axw64 * 8 + 255) & ~size_t(255)) +
                       ((std::max<uint64_t>(w, 1) * axw64 * 8 + 255) & ~size_t(255)) +
                       2 * ((static_cast<size_t>(pitch) * 8 + 255) & ~size_t(255)) +
+                      ((2 * static_cast<size_t>(G) * sw * 8 + 255) & ~size_t(255)) +
                       env_size("SCB_ARENA_SHIFT", 0) + env_size("SCB_SYNC_SHIFT", 0) + env_size("SCB_SLOT_SHIFT", 0) +
                       env_size("SCB_TB_SHIFT", 0) + env_size("SCB_ZS_SHIFT", 0);
   if (need > ctx->arena_bytes) {
@@ -416,6 +417,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   double* zfull = carve<double>(cur, static_cast<size_t>(pitch));
   cur += env_size("SCB_ZS_SHIFT", 0);
   double* zstate = carve<double>(cur, static_cast<size_t>(pitch));
+  unsigned long long* flipw = carve<unsigned long long>(cur, 2 * static_cast<size_t>(G) * sw);
 
   // ---- host staging (pinned) for the start vectors ----
   const size_t t0_bytes = nstart * wn * 8, ax0_bytes = nstart * axw64 * 8;
@@ -531,6 +533,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   kp.AX_out = reinterpret_cast<uint32_t*>(AX_out);
   kp.zfull = zfull;
   kp.zstate = zstate;
+  kp.flipw = flipw;
   // Sparse delta passes between dense refreshes (matrices, any row length: the dz of
   // flipped rows walks every column chunk).
   kp.delta = static_cast<int>(env_size("SCB_DELTA", 1));
@@ -566,8 +569,8 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   const bool prof = std::getenv("SCB_PROF") != nullptr;
   unsigned long long* dprof = nullptr;
   if (prof) {
-    SC_CUDA(ctx, cudaMalloc(&dprof, static_cast<size_t>(G) * 16 * 8));
-    SC_CUDA(ctx, cudaMemsetAsync(dprof, 0, static_cast<size_t>(G) * 16 * 8, st));
+    SC_CUDA(ctx, cudaMalloc(&dprof, static_cast<size_t>(G) * 24 * 8));
+    SC_CUDA(ctx, cudaMemsetAsync(dprof, 0, static_cast<size_t>(G) * 24 * 8, st));
   }
   kp.prof = dprof;
   // SearchDiagnostics::sweep_values of term 0, every restart (the host keeps the winner's)
@@ -653,8 +656,16 @@ sc_status finish_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, RunState&
   res->kernel_ms = kms;
   res->kernel_launches = 1;
   if (prof) {
-    std::vector<unsigned long long> hp(static_cast<size_t>(G) * 16);
+    std::vector<unsigned long long> hp(static_cast<size_t>(G) * 24);
     cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost);
+    {
+      double d[6] = {0, 0, 0, 0, 0, 0};
+      for (int g = 0; g < G; ++g)
+        for (int i = 0; i < 6; ++i) d[i] += static_cast<double>(hp[static_cast<size_t>(G) * 16 + g * 8 + i]);
+      const double nd = std::max<double>(1.0, static_cast<double>(h_stats[3])) * G;
+      std::fprintf(stderr, "[scb prof delta] per delta pass per CTA: fliplists %.0f gathers %.0f sync %.0f signs %.0f dz %.0f | CTAs with dz per pass %.2f\n",
+                   d[0] / nd, d[1] / nd, d[2] / nd, d[3] / nd, d[4] / nd, d[5] / std::max<double>(1.0, static_cast<double>(h_stats[3])));
+    }
     cudaFree(dprof);
     double acc[16] = {0};
     for (int g = 0; g < G; ++g)

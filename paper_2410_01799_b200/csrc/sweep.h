@@ -129,6 +129,7 @@ struct KParams {
   int delta_div;       // delta pass only if the last sweep flipped <= n / delta_div columns
   int delta_refresh;   // dense refresh every delta_refresh sweeps
   double* zstate;      // [pitch] z = R^T s of the previous pass (owners' columns)
+  unsigned long long* flipw;  // [2][G][sw] per-CTA (flip | s' << 32) words of a matrix delta pass, by parity
   // wide rows: every row is streamed as cpr column chunks of chunk_cols
   // elements (one stage each); cpr == 1, chunk_cols == pitch otherwise
   int cpr;
@@ -177,13 +178,15 @@ constexpr int kRing = 4;  // dot-partial ring depth (groups)
 
 // Shared-memory carve-up (byte offsets from the dynamic smem base).
 struct Layout {
-  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, ypart, txor, dzmask, ybak, zst, total;
+  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, ypart, txor, dzmask, ybak, zst, fws, fbuf, total;
 };
+
+constexpr int kFBuf = 64;  // per-warp flipped-row list entries (owners' delta-pass dz)
 
 inline __host__ __device__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
 inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_rows, int rg, int nw, int rows_max,
-                                              int Q, int zl, int sw, int axw = 0) {
+                                              int Q, int zl, int sw, int axw, int G) {
   Layout L;
   size_t o = 0;
   L.stage = o;
@@ -218,6 +221,10 @@ inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_r
   o += align16(static_cast<size_t>(rows_max) * 8);
   L.zst = o;  // [zl][32]: z state of the owner's column words (delta passes)
   o += static_cast<size_t>(zl) * 32 * 8;
+  L.fws = o;  // [G][sw]: every CTA's (flip | s' << 32) words of a matrix delta pass (owners)
+  o += static_cast<size_t>(G) * sw * 8;
+  L.fbuf = o;  // [nw][kFBuf]: per-warp flipped-row lists (owners)
+  o += static_cast<size_t>(nw) * kFBuf * 4;
   L.total = o;
   return L;
 }

@@ -740,11 +740,16 @@ __device__ __forceinline__ double dot_pass_2ph_impl(const DotArgs& a) {
   auto upd_row = [&](int j, const VT* rp, E (&x)[NE]) {
     const uint32_t sneg = ((s_upd[j >> 5] >> (j & 31)) & 1u) << 31;
     nacc += deflate<E, EPV, VPT>(x, um, sneg, ua.alpha, colv, vok, ua.n);
-    VT* dst = j < nres ? const_cast<VT*>(rp)
-                       : reinterpret_cast<VT*>(static_cast<E*>(ua.Rband) + static_cast<size_t>(j) * ua.pitch);
+    // global R stays current for every row (resident rows too: the owners of a delta
+    // pass read flipped rows from global memory); resident rows also in place in SMEM
+    VT* dst = reinterpret_cast<VT*>(static_cast<E*>(ua.Rband) + static_cast<size_t>(j) * ua.pitch);
+    VT* sdst = const_cast<VT*>(rp);
 #pragma unroll
     for (int k = 0; k < VPT; ++k)
-      if (vok[k]) dst[vidx[k]] = Vec<E>::join(&x[k * EPV]);
+      if (vok[k]) {
+        dst[vidx[k]] = Vec<E>::join(&x[k * EPV]);
+        if (j < nres) sdst[vidx[k]] = Vec<E>::join(&x[k * EPV]);
+      }
   };
 
   long long twait = 0;
@@ -1182,7 +1187,11 @@ struct DeltaArgs {
   double* zrow;       // this CTA's z partial row of this pass
   unsigned* errp;
   int* has_dz;
-  int* nfrows;        // [2] run totals: flipped streamed rows read from global, dz partials written
+  int* nfrows;        // [2] run totals: flipped rows read (from global), dz partials written
+  int local_dz;       // 1: this CTA forms the dz partial of its flipped rows (order-k mode); 0: it
+                      //    publishes its flip words and the column owners read the flipped rows
+  unsigned long long* flipw;  // [sw] this pass's (flip mask | s' << 32) words of the band (local_dz == 0)
+  unsigned long long* prof;  // SCB_PROFILE builds: [6] thread-0 cycle sums of the delta pass sections
   long long pitch;
   unsigned rowB;
   int rows_g, nres, Q, NV, P;
@@ -1203,6 +1212,12 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
   const uint32_t* tws = reinterpret_cast<const uint32_t*>(smem + a.tws);
   const uint32_t* txor = reinterpret_cast<const uint32_t*>(smem + a.txor);
   const E* Rg = static_cast<const E*>(a.Rrows);
+#ifdef SCB_PROFILE
+  long long dt0 = clock64();
+#define SCB_DT(k) do { if (a.prof && tid == 0) { const long long t1_ = clock64(); a.prof[k] += t1_ - dt0; dt0 = t1_; } } while (0)
+#else
+#define SCB_DT(k) do {} while (0)
+#endif
   auto row_ptr = [&](int j) -> const E* {
     return j < nres ? reinterpret_cast<const E*>(smem + a.res + static_cast<size_t>(j) * a.rowB)
                     : Rg + static_cast<size_t>(j) * a.pitch;
@@ -1232,6 +1247,7 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
       }
     }
   }
+  SCB_DT(0);  // flip lists
   // rows per warp per round trip: up to four, no more than the band needs
   const int rpg = rows_g > 2 * NW ? 4 : (rows_g > NW ? 2 : 1);
   const bool any_over = __any_sync(0xffffffffu, over);
@@ -1334,7 +1350,9 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
       }
     }
   }
+  SCB_DT(1);  // y gathers
   consumer_sync(NW * 32);
+  SCB_DT(2);  // sync
   // ---- s' = sgn(y) ----
   for (int jb = 0; jb < rows_g; jb += NW * 32) {
     const int jj = jb + tid;
@@ -1345,13 +1363,33 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
     if (lane == 0 && jb + warp * 32 < rows_g) s_nxt[(jb >> 5) + warp] = word;
   }
   consumer_sync(NW * 32);
+  SCB_DT(3);  // signs + sync
+  const int sw = (rows_g + 31) / 32;
+  if (!a.local_dz) {
+    // Matrix mode: publish (flipped rows, new signs) of the band; the owner of each
+    // 32-column word reads those rows of R after the grid barrier and adds
+    // 2 s'_i R[i, cols] to its z state.  No dz partial row here: the pass costs every
+    // CTA the same whatever its rows did (no arrival spread at the barrier).
+    int nf = 0;
+    for (int w = lane; w < sw; w += 32) {
+      uint32_t f = s_nxt[w] ^ s_cur[w];
+      if (w == sw - 1 && (rows_g & 31)) f &= (1u << (rows_g & 31)) - 1u;
+      if (warp == 0) __stcg(a.flipw + w, static_cast<unsigned long long>(f) | (static_cast<unsigned long long>(s_nxt[w]) << 32));
+      nf += __popc(f);
+    }
+    if (warp == 0) {
+      nf = static_cast<int>(warp_sum(static_cast<double>(nf)));
+      if (lane == 0) a.nfrows[0] += nf;  // flipped rows the owners read (traffic accounting)
+    }
+    SCB_DT(4);
+    return;
+  }
   // ---- dz over the rows whose sign flipped (ascending rows) ----
   // Rows wider than one warp tile (column chunks, cpr > 1) are covered chunk by
   // chunk: the flipped rows are read once per chunk, each chunk's partial stored.
   constexpr int chunkV = NW * 32 * VPT;
   bool any = false;
   int nfg = 0;  // flipped streamed rows (read from L2 / HBM), counted once
-  const int sw = (rows_g + 31) / 32;
   for (int ck = 0; ck < a.cpr; ++ck) {
     int vidx[VPT];
     bool vok[VPT];
@@ -1418,11 +1456,16 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
       }
     }
   }
+  SCB_DT(4);  // dz
   if (tid == 0) {
     *a.has_dz = any ? 1 : 0;
     a.nfrows[0] += nfg;       // totals over the run (traffic accounting)
     a.nfrows[1] += any ? 1 : 0;
+#ifdef SCB_PROFILE
+    if (a.prof && any) a.prof[5] += 1;
+#endif
   }
+#undef SCB_DT
 }
 
 // ---------------------------------------------------------------------------
@@ -1664,7 +1707,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
   // stage = one row, or one column chunk of a wide row (then no resident rows)
   const size_t stageB = p.cpr > 1 ? static_cast<size_t>(p.chunk_cols) * sizeof(E) : rowB;
   const int npieces = nstream * p.cpr;  // TMA pieces per streaming sweep over the band
-  const Layout L = make_layout(stageB, D, p.res_rows, RG, NW, p.rows_max, p.Q, p.zl, p.sw, p.axw);
+  const Layout L = make_layout(stageB, D, p.res_rows, RG, NW, p.rows_max, p.Q, p.zl, p.sw, p.axw, G);
   unsigned char* stage_base = smem + L.stage;
   unsigned char* res_base = smem + L.res;
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + L.ctl);
@@ -1678,6 +1721,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
   uint32_t* txor = reinterpret_cast<uint32_t*>(smem + L.txor);             // [Q] t ^ previous t
   uint32_t* tprev = txor + p.Q;                                            // [Q] previous pass's t
   uint32_t* dzmask = reinterpret_cast<uint32_t*>(smem + L.dzmask);         // [64] CTAs with a dz partial
+  unsigned long long* fws = reinterpret_cast<unsigned long long*>(smem + L.fws);  // [G][sw] flip words of the pass
+  uint32_t* fbuf = reinterpret_cast<uint32_t*>(smem + L.fbuf);             // [CW][kFBuf] flipped-row lists
   double* ybak = reinterpret_cast<double*>(smem + L.ybak);                 // [rows_max] cached y
   uint32_t* sax = reinterpret_cast<uint32_t*>(smem + L.ax);                // [axw] axes 1..k-1 (order-k)
   uint32_t* sax_best = sax + p.axw;                                        // [axw] best restart's
@@ -1850,6 +1895,52 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
   // triple's t lives in the other buffer).
   // Warps w0..CW-1 take part (w0 = 1: warp 0 runs the controller decision meanwhile
   // and the participants synchronise on named barrier 2).
+  // Matrix delta passes: the owner's dz for column `col` from the flipped rows of the
+  // rank's CTAs [gs, ge) (their flip words staged in fws after the barrier), read
+  // straight from R (row-major, current in global memory for every row):
+  // sum over flipped rows i, ascending, of 2 s'_i R[i, col].  A per-warp shared
+  // buffer lists up to kFBuf rows at a time so that 8 row loads are in flight.
+  auto flip_rows_sum = [&](int col, int gs, int ge, int lw) -> double {
+    uint32_t* buf = fbuf + lw * kFBuf;
+    const E* Rc = R + col;
+    double acc = 0.0;
+    auto drain = [&](int cnt) {
+      __syncwarp();
+      for (int k = 0; k < cnt; k += 8) {
+        E v[8];
+        uint32_t e[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          e[u] = (k + u < cnt) ? buf[k + u] : 0u;
+          v[u] = (k + u < cnt) ? __ldcg(Rc + static_cast<size_t>(e[u] & 0x7fffffffu) * pitch) : E(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (k + u < cnt) acc = fma(static_cast<double>(v[u]), (e[u] >> 31) ? -2.0 : 2.0, acc);
+      }
+      __syncwarp();
+    };
+    int nb = 0;
+    for (int gp = gs; gp < ge; ++gp) {
+      const int r0p = gp * p.rows_base + min(gp, p.rows_rem);
+      for (int w = 0; w < p.sw; ++w) {
+        const unsigned long long fw = fws[gp * p.sw + w];
+        const uint32_t f = static_cast<uint32_t>(fw), sn = static_cast<uint32_t>(fw >> 32);
+        if (!f) continue;
+        const int cnt = __popc(f);
+        if (nb + cnt > kFBuf) {
+          drain(nb);
+          nb = 0;
+        }
+        if ((f >> lane) & 1u)
+          buf[nb + __popc(f & ((1u << lane) - 1u))] =
+              static_cast<uint32_t>(r0p + w * 32 + lane) | (((sn >> lane) & 1u) << 31);
+        nb += cnt;
+      }
+    }
+    drain(nb);
+    return acc;
+  };
   auto col_reduce = [&](int mode, int P, bool delta, int tbuf, int w0) {
     const int NP = CW - w0, lw = warp - w0;
     auto psync = [&]() {
@@ -1863,6 +1954,65 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     unsigned long long* tout = p.tb64 + static_cast<size_t>(tbuf) * p.Q * kTbStride;
     const unsigned long long tag = static_cast<unsigned long long>(P + 1) << 32;
     const int gs = (lw * G) / NP, ge = ((lw + 1) * G) / NP;
+    // Matrix delta pass: one ascending list of every flipped row of the rank (built
+    // once by the participating warps, prefix-scanned), split into NP contiguous
+    // slices; when it would not fit in fbuf the warps walk their CTA ranges instead.
+    int nlist = -1;
+    if (delta && mode != 1) {
+      const int items = G * p.sw, lt = lw * 32 + lane, per = (items + NP * 32 - 1) / (NP * 32);
+      const int i0 = min(items, lt * per), i1 = min(items, i0 + per);
+      int cnt = 0;
+      for (int i = i0; i < i1; ++i) cnt += __popc(static_cast<uint32_t>(fws[i]));
+      int inc = cnt;  // inclusive warp scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      int* wtot = reinterpret_cast<int*>(zst);  // scratch (z state is staged later)
+      if (lane == 31) wtot[lw] = inc;
+      psync();
+      int base = 0, total = 0;
+      for (int w = 0; w < NP; ++w) {
+        const int t = wtot[w];
+        if (w < lw) base += t;
+        total += t;
+      }
+      if (total <= CW * kFBuf) {
+        int pos = base + inc - cnt;
+        for (int i = i0; i < i1; ++i) {
+          uint32_t f = static_cast<uint32_t>(fws[i]);
+          const uint32_t sn = static_cast<uint32_t>(fws[i] >> 32);
+          const int gp = i / p.sw, w = i - gp * p.sw;
+          const int rb = gp * p.rows_base + min(gp, p.rows_rem) + w * 32;
+          while (f) {
+            const int b = __ffs(f) - 1;
+            f &= f - 1;
+            fbuf[pos++] = static_cast<uint32_t>(rb + b) | (((sn >> b) & 1u) << 31);
+          }
+        }
+        nlist = total;
+      }
+      psync();
+    }
+    auto list_sum = [&](int col) -> double {  // this warp's slice of the list, in order
+      const int k0 = (nlist * lw) / NP, k1 = (nlist * (lw + 1)) / NP;
+      const E* Rc = R + col;
+      double acc = 0.0;
+      for (int k = k0; k < k1; k += 8) {
+        E v[8];
+        uint32_t e[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          e[u] = (k + u < k1) ? fbuf[k + u] : 0u;
+          v[u] = (k + u < k1) ? __ldcg(Rc + static_cast<size_t>(e[u] & 0x7fffffffu) * pitch) : E(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (k + u < k1) acc = fma(static_cast<double>(v[u]), (e[u] >> 31) ? -2.0 : 2.0, acc);
+      }
+      return acc;
+    };
     for (int q0 = g; q0 < p.Q; q0 += G * p.zl) {
       int nls = 0;
       for (int j = 0; j < p.zl && q0 + j * G < p.Q; ++j) nls = j + 1;
@@ -1872,6 +2022,9 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         if (zstate_here && lw == 0 && col < p.n) zsv[j] = __ldcg(p.zstate + col);  // issued early
         double a = 0.0;
         const double* zb = p.zpart + par;
+        if (delta && mode != 1) {  // matrix delta pass: the flipped rows themselves (no partials)
+          a = nlist >= 0 ? list_sum(col) : flip_rows_sum(col, gs, ge, lw);
+        } else
         for (int g0 = gs; g0 < ge; g0 += 32) {  // one round of up to 32 L2 loads in flight
           double v[32];
 #pragma unroll
@@ -2104,6 +2257,9 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         dl.errp = da.errp;
         dl.has_dz = &ctl->has_dz;
         dl.nfrows = &ctl->nfrows;
+        dl.local_dz = TS ? 1 : 0;
+        dl.flipw = p.flipw + (static_cast<size_t>(P & 1) * G + g) * p.sw;
+        dl.prof = prof ? p.prof + static_cast<size_t>(p.G) * 16 + g * 8 : nullptr;
         dl.pitch = pitch;
         dl.rowB = static_cast<unsigned>(rowB);
         dl.rows_g = rows_g;
@@ -2167,7 +2323,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
                   x[e] = Vec<E>::narrow(static_cast<double>(x[e]) + flipd(-alpha, sneg ^ bitmask(ub, e)));
               if (j < nres) rv[v] = Vec<E>::join(x);
             }
-            if ((j >= nres && (kind & F_UPD)) || (kind & F_WB)) grow[v] = Vec<E>::join(x);
+            if (kind & (F_UPD | F_WB)) grow[v] = Vec<E>::join(x);  // every row current in global R
 #pragma unroll
             for (int e = 0; e < EPV; ++e) {
               const double d = static_cast<double>(x[e]);
@@ -2256,6 +2412,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         ns += __ldcg(&s->n[P & 1]);
         if ((kind & F_DELTA) && __ldcg(&s->dz[P & 1]) != 0.0) atomicOr(&dzmask[i >> 5], 1u << (i & 31));
       }
+      if (!TS && (kind & F_DELTA) && g < p.Q) {  // owners: every CTA's flip words of this pass
+        const unsigned long long* src = p.flipw + static_cast<size_t>(P & 1) * G * p.sw;
+        for (int i = tid; i < G * p.sw; i += CT) fws[i] = __ldcg(src + i);
+      }
       cs = warp_sum(cs);
       ns = warp_sum(ns);
       if (tid == 32) {  // error flags for the decision, off thread 0's serial path
@@ -2282,7 +2442,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
           ns += ctl->nred[w];
         }
         unsigned anydz = 0;
-        for (int i = 0; i < 64; ++i) anydz |= dzmask[i];
+        if (TS)
+          for (int i = 0; i < 64; ++i) anydz |= dzmask[i];
+        else if (kind & F_DELTA)  // g == 0 is an owner: its fws holds the rank's flip words
+          for (int i = 0; i < G * p.sw; ++i) anydz |= static_cast<unsigned>(fws[i] != 0ull);
         if (g == 0) {
           Slot* rs = p.rslot_own;
           __stcg(&rs->c[P & 1], cs);
