@@ -307,6 +307,9 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
     return set_err(ctx, SC_NOT_SUPPORTED, "row length %llu exceeds the fused-kernel envelope",
                    static_cast<unsigned long long>(n));
   var.tensor = tensor ? 1 : 0;  // order-k kernels are separate instantiations
+  var.mr = (sh && sh->world > 1 && !vr) ? 1 : 0;  // the multi-rank exchange is compiled in separately
+  if (var.mr && !scb::has_vr(var))
+    return set_err(ctx, SC_NOT_SUPPORTED, "row sharding: no multi-rank kernel for rows of %llu", static_cast<unsigned long long>(n));
   if (vr && !scb::has_vr(var))
     return set_err(ctx, SC_NOT_SUPPORTED, "emulated row sharding: no virtual-rank kernel for rows of %llu", static_cast<unsigned long long>(n));
 

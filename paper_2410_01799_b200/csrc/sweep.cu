@@ -14,9 +14,11 @@ void* kernel_f32t(const Variant& v);
 void* kernel_f64m(const Variant& v);
 void* kernel_f64t(const Variant& v);
 void* kernel_vr(const Variant& v);
+void* kernel_mr(const Variant& v);
 
 namespace {
 void* kernel_for(const Variant& v) {
+  if (v.mr) return kernel_mr(v);
   if (v.dtype == 0) return v.tensor ? kernel_f32t(v) : kernel_f32m(v);
   return v.tensor ? (v.cps == 1 ? kernel_f64t(v) : nullptr) : kernel_f64m(v);
 }
@@ -30,6 +32,7 @@ int pick_variant(int dtype, long long pitch, Variant* v) {
   v->dtype = dtype;
   v->cps = 1;
   v->tensor = 0;
+  v->mr = 0;
   v->nw = 8;
   if (nv <= 256) {
     v->vpt = 1; v->rg = 4;

@@ -172,6 +172,7 @@ struct Variant {
   int rg;     // rows per group (one dot-partial publication per group)
   int cps;    // CTAs per SM (2: 113-register budget, raw lag buffers)
   int tensor; // order-k instantiation (set by the host after pick_variant)
+  int mr;     // multi-rank (row-sharded world > 1) instantiation (set by the host)
 };
 
 constexpr int kRing = 4;  // dot-partial ring depth (groups)

@@ -1679,7 +1679,9 @@ __device__ __noinline__ int tensor_continue(Ctl* ctl, int delta, int refresh, in
 // v_k = (k * NW + w) * 32 + l, k < VPT, of every row (coalesced LDS.128), i.e.
 // NE = VPT * EPV elements per row, and the matching NE f64 column accumulators.
 // CPS: CTAs per SM (1, or 2 with a 112-register budget and raw lag buffers).
-template <typename E, int NW, int VPT, int RG, int CPS, bool TS>
+// MR: the multi-rank (row-sharded, world > 1) exchange is compiled in.  The
+// single-GPU kernels carry none of it (smaller code on the per-pass path).
+template <typename E, int NW, int VPT, int RG, int CPS, bool TS, bool MR = false>
 __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
   constexpr int EPV = Vec<E>::N;
   constexpr int CW = NW;       // consumer warps
@@ -2146,7 +2148,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       } else if (!TS) {  // order-k: tws was rebuilt by the previous pass's axial step
         // t words were published before the last grid barrier, tagged with this pass
         const unsigned long long* tw = p.tb64 + static_cast<size_t>(ctl->tsel) * p.Q * kTbStride;
-        if (p.world > 1) {  // published by owners on every rank: bounded spin
+        if (MR && p.world > 1) {  // published by owners on every rank: bounded spin
           SpinBound sb{p.abort_word, p.timeout_ns, 0ull, 0u};
           for (int i = tid; i < p.Q; i += CT) {
             unsigned long long x;
@@ -2199,7 +2201,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
                                  : static_cast<uint32_t>(__ldcg(p.tb64 + (static_cast<size_t>(ctl->utsel) * p.Q + i) * kTbStride));
     }
     consumer_sync(CT);
-    if (p.world > 1 && ctl->aborted) break;  // uniform: set before the barrier
+    if (MR && p.world > 1 && ctl->aborted) break;  // uniform: set before the barrier
     if (g == 0 && tid == 32 && (kind & F_DELTA)) nflip_sum += static_cast<unsigned>(ctl->nflip);
     if (prof && tid == 0) pacc[5] += clock64() - t_pass0;
     // A sweep whose t equals the previous pass's t is a fixed point of the cached
@@ -2390,7 +2392,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     }
     if (tid == 0) {
       const long long tb0 = prof ? clock64() : 0;
-      if (p.world > 1) {  // rank-local barrier first (the rank partials need this rank's partials)
+      if (MR && p.world > 1) {  // rank-local barrier first (the rank partials need this rank's partials)
         if (!grid_barrier_bounded<false>(p.bar_local, ++lepoch * static_cast<unsigned>(G), p.abort_word,
                                          p.timeout_ns)) {
           ctl->aborted = 1;
@@ -2402,7 +2404,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       if (prof) pacc[6] += clock64() - tb0;  // barrier (incl. waiting for the last CTA)
     }
     consumer_sync(CT);
-    if (p.world > 1 && ctl->aborted) break;
+    if (MR && p.world > 1 && ctl->aborted) break;
     {
       // every CTA reduces the G partials of its rank in the same fixed order
       double cs = 0.0, ns = 0.0;
@@ -2430,7 +2432,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       }
     }
     consumer_sync(CT);
-    if (p.world > 1) {
+    if (MR && p.world > 1) {
       // Rank stage: this rank's column partials -> one rank partial zr (local
       // owners), its slots -> one rank slot; then the cross-rank barrier, after
       // which every CTA of every rank combines the world rank slots in rank order.
@@ -2514,7 +2516,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     // Matrix dot pass: owners reduce z and publish the next t right away (it does
     // not depend on the decision), taking the decision off every CTA's critical path.
     if (!TS && (kind & F_DOT) && warp >= 1) {  // warp 0 runs the decision below meanwhile
-      if (p.world > 1)
+      if (MR && p.world > 1)
         col_reduce_global(P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
       else
         col_reduce(0, P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
@@ -2751,7 +2753,12 @@ template <typename E, int NW, int VPT, int RG>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel_vr(const __grid_constant__ KParamsVR pv) {
   const int G = pv.r[0].G;
   const int rank = static_cast<int>(blockIdx.x) / G;
-  sweep_body<E, NW, VPT, RG, 1, false>(pv.r[rank], static_cast<int>(blockIdx.x) - rank * G);
+  sweep_body<E, NW, VPT, RG, 1, false, true>(pv.r[rank], static_cast<int>(blockIdx.x) - rank * G);
+}
+// Row-sharded rank on its own GPU (world > 1, peer-mapped exchange regions).
+template <typename E, int NW, int VPT, int RG>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) sweep_kernel_mr(const KParams p) {
+  sweep_body<E, NW, VPT, RG, 1, false, true>(p, blockIdx.x);
 }
 
 
