@@ -352,6 +352,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   // the cooperative launch needs every CTA co-resident: trim resident rows until
   // the occupancy API confirms var.cps CTAs per SM at this footprint
   while (var.cps > 1 && res_rows > 0 && scb::blocks_per_sm(var, smem_for(stages, res_rows)) < var.cps) --res_rows;
+  while (var.cps > 1 && stages > 2 && scb::blocks_per_sm(var, smem_for(stages, res_rows)) < var.cps) --stages;
   const size_t smem = smem_for(stages, res_rows);
   if (scb::blocks_per_sm(var, smem) < var.cps)
     return set_err(ctx, SC_NOT_SUPPORTED, "%d CTAs per SM do not fit (%zu bytes of shared memory each)", var.cps, smem);

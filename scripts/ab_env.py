@@ -1,5 +1,5 @@
 """Same-box, same-process A/B of run-time engine settings (environment knobs read
-per call): AB_ENVS="SCB_FUSE_UPDATE=1;SCB_FUSE_UPDATE=0" alternates the settings
+per call): AB_ENVS="SCB_FUSE_UPDATE=1;SCB_FUSE_UPDATE=0|SCB_DELTA=0" alternates the settings (";" between settings, "|" between variables)
 for AB_ROUNDS rounds on the 4096^2 f32 config-2 matrix, AB_W cuts per call."""
 import os
 import sys
@@ -22,7 +22,7 @@ eng.run(a, sc.DecomposeConfig(width=4, search=sc.SearchConfig(seed=SEED)), dtype
 res = {}
 for rnd in range(int(os.environ.get("AB_ROUNDS", 3))):
     for st in settings:
-        kv = [x.split("=", 1) for x in st.split(",") if x]
+        kv = [x.split("=", 1) for x in st.split("|") if x]
         old = {k: os.environ.get(k) for k, _ in kv}
         for k, v in kv:
             os.environ[k] = v
