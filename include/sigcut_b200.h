@@ -14,6 +14,9 @@
  *   sc_validate_problem  restates  detail::check_decompose_config decompose.hpp:290-298,
  *                                  DenseTensor shape checks       dense_tensor.hpp:57-79,
  *                                  best_of_restarts checks        search.hpp:217-218
+ *   sc_batch_decompose   runs independent greedy_decompose calls over several
+ *                                  devices (the reference's "concurrent calls on
+ *                                  distinct inputs are safe", README:179-181)
  *   sc_start_vectors     restates  the per-cut start draw of greedy_matrix_run /
  *                                  axial_run (search.hpp:149-150, :197) seeded by
  *                                  term_search_config (decompose.hpp:300-304) and
@@ -140,6 +143,17 @@ sc_status sc_create(sc_ctx** out, int device);
 void sc_destroy(sc_ctx* ctx);
 const char* sc_last_error(const sc_ctx* ctx);
 
+/* Engine options of this context (tuning / test knobs; the defaults are the
+ * measured best).  Names: "ctas" (CTA cap, 0 auto), "delta" (sparse delta passes,
+ * 1), "delta_div" (32), "delta_refresh" (64), "two_phase" (dot-pass form: -1 auto,
+ * 0 fused single read, 1 two-phase), "stages" (TMA ring depth, 0 auto),
+ * "res_rows" (cap on SMEM-resident rows, -1 none), "fuse_update" (rank-1 update
+ * fused into the next term's first dot pass, 1), "variant" (tile override
+ * nw*1000000 + vpt*10000 + rg*100 + cps, 0 auto), "profile" (clock64 breakdown of
+ * SCB_PROFILE builds to stderr, 0).  No option changes results except through the
+ * documented summation orders (signs and sweep counts are option-independent). */
+sc_status sc_set_option(sc_ctx* ctx, const char* name, int64_t value);
+sc_status sc_get_option(const sc_ctx* ctx, const char* name, int64_t* value);
 /* Greedy width-w signed-cut decomposition on the device (Alg. 5/13). */
 sc_status sc_greedy_decompose(sc_ctx* ctx, const sc_problem* problem, sc_result* result);
 
@@ -160,6 +174,22 @@ void sc_fill_normal_f32(uint64_t seed, uint64_t count, float* out);
 uint64_t sc_width_for_compression(int coeff_bits, int source_bits, int order,
                                   const uint64_t* shape, double rate);
 
+/* A batch of independent decompositions over several devices (
+ * the reference's concurrency contract: concurrent calls on distinct inputs are
+ * safe).  Jobs are assigned longest-processing-time first (cost =
+ * width x numel, sc_lpt_schedule) to `devices`; one host thread and one context
+ * per device run their jobs longest first, with no data-path communication.
+ * Every job's result equals sc_greedy_decompose of it on any device.  Returns
+ * SC_OK when every job succeeded, else the first failure's status (message in
+ * msg); each job's own status and device are written back. */
+typedef struct sc_batch_job {
+  sc_problem problem;  /* host or device data (device data must live on the job's device) */
+  sc_result* result;   /* caller-owned outputs, as for sc_greedy_decompose */
+  int32_t status;      /* out: sc_status of this job */
+  int32_t device;      /* out: device that ran it */
+} sc_batch_job;
+sc_status sc_batch_decompose(const int32_t* devices, int32_t ndevices, sc_batch_job* jobs, uint64_t njobs,
+                             char* msg, size_t msg_len);
 /* Longest-processing-time-first assignment of `count` independent jobs with
  * the given costs to `bins` devices; writes the bin of each job.  Used by the
  * multi-GPU batch path (one process per GPU, no data-path collective). */

@@ -81,98 +81,148 @@ struct RunOutput {
   double kernel_ms = 0.0;
 };
 
+namespace detail {
+/// One decomposition call's C-ABI problem and caller-owned output buffers, and the
+/// conversion of the outputs to the reference's result types.
+struct Call {
+  std::vector<std::size_t> shape;
+  std::vector<std::uint64_t> shp;
+  std::vector<float> a32;
+  sc_problem p{};
+  sc_result r{};
+  std::size_t w = 0;
+  bool record_curve = true, want_remainder = false;
+  DType dtype = DType::kF64;
+  std::vector<std::vector<std::uint64_t>> words;
+  std::vector<double> alpha, cut, rn, rne, rem64, sv;
+  std::vector<float> rem32;
+  std::vector<std::uint32_t> sweeps;
+
+  Call(const DenseTensor& a, const DecomposeConfig& cfg, DType dt, bool want_rem, sc_seed_mode seed_mode,
+       bool want_diag)
+      : shape(a.shape()), shp(shape.begin(), shape.end()), w(cfg.width), record_curve(cfg.record_curve),
+        want_remainder(want_rem), dtype(dt) {
+    if (cfg.method != DecomposeConfig::Method::kGreedy)
+      throw std::invalid_argument("sigcut_b200: only the greedy method runs on the device");
+    p.dtype = static_cast<std::int32_t>(dtype);
+    p.order = static_cast<std::int32_t>(shape.size());
+    p.shape = shp.data();
+    if (dtype == DType::kF32) {
+      a32.assign(a.data().begin(), a.data().end());  // same rounding as the DTEN f32 path
+      p.data = a32.data();
+    } else {
+      p.data = a.data().data();
+    }
+    p.data_on_device = 0;
+    p.seed_mode = seed_mode;
+    p.width = cfg.width;
+    p.flush_width = cfg.flush_width;
+    p.seed = cfg.search.seed;
+    p.restarts = cfg.search.restarts;
+    p.max_sweeps = cfg.search.max_sweeps;
+    p.min_value_fraction = cfg.min_value_fraction;
+    p.max_factor_bytes = cfg.max_factor_bytes;
+    char msg[256];
+    const sc_status vst = sc_validate_problem(&p, msg, sizeof msg);
+    if (vst != SC_OK) raise(vst, msg);
+    words.resize(shape.size());
+    for (std::size_t ax = 0; ax < shape.size(); ++ax) {
+      words[ax].assign(w * SignVector::word_count(shape[ax]), 0);
+      r.sign_words[ax] = words[ax].data();
+    }
+    alpha.assign(w, 0.0);
+    cut.assign(w, 0.0);
+    rn.assign(w, 0.0);
+    rne.assign(w, 0.0);
+    sweeps.assign(w, 0);
+    r.alpha = alpha.data();
+    r.cut_value = cut.data();
+    r.resid_norm = rn.data();
+    r.resid_norm_exact = rne.data();
+    r.sweeps = sweeps.data();
+    if (want_remainder) {
+      if (dtype == DType::kF32) {
+        rem32.resize(a.numel());
+        r.remainder = rem32.data();
+      } else {
+        rem64.resize(a.numel());
+        r.remainder = rem64.data();
+      }
+    }
+    if (want_diag) {
+      sv.assign(std::max<std::size_t>(cfg.search.max_sweeps, 1), 0.0);
+      r.sweep_values = sv.data();
+    }
+  }
+
+  RunOutput finish(SearchDiagnostics* diag) {
+    if (diag != nullptr) {  // SearchDiagnostics (search.hpp:37-40); no CPU delta cache to check
+      diag->sweep_values.assign(sv.begin(), sv.begin() + static_cast<std::ptrdiff_t>(r.n_sweep_values));
+      diag->max_cache_rel_error = 0.0;
+    }
+    RunOutput out;
+    CutDecomposition d = CutDecomposition::with_shape(shape);
+    CutReport rep;
+    rep.input_norm = r.input_norm;
+    const StorageModel model{64, 64, shape, -1};
+    for (std::size_t k = 0; k < r.width_done; ++k) {
+      std::vector<SignVector> signs;
+      for (std::size_t ax = 0; ax < shape.size(); ++ax) {
+        const std::size_t nw = SignVector::word_count(shape[ax]);
+        signs.push_back(SignVector::from_words(
+            shape[ax], std::vector<std::uint64_t>(words[ax].begin() + k * nw, words[ax].begin() + (k + 1) * nw)));
+      }
+      d.append_term(signs, std::span<const double>(&alpha[k], 1));
+      if (record_curve) rep.steps.push_back(CutStep{k + 1, cut[k], rn[k], compression_rate(k + 1, model)});
+    }
+    rep.width = d.width();
+    rep.final_residual_norm = r.final_residual_norm;
+    out.sweeps.assign(sweeps.begin(), sweeps.begin() + r.width_done);
+    out.resid_norm_exact.assign(rne.begin(), rne.begin() + r.width_done);
+    if (want_remainder) {
+      std::vector<double> v = dtype == DType::kF32 ? std::vector<double>(rem32.begin(), rem32.end()) : rem64;
+      out.remainder = DenseTensor::from_raw(shape, std::move(v));
+    }
+    out.kernel_ms = r.kernel_ms;
+    out.result = {std::move(d), std::move(rep)};
+    return out;
+  }
+};
+}  // namespace detail
+
 /// Greedy width-w decomposition on the device; fills the reference's result
 /// types exactly as sigcut::greedy_decompose does (decompose.hpp:314-361).
 inline RunOutput run(const DenseTensor& a, const DecomposeConfig& cfg, DType dtype, Engine& eng,
                      bool want_remainder, sc_seed_mode seed_mode = SC_SEED_PER_TERM,
                      SearchDiagnostics* diag = nullptr) {
-  if (cfg.method != DecomposeConfig::Method::kGreedy)
-    throw std::invalid_argument("sigcut_b200: only the greedy method runs on the device");
-  const std::vector<std::size_t>& shape = a.shape();
-  std::vector<std::uint64_t> shp(shape.begin(), shape.end());
-  std::vector<float> a32;
-  sc_problem p{};
-  p.dtype = static_cast<std::int32_t>(dtype);
-  p.order = static_cast<std::int32_t>(shape.size());
-  p.shape = shp.data();
-  if (dtype == DType::kF32) {
-    a32.assign(a.data().begin(), a.data().end());  // same rounding as the DTEN f32 path
-    p.data = a32.data();
-  } else {
-    p.data = a.data().data();
-  }
-  p.data_on_device = 0;
-  p.seed_mode = seed_mode;
-  p.width = cfg.width;
-  p.flush_width = cfg.flush_width;
-  p.seed = cfg.search.seed;
-  p.restarts = cfg.search.restarts;
-  p.max_sweeps = cfg.search.max_sweeps;
-  p.min_value_fraction = cfg.min_value_fraction;
-  p.max_factor_bytes = cfg.max_factor_bytes;
+  detail::Call c(a, cfg, dtype, want_remainder, seed_mode, diag != nullptr);
+  eng.check(sc_greedy_decompose(eng.get(), &c.p, &c.r));
+  return c.finish(diag);
+}
 
-  char msg[256];
-  const sc_status vst = sc_validate_problem(&p, msg, sizeof msg);
-  if (vst != SC_OK) detail::raise(vst, msg);
-
-  const std::size_t w = cfg.width;
-  sc_result r{};
-  std::vector<std::vector<std::uint64_t>> words(shape.size());
-  for (std::size_t ax = 0; ax < shape.size(); ++ax) {
-    words[ax].assign(w * SignVector::word_count(shape[ax]), 0);
-    r.sign_words[ax] = words[ax].data();
+/// A batch of independent decompositions over several devices:
+/// longest-processing-time-first assignment (cost width x numel), one host thread
+/// and one context per device, no data-path communication.  Each result equals
+/// the single-device greedy_decompose of that input.  The reference's contract
+/// for this is "concurrent calls on distinct inputs are safe".
+inline std::vector<std::pair<CutDecomposition, CutReport>> batch_decompose(
+    const std::vector<DenseTensor>& inputs, const std::vector<DecomposeConfig>& cfgs, DType dtype = DType::kF64,
+    const std::vector<int>& devices = {0}) {
+  if (inputs.size() != cfgs.size()) throw std::invalid_argument("batch_decompose: inputs and configs differ in count");
+  std::vector<std::unique_ptr<detail::Call>> calls;
+  std::vector<sc_batch_job> jobs(inputs.size());
+  for (std::size_t i = 0; i < inputs.size(); ++i) {
+    calls.push_back(std::make_unique<detail::Call>(inputs[i], cfgs[i], dtype, false, SC_SEED_PER_TERM, false));
+    jobs[i].problem = calls[i]->p;
+    jobs[i].result = &calls[i]->r;
   }
-  std::vector<double> alpha(w), cut(w), rn(w), rne(w);
-  std::vector<std::uint32_t> sweeps(w);
-  std::vector<double> rem64;
-  std::vector<float> rem32;
-  r.alpha = alpha.data();
-  r.cut_value = cut.data();
-  r.resid_norm = rn.data();
-  r.resid_norm_exact = rne.data();
-  r.sweeps = sweeps.data();
-  if (want_remainder) {
-    if (dtype == DType::kF32) {
-      rem32.resize(a.numel());
-      r.remainder = rem32.data();
-    } else {
-      rem64.resize(a.numel());
-      r.remainder = rem64.data();
-    }
-  }
-  std::vector<double> sv(diag != nullptr ? std::max<std::size_t>(cfg.search.max_sweeps, 1) : 0);
-  r.sweep_values = diag != nullptr ? sv.data() : nullptr;
-  eng.check(sc_greedy_decompose(eng.get(), &p, &r));
-  if (diag != nullptr) {  // SearchDiagnostics (search.hpp:37-40); no CPU delta cache to check
-    diag->sweep_values.assign(sv.begin(), sv.begin() + static_cast<std::ptrdiff_t>(r.n_sweep_values));
-    diag->max_cache_rel_error = 0.0;
-  }
-
-  RunOutput out;
-  CutDecomposition d = CutDecomposition::with_shape(shape);
-  CutReport rep;
-  rep.input_norm = r.input_norm;
-  const StorageModel model{64, 64, shape, -1};
-  for (std::size_t k = 0; k < r.width_done; ++k) {
-    std::vector<SignVector> signs;
-    for (std::size_t ax = 0; ax < shape.size(); ++ax) {
-      const std::size_t nw = SignVector::word_count(shape[ax]);
-      signs.push_back(SignVector::from_words(
-          shape[ax], std::vector<std::uint64_t>(words[ax].begin() + k * nw, words[ax].begin() + (k + 1) * nw)));
-    }
-    d.append_term(signs, std::span<const double>(&alpha[k], 1));
-    if (cfg.record_curve) rep.steps.push_back(CutStep{k + 1, cut[k], rn[k], compression_rate(k + 1, model)});
-  }
-  rep.width = d.width();
-  rep.final_residual_norm = r.final_residual_norm;
-  out.sweeps.assign(sweeps.begin(), sweeps.begin() + r.width_done);
-  out.resid_norm_exact.assign(rne.begin(), rne.begin() + r.width_done);
-  if (want_remainder) {
-    std::vector<double> v = dtype == DType::kF32 ? std::vector<double>(rem32.begin(), rem32.end()) : rem64;
-    out.remainder = DenseTensor::from_raw(shape, std::move(v));
-  }
-  out.kernel_ms = r.kernel_ms;
-  out.result = {std::move(d), std::move(rep)};
+  std::vector<std::int32_t> devs(devices.begin(), devices.end());
+  char msg[512];
+  const sc_status st = sc_batch_decompose(devs.data(), static_cast<std::int32_t>(devs.size()), jobs.data(),
+                                          jobs.size(), msg, sizeof msg);
+  if (st != SC_OK) detail::raise(st, msg);
+  std::vector<std::pair<CutDecomposition, CutReport>> out;
+  for (auto& c : calls) out.push_back(c->finish(nullptr).result);
   return out;
 }
 

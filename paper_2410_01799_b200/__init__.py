@@ -19,6 +19,7 @@ from .api import (  # noqa: F401
     SearchDiagnostics,
     SigcutRuntimeError,
     axial_greedy_cut,
+    batch_decompose,
     correct_coefficients,
     decompose,
     default_engine,

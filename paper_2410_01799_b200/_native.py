@@ -78,6 +78,15 @@ class ScShardConfig(C.Structure):
     ]
 
 
+class ScBatchJob(C.Structure):
+    _fields_ = [
+        ("problem", ScProblem),
+        ("result", C.POINTER(ScResult)),
+        ("status", C.c_int32),
+        ("device", C.c_int32),
+    ]
+
+
 class ScShardEmulation(C.Structure):
     _fields_ = [
         ("world", C.c_int32),
@@ -118,6 +127,8 @@ SIGNATURES = {
     "sc_create": (C.c_int, [P(C.c_void_p), C.c_int]),
     "sc_destroy": (None, [C.c_void_p]),
     "sc_last_error": (C.c_char_p, [C.c_void_p]),
+    "sc_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
+    "sc_get_option": (C.c_int, [C.c_void_p, C.c_char_p, P(C.c_int64)]),
     "sc_greedy_decompose": (C.c_int, [C.c_void_p, P(ScProblem), P(ScResult)]),
     "sc_validate_problem": (C.c_int, [P(ScProblem), C.c_char_p, C.c_size_t]),
     "sc_start_vectors": (u64, [P(ScProblem), u64, u64, P(u64)]),
@@ -125,6 +136,7 @@ SIGNATURES = {
     "sc_fill_normal_f32": (None, [u64, u64, P(C.c_float)]),
     "sc_width_for_compression": (u64, [C.c_int, C.c_int, C.c_int, P(u64), C.c_double]),
     "sc_lpt_schedule": (None, [P(C.c_double), u64, C.c_uint32, P(C.c_uint32)]),
+    "sc_batch_decompose": (C.c_int, [P(C.c_int32), C.c_int32, P(ScBatchJob), u64, C.c_char_p, C.c_size_t]),
     "sc_shard_open": (C.c_int, [C.c_void_p, P(ScShardConfig), C.c_void_p]),
     "sc_shard_connect": (C.c_int, [C.c_void_p, C.c_void_p]),
     "sc_shard_reset": (C.c_int, [C.c_void_p]),

@@ -30,6 +30,7 @@ computes the decomposition on the CPU.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass, field
 from typing import List, Optional
@@ -187,7 +188,7 @@ def _shape_array(shape):
 class Engine:
     """One device context (reference calls are reentrant; one Engine per device)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, **options):
         self.lib = N.lib()
         h = C.c_void_p()
         st = self.lib.sc_create(C.byref(h), device)
@@ -195,6 +196,30 @@ class Engine:
             raise DeviceError(f"sc_create(device={device}) failed: no usable sm_100 device")
         self.handle = h
         self.device = device
+        for k, v in options.items():
+            self.set_option(k, v)
+
+    def set_option(self, name: str, value: int) -> None:
+        """Engine option of this context (sc_set_option): ctas, delta, delta_div,
+        delta_refresh, two_phase, stages, res_rows, fuse_update, variant, profile."""
+        self._check(self.lib.sc_set_option(self.handle, name.encode(), int(value)))
+
+    def get_option(self, name: str) -> int:
+        v = C.c_int64()
+        self._check(self.lib.sc_get_option(self.handle, name.encode(), C.byref(v)))
+        return int(v.value)
+
+    @contextlib.contextmanager
+    def options(self, **kv):
+        """Temporarily set engine options (restored on exit)."""
+        old = {k: self.get_option(k) for k in kv}
+        try:
+            for k, v in kv.items():
+                self.set_option(k, v)
+            yield self
+        finally:
+            for k, v in old.items():
+                self.set_option(k, v)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -590,4 +615,75 @@ def lpt_schedule(costs, bins: int) -> np.ndarray:
     out = np.zeros(len(c), np.uint32)
     N.lib().sc_lpt_schedule(c.ctypes.data_as(C.POINTER(C.c_double)), len(c), bins,
                             out.ctypes.data_as(C.POINTER(C.c_uint32)))
+    return out
+
+
+def batch_decompose(inputs, cfgs, dtype: Optional[str] = None, devices=(0,)):
+    """Independent greedy decompositions over several devices (sc_batch_decompose:
+    LPT by width x numel, one host thread and context per device, no data-path
+    communication).  Returns [(CutDecomposition, CutReport, device)] in input order;
+    each equals Engine.run of that input.  Raises the first failing job's error."""
+    inputs = [np.ascontiguousarray(a) for a in inputs]
+    cfgs = list(cfgs)
+    if len(inputs) != len(cfgs):
+        raise InvalidArgument("batch_decompose: inputs and configs differ in count")
+    keep, calls = [], []
+    jobs = (N.ScBatchJob * max(1, len(inputs)))()
+    for i, (a0, cfg) in enumerate(zip(inputs, cfgs)):
+        dt = dtype or ("f32" if a0.dtype == np.float32 else "f64")
+        a = np.ascontiguousarray(a0, dtype=np.float32 if dt == "f32" else np.float64)
+        shape = a.shape
+        sh = _shape_array(shape)
+        p = jobs[i].problem
+        p.dtype = N.SC_F32 if dt == "f32" else N.SC_F64
+        p.order = len(shape)
+        p.shape = C.cast(sh, C.POINTER(N.u64))
+        p.data = a.ctypes.data
+        p.data_on_device = 0
+        p.seed_mode = N.SC_SEED_PER_TERM
+        p.width = int(cfg.width)
+        p.flush_width = int(cfg.flush_width)
+        p.seed = int(cfg.search.seed) & ((1 << 64) - 1)
+        p.restarts = int(cfg.search.restarts)
+        p.max_sweeps = int(cfg.search.max_sweeps)
+        p.min_value_fraction = float(cfg.min_value_fraction)
+        p.max_factor_bytes = int(cfg.max_factor_bytes)
+        w = max(int(cfg.width), 1)
+        bufs = {"signs": [np.zeros((w, (int(d) + 63) // 64), np.uint64) for d in shape],
+                "alpha": np.zeros(w), "cut": np.zeros(w), "rn": np.zeros(w), "rne": np.zeros(w),
+                "sweeps": np.zeros(w, np.uint32)}
+        res = N.ScResult()
+        for k, sg in enumerate(bufs["signs"]):
+            res.sign_words[k] = sg.ctypes.data_as(C.POINTER(N.u64))
+        res.alpha = bufs["alpha"].ctypes.data_as(C.POINTER(C.c_double))
+        res.cut_value = bufs["cut"].ctypes.data_as(C.POINTER(C.c_double))
+        res.resid_norm = bufs["rn"].ctypes.data_as(C.POINTER(C.c_double))
+        res.resid_norm_exact = bufs["rne"].ctypes.data_as(C.POINTER(C.c_double))
+        res.sweeps = bufs["sweeps"].ctypes.data_as(C.POINTER(C.c_uint32))
+        jobs[i].result = C.pointer(res)
+        keep.append((a, sh, res))
+        calls.append((shape, cfg, bufs, res))
+    devs = (C.c_int32 * len(devices))(*devices)
+    msg = C.create_string_buffer(512)
+    st = N.lib().sc_batch_decompose(devs, len(devices), jobs, len(inputs), msg, 512)
+    if st != N.SC_OK:
+        raise _ERRORS.get(st, SigcutRuntimeError)(msg.value.decode())
+    out = []
+    for i, (shape, cfg, b, res) in enumerate(calls):
+        wd = int(res.width_done)
+        numel = float(np.prod([float(d) for d in shape]))
+        bpt = 64 + sum(int(d) for d in shape)
+        steps = [CutStep(k + 1, float(b["cut"][k]), float(b["rn"][k]), (k + 1) * bpt / (64.0 * numel))
+                 for k in range(wd)] if cfg.record_curve else []
+        dec = CutDecomposition(tuple(int(d) for d in shape), [sg[:wd].copy() for sg in b["signs"]],
+                               b["alpha"][:wd].copy())
+        rep = CutReport(steps, float(res.input_norm), float(res.final_residual_norm), wd,
+                        residual_norm_exact=b["rne"][:wd].copy(), sweeps=b["sweeps"][:wd].copy(),
+                        passes=int(res.passes), kernel_ms=float(res.kernel_ms), total_ms=float(res.total_ms),
+                        h2d_bytes=int(res.h2d_bytes), d2h_bytes=int(res.d2h_bytes),
+                        kernel_launches=int(res.kernel_launches), dense_passes=int(res.dense_passes),
+                        delta_passes=int(res.delta_passes), device_bytes=int(res.device_bytes))
+        rep._cut_values = b["cut"][:wd].copy()
+        out.append((dec, rep, int(jobs[i].device)))
+    del keep
     return out

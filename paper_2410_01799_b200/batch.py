@@ -28,6 +28,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import sys
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -112,7 +113,7 @@ def plan(jobs: Sequence[Job], world: int) -> np.ndarray:
 def run_batch(jobs: Sequence[Job], rank: int, world: int,
               execute: Callable[..., Dict], gather: Optional[Callable[[list], List[list]]] = None,
               prepare: Optional[Callable[[Job], object]] = None,
-              pair: Optional[Callable[[Job], bool]] = None) -> Dict:
+              pair: Optional[Callable[[Job], bool]] = None, lookahead: int = 1) -> Dict:
     """Run this rank's share and collect every rank's summaries.
 
     ``execute(job)`` returns a dict summary (it must contain ``cuts`` and
@@ -121,7 +122,8 @@ def run_batch(jobs: Sequence[Job], rank: int, world: int,
     single process.  With ``prepare(job)`` (host-side input synthesis), the next
     job's input is prepared on a background thread while the device works on the
     current one (the engine call releases the GIL), and ``execute(job, data)`` is
-    called.  With ``pair(job)``, the jobs it accepts (the sync-bound small
+    called; ``lookahead`` jobs are prepared concurrently (host threads; numpy
+    releases the GIL).  With ``pair(job)``, the jobs it accepts (the sync-bound small
     shapes, which sort to the tail of the longest-first order) run two at a time
     on two host threads as ``execute(job, data, lane)``, lane 0 or 1, each lane
     on its own engine with half the grid (1024×4096 jobs +76%); the
@@ -139,15 +141,16 @@ def run_batch(jobs: Sequence[Job], rank: int, world: int,
     solo = [j for j in mine if pair is None or not pair(j)]
     duo = [j for j in mine if pair is not None and pair(j)]
     order = solo + duo
-    pool = ThreadPoolExecutor(max_workers=1) if prepare is not None and order else None
-    nxt = pool.submit(prepare, order[0]) if pool else None
+    la = max(1, int(lookahead))
+    pool = ThreadPoolExecutor(max_workers=la) if prepare is not None and order else None
+    ahead = {k: pool.submit(prepare, order[k]) for k in range(min(la, len(order)))} if pool else {}
 
     def fetch(k):
-        nonlocal nxt
         if pool is None:
             return None
-        data = nxt.result()
-        nxt = pool.submit(prepare, order[k + 1]) if k + 1 < len(order) else None
+        data = ahead.pop(k).result()
+        if k + la < len(order):
+            ahead[k + la] = pool.submit(prepare, order[k + la])
         return data
 
     def record(j, s):
@@ -185,8 +188,10 @@ def run_batch(jobs: Sequence[Job], rank: int, world: int,
 
 def _main() -> int:
     ap = argparse.ArgumentParser()
-    ap.add_argument("--jobs", type=int, default=14, help="first J jobs of the 226 (layer order)")
-    ap.add_argument("--prefix-cuts", type=int, default=64, help="cuts per job (prefix of its Table-2 width)")
+    ap.add_argument("--jobs", type=int, default=226, help="first J jobs of the 226 (layer order)")
+    ap.add_argument("--prefix-cuts", type=int, default=512, help="cuts per job (prefix of its Table-2 width)")
+    ap.add_argument("--lookahead", type=int, default=8, help="jobs synthesised concurrently on the host")
+    ap.add_argument("--out", default="", help="also write the JSON summary here")
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--pair-rows", type=int, default=0,
                     help="jobs with at most this many rows run two at a time, half the grid each "
@@ -204,22 +209,29 @@ def _main() -> int:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     eng = Engine(local)
-    engs = [eng, Engine(local)] if args.pair_rows > 0 else [eng]
     half = torch.cuda.get_device_properties(local).multi_processor_count // 2
-    for e in engs[1:]:  # first-use setup of the second lane's engine stays out of the batch
+    # pair phase: one engine per lane, each grid capped at half the SMs (engine option)
+    lanes = [Engine(local, ctas=half), Engine(local, ctas=half)] if args.pair_rows > 0 else []
+    for e in lanes:  # first-use setup of the lanes' engines stays out of the batch
         e.run(np.ones((64, 64), np.float32), DecomposeConfig(width=1), dtype=args.dtype)
     jobs = [Job(j.index, j.name, j.shape, min(j.width, args.prefix_cuts), j.seed)
             for j in mistral_jobs()[: args.jobs]]
 
     def execute(job: Job, a, lane: Optional[int] = None) -> Dict:
         cfg = DecomposeConfig(width=job.width, search=SearchConfig(seed=job.seed))
-        if lane is not None:
-            # pair phase (after every solo job): each engine's grid capped at half the SMs
-            os.environ["SCB_CTAS"] = str(half)
-        dec, rep, _ = engs[lane or 0].run(a, cfg, dtype=args.dtype)
-        return {"cuts": dec.width(), "device_s": rep.kernel_ms / 1e3, "call_s": rep.total_ms / 1e3,
-                "rel_residual": rep.final_residual_norm / rep.input_norm,
-                "sweeps_mean": float(np.mean(rep.sweeps)) if len(rep.sweeps) else 0.0}
+        try:
+            dec, rep, _ = (eng if lane is None else lanes[lane]).run(a, cfg, dtype=args.dtype)
+        except Exception as e:  # reported per job; the batch goes on
+            print(f"job {job.index} {job.name} {job.shape}: {e!r}", file=sys.stderr, flush=True)
+            return {"shape": list(job.shape), "cuts": 0, "device_s": 0.0, "error": repr(e)}
+        print(f"job {job.index} {job.name} {job.shape}: {dec.width()} cuts in {rep.kernel_ms:.1f} ms",
+              file=sys.stderr, flush=True)
+        return {"shape": list(job.shape), "cuts": dec.width(), "device_s": rep.kernel_ms / 1e3,
+                "call_s": rep.total_ms / 1e3, "rel_residual": rep.final_residual_norm / rep.input_norm,
+                "sweeps_mean": float(np.mean(rep.sweeps)) if len(rep.sweeps) else 0.0,
+                "sweeps_max": int(np.max(rep.sweeps)) if len(rep.sweeps) else 0,
+                "cap_hits": int(np.sum(rep.sweeps >= 100)), "passes": rep.passes,
+                "device_bytes": rep.device_bytes}
 
     def gather(obj):
         out = [None] * world
@@ -229,14 +241,19 @@ def _main() -> int:
     t0 = time.perf_counter()
     pair = (lambda j: j.shape[0] <= args.pair_rows) if args.pair_rows > 0 else None
     res = run_batch(jobs, rank, world, execute, gather if world > 1 else None, prepare=mistral_matrix,
-                    pair=pair)
-    os.environ.pop("SCB_CTAS", None)
+                    pair=pair, lookahead=args.lookahead)
     wall = time.perf_counter() - t0
     if rank == 0:
-        print(json.dumps({"metric": "batch signed cuts/sec (Mistral-shaped prefix)", "n_gpus": world,
-                          "jobs": len(jobs), "cuts": res["cuts"], "device_s_max_rank": res["device_s"],
-                          "value": res["cuts"] / res["device_s"], "unit": "cuts/s", "wall_s": wall,
-                          "per_job": res["jobs"]}))
+        out = {"metric": "batch signed cuts/sec (Mistral-shaped prefix)", "n_gpus": world,
+               "jobs": len(jobs), "cuts_per_job": args.prefix_cuts, "cuts": res["cuts"],
+               "device_s_max_rank": res["device_s"], "value": res["cuts"] / res["device_s"], "unit": "cuts/s",
+               "wall_s": wall, "schedule": "LPT over ranks (sc_lpt_schedule), cost w*m*n",
+               "data": "synthetic Mistral-7B-shaped matrices (rank-64 + noise, bf16-rounded, f32)",
+               "per_job": res["jobs"]}
+        print(json.dumps(out))
+        if args.out:
+            with open(args.out, "w") as f:
+                json.dump(out, f, indent=1)
     if world > 1:
         dist.destroy_process_group()
     return 0

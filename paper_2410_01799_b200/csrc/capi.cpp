@@ -14,7 +14,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <numeric>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -95,10 +97,6 @@ T* carve(char*& cur, size_t count) {
   return p;
 }
 
-size_t env_size(const char* name, size_t dflt) {
-  const char* v = std::getenv(name);
-  return v ? static_cast<size_t>(std::strtoull(v, nullptr, 10)) : dflt;
-}
 
 }  // namespace
 
@@ -152,6 +150,42 @@ void sc_destroy(sc_ctx* ctx) {
 }
 
 const char* sc_last_error(const sc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+sc_status sc_set_option(sc_ctx* ctx, const char* name, int64_t value) {
+  if (ctx == nullptr || name == nullptr) return SC_INVALID_ARGUMENT;
+  auto& o = ctx->opts;
+  struct {
+    const char* name;
+    long long* field;
+  } const table[] = {{"ctas", &o.ctas},           {"delta", &o.delta},         {"delta_div", &o.delta_div},
+                     {"delta_refresh", &o.delta_refresh}, {"two_phase", &o.two_phase}, {"stages", &o.stages},
+                     {"res_rows", &o.res_rows},   {"fuse_update", &o.fuse_update}, {"variant", &o.variant},
+                     {"profile", &o.profile}};
+  for (const auto& e : table)
+    if (std::strcmp(e.name, name) == 0) {
+      *e.field = value;
+      return SC_OK;
+    }
+  return set_err(ctx, SC_INVALID_ARGUMENT, "sc_set_option: unknown option '%s'", name);
+}
+
+sc_status sc_get_option(const sc_ctx* ctx, const char* name, int64_t* value) {
+  if (ctx == nullptr || name == nullptr || value == nullptr) return SC_INVALID_ARGUMENT;
+  const auto& o = ctx->opts;
+  struct {
+    const char* name;
+    long long v;
+  } const table[] = {{"ctas", o.ctas},           {"delta", o.delta},         {"delta_div", o.delta_div},
+                     {"delta_refresh", o.delta_refresh}, {"two_phase", o.two_phase}, {"stages", o.stages},
+                     {"res_rows", o.res_rows},   {"fuse_update", o.fuse_update}, {"variant", o.variant},
+                     {"profile", o.profile}};
+  for (const auto& e : table)
+    if (std::strcmp(e.name, name) == 0) {
+      *value = e.v;
+      return SC_OK;
+    }
+  return SC_INVALID_ARGUMENT;
+}
 
 sc_status sc_validate_problem(const sc_problem* problem, char* msg, size_t msg_len) {
   std::string m;
@@ -209,6 +243,65 @@ void sc_lpt_schedule(const double* costs, uint64_t count, uint32_t bins, uint32_
   }
 }
 
+sc_status sc_batch_decompose(const int32_t* devices, int32_t ndevices, sc_batch_job* jobs, uint64_t njobs,
+                             char* msg, size_t msg_len) {
+  auto fail_msg = [&](const char* m) {
+    if (msg && msg_len) std::snprintf(msg, msg_len, "%s", m);
+  };
+  if (msg && msg_len) msg[0] = '\0';
+  if (devices == nullptr || ndevices < 1 || (jobs == nullptr && njobs > 0)) {
+    fail_msg("sc_batch_decompose: no devices / null jobs");
+    return SC_INVALID_ARGUMENT;
+  }
+  std::vector<double> cost(njobs, 0.0);
+  for (uint64_t j = 0; j < njobs; ++j) {
+    const sc_problem& p = jobs[j].problem;
+    double numel = 1.0;
+    for (int i = 0; p.shape != nullptr && i < p.order && i < SC_MAX_ORDER; ++i) numel *= static_cast<double>(p.shape[i]);
+    cost[j] = static_cast<double>(std::max<uint64_t>(p.width, 1)) * numel;
+    jobs[j].status = SC_OK;
+    jobs[j].device = -1;
+  }
+  std::vector<uint32_t> bin(njobs, 0);
+  sc_lpt_schedule(cost.data(), njobs, static_cast<uint32_t>(ndevices), bin.data());
+  std::mutex mu;
+  sc_status first = SC_OK;
+  std::string first_msg;
+  auto note = [&](sc_status st, const std::string& m) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (first == SC_OK) {
+      first = st;
+      first_msg = m;
+    }
+  };
+  auto worker = [&](int32_t b) {
+    std::vector<uint64_t> mine;
+    for (uint64_t j = 0; j < njobs; ++j)
+      if (bin[j] == static_cast<uint32_t>(b)) mine.push_back(j);
+    std::stable_sort(mine.begin(), mine.end(), [&](uint64_t x, uint64_t y) { return cost[x] > cost[y]; });
+    sc_ctx* ctx = nullptr;
+    const sc_status cst = sc_create(&ctx, devices[b]);
+    for (uint64_t j : mine) {
+      jobs[j].device = devices[b];
+      if (cst != SC_OK) {
+        jobs[j].status = cst;
+        note(cst, "sc_batch_decompose: sc_create(device " + std::to_string(devices[b]) + ") failed");
+        continue;
+      }
+      const sc_status st = sc_greedy_decompose(ctx, &jobs[j].problem, jobs[j].result);
+      jobs[j].status = st;
+      if (st != SC_OK) note(st, "job " + std::to_string(j) + ": " + sc_last_error(ctx));
+    }
+    if (ctx) sc_destroy(ctx);
+  };
+  std::vector<std::thread> threads;
+  for (int32_t b = 1; b < ndevices; ++b) threads.emplace_back(worker, b);
+  worker(0);
+  for (auto& t : threads) t.join();
+  if (first != SC_OK) fail_msg(first_msg.c_str());
+  return first;
+}
+
 namespace {
 // Everything finish_run needs after the launch (prepare_run fills it).
 struct RunState {
@@ -257,7 +350,10 @@ namespace {
 sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc_ctx::Shard* sh) {
   RunState S;
   if (sc_status st = prepare_run(ctx, p, res, sh, S, false); st != SC_OK) return st;
-  SC_CUDA(ctx, scb::set_smem_limit(S.var, S.smem));
+  // the attribute is a per-function maximum shared by every context and thread of
+  // the process: always the device's opt-in limit, so concurrent engines never
+  // lower it under each other's launches (the launch passes the real size)
+  SC_CUDA(ctx, scb::set_smem_limit(S.var, ctx->smem_optin));
   SC_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   SC_CUDA(ctx, scb::launch_sweep(S.var, S.kp, S.smem, ctx->stream));
   SC_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
@@ -303,7 +399,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   const size_t es = dt == SC_F32 ? 4 : 8;
   const long long pitch = static_cast<long long>((n + 31) / 32 * 32);
   scb::Variant var{};
-  if (scb::pick_variant(dt, pitch, &var) != 0)
+  if (scb::pick_variant(dt, pitch, &var, ctx->opts.variant) != 0)
     return set_err(ctx, SC_NOT_SUPPORTED, "row length %llu exceeds the fused-kernel envelope",
                    static_cast<unsigned long long>(n));
   var.tensor = tensor ? 1 : 0;  // order-k kernels are separate instantiations
@@ -323,7 +419,8 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   // grid is faster (1024^2 f32: 11.5 vs 13.1 us/pass).  SCB_CTAS caps G (tuning).
   const uint64_t g_auto = auto_ctas(ctx->num_sms, var.cps, m);
   const int G = sh ? sh->G
-                  : static_cast<int>(std::min<uint64_t>(g_auto, env_size("SCB_CTAS", static_cast<size_t>(g_auto))));
+                  : static_cast<int>(ctx->opts.ctas > 0 ? std::min<uint64_t>(g_auto, static_cast<uint64_t>(ctx->opts.ctas))
+                                                        : g_auto);
   const int rows_base = static_cast<int>(m / G), rows_rem = static_cast<int>(m % G);
   const int rows_max = rows_base + (rows_rem ? 1 : 0);
   const int Q = static_cast<int>(pitch / 32);
@@ -339,15 +436,14 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   const size_t cap = var.cps == 1 ? ctx->smem_optin : std::min(ctx->smem_optin, (ctx->smem_per_sm / var.cps) - 1024);
   int stages = 0, res_rows = rows_max;
   if (cpr > 1 || smem_for(0, rows_max) > cap) {
-    stages = static_cast<int>(env_size("SCB_STAGES", static_cast<size_t>(2 * var.rg + 4)));
+    stages = static_cast<int>(ctx->opts.stages > 0 ? ctx->opts.stages : 2 * var.rg + 4);
     stages = std::max(2, std::min(stages, scb::kMaxStages));
     while (stages > 2 && smem_for(stages, 0) > cap) --stages;
     if (smem_for(stages, 0) > cap)
       return set_err(ctx, SC_NOT_SUPPORTED, "row of %zu bytes does not fit the shared-memory ring", rowB);
     res_rows = 0;
     while (cpr == 1 && res_rows < rows_max && smem_for(stages, res_rows + 1) <= cap) ++res_rows;
-    res_rows = static_cast<int>(std::min<size_t>(env_size("SCB_RES_ROWS", static_cast<size_t>(res_rows)),
-                                                 static_cast<size_t>(res_rows)));
+    if (ctx->opts.res_rows >= 0) res_rows = static_cast<int>(std::min<long long>(ctx->opts.res_rows, res_rows));
   }
   // the cooperative launch needs every CTA co-resident: trim resident rows until
   // the occupancy API confirms var.cps CTAs per SM at this footprint
@@ -375,9 +471,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
                       ((nstart * axw64 * 8 + 255) & ~size_t(255)) +
                       ((std::max<uint64_t>(w, 1) * axw64 * 8 + 255) & ~size_t(255)) +
                       2 * ((static_cast<size_t>(pitch) * 8 + 255) & ~size_t(255)) +
-                      ((2 * static_cast<size_t>(G) * sw * 8 + 255) & ~size_t(255)) +
-                      env_size("SCB_ARENA_SHIFT", 0) + env_size("SCB_SYNC_SHIFT", 0) + env_size("SCB_SLOT_SHIFT", 0) +
-                      env_size("SCB_TB_SHIFT", 0) + env_size("SCB_ZS_SHIFT", 0);
+                      ((2 * static_cast<size_t>(G) * sw * 8 + 255) & ~size_t(255));
   if (need > ctx->arena_bytes) {
     if (ctx->arena) cudaFree(ctx->arena);
     ctx->arena = nullptr;
@@ -385,17 +479,12 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
     SC_CUDA(ctx, cudaMalloc(&ctx->arena, need));
     ctx->arena_bytes = need;
   }
-  // SCB_ARENA/SYNC/SLOT/TB/ZS_SHIFT: placement probes only
-  // (scripts/layout_probe.py; DESIGN.md 5 "Placement of the exchange words")
-  char* cur = static_cast<char*>(ctx->arena) + env_size("SCB_ARENA_SHIFT", 0);
+  char* cur = static_cast<char*>(ctx->arena);
   void* dR = carve<char>(cur, m * rowB);
-  cur += env_size("SCB_SYNC_SHIFT", 0);
   double* zpart = carve<double>(cur, 2 * static_cast<size_t>(G) * pitch);  // [2][G][pitch] by pass parity
-  cur += env_size("SCB_SLOT_SHIFT", 0);
   scb::Slot* slots = carve<scb::Slot>(cur, G);
   unsigned* ctr = carve<unsigned>(cur, 8);  // [0] grid barrier, [1..3] err_pass
   unsigned long long* stats = carve<unsigned long long>(cur, 8);
-  cur += env_size("SCB_TB_SHIFT", 0);
   unsigned long long* tb64 = carve<unsigned long long>(cur, 2 * static_cast<size_t>(tw32) * scb::kTbStride);
   unsigned* ctr_g = ctr;  // the grid's barrier / error words (rank 0's when sharded)
   if (sh) {  // exchange buffers live in the peer-mapped shard region (reset by sc_shard_reset)
@@ -419,7 +508,6 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   uint64_t* ax0 = carve<uint64_t>(cur, std::max<uint64_t>(nstart * axw64, 1));
   uint64_t* AX_out = carve<uint64_t>(cur, std::max<uint64_t>(std::max<uint64_t>(w, 1) * axw64, 1));
   double* zfull = carve<double>(cur, static_cast<size_t>(pitch));
-  cur += env_size("SCB_ZS_SHIFT", 0);
   double* zstate = carve<double>(cur, static_cast<size_t>(pitch));
   unsigned long long* flipw = carve<unsigned long long>(cur, 2 * static_cast<size_t>(G) * sw);
 
@@ -540,10 +628,10 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   kp.flipw = flipw;
   // Sparse delta passes between dense refreshes (matrices, any row length: the dz of
   // flipped rows walks every column chunk).
-  kp.delta = static_cast<int>(env_size("SCB_DELTA", 1));
-  kp.fuse_update = static_cast<int>(env_size("SCB_FUSE_UPDATE", 1));
-  kp.delta_div = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_DIV", 32)));
-  kp.delta_refresh = static_cast<int>(std::max<size_t>(1, env_size("SCB_DELTA_REFRESH", 64)));
+  kp.delta = ctx->opts.delta ? 1 : 0;
+  kp.fuse_update = ctx->opts.fuse_update ? 1 : 0;
+  kp.delta_div = static_cast<int>(std::max<long long>(1, ctx->opts.delta_div));
+  kp.delta_refresh = static_cast<int>(std::max<long long>(1, ctx->opts.delta_refresh));
   // Dot-pass form: the two-phase pass reads R twice per sweep but has no per-row
   // serial chain -- the better choice while R stays in SMEM / L2; once R spills
   // to HBM the fused single-read pass wins (14336x4096 f32: 77.6 vs 84 us/pass).
@@ -551,7 +639,8 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   const bool l2_resident = m * rowB <= (size_t{160} << 20);  // 4096^2 f64 (128 MB): two-phase 24.0 vs 24.6 us/pass
   // The 16-warp whole-row variants (8193..14336 f32 columns) are faster two-phase
   // even when R spills to HBM (4096 x 14336 f32: 58 vs 97 us/pass; C3: 91 vs 183).
-  kp.two_phase = (cpr > 1 || var.nw == 16) ? 1 : static_cast<int>(env_size("SCB_2PH", l2_resident ? 1 : 0));
+  kp.two_phase = (cpr > 1 || var.nw == 16) ? 1
+                 : (ctx->opts.two_phase >= 0 ? (ctx->opts.two_phase ? 1 : 0) : (l2_resident ? 1 : 0));
   kp.cpr = cpr;
   kp.world = sh ? sh->world : 1;
   kp.rank = sh ? sh->rank : 0;
@@ -570,7 +659,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   kp.fault = sh ? sh->fault : 0;
   kp.chunk_cols = cpr > 1 ? static_cast<int>(tile_cols) : static_cast<int>(pitch);
 
-  const bool prof = std::getenv("SCB_PROF") != nullptr;
+  const bool prof = ctx->opts.profile != 0;
   unsigned long long* dprof = nullptr;
   if (prof) {
     SC_CUDA(ctx, cudaMalloc(&dprof, static_cast<size_t>(G) * 24 * 8));
@@ -700,7 +789,7 @@ sc_status finish_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, RunState&
           mx[i] = std::max(mx[i], static_cast<double>(hp[g * 16 + i]));
         }
       const double np_ = std::max<double>(1.0, static_cast<double>(h_stats[1]));
-      if (std::getenv("SCB_PROF_CTA")) {
+      if (ctx->opts.profile >= 2) {
         std::fprintf(stderr, "[scb cta] barrier wait per pass:");
         for (int g = 0; g < G; ++g) std::fprintf(stderr, " %.0f", static_cast<double>(hp[g * 16 + 6]) / np_);
         std::fprintf(stderr, "\n[scb cta] dot pass per pass:");
@@ -982,6 +1071,7 @@ sc_status sc_greedy_decompose_sharded_emulated(sc_ctx* ctx, const sc_problem* p,
     c->ev0 = ctx->ev0;
     c->ev1 = ctx->ev1;
     c->borrowed = true;
+    c->opts = ctx->opts;  // the parent's engine options apply to every rank
     k.row0 = static_cast<uint64_t>(r) * m / world;
     k.rows = static_cast<uint64_t>(r + 1) * m / world - k.row0;
     sc_shard_config cfg{};
@@ -1055,7 +1145,7 @@ sc_status sc_greedy_decompose_sharded_emulated(sc_ctx* ctx, const sc_problem* p,
   }
   if (static_cast<size_t>(smem) > ctx->smem_optin)
     return fail(set_err(ctx, SC_NOT_SUPPORTED, "emulated row sharding: %zu bytes of shared memory", smem));
-  if (cudaError_t e = scb::set_smem_limit_vr(R[0].S.var, smem); e != cudaSuccess)
+  if (cudaError_t e = scb::set_smem_limit_vr(R[0].S.var, ctx->smem_optin); e != cudaSuccess)
     return fail(set_err(ctx, SC_CUDA_ERROR, "set_smem_limit_vr: %s", cudaGetErrorString(e)));
   cudaEventRecord(ctx->ev0, ctx->stream);
   if (cudaError_t e = scb::launch_sweep_vr(R[0].S.var, pv, G, smem, ctx->stream); e != cudaSuccess)

@@ -20,6 +20,20 @@ struct sc_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool borrowed = false;  // stream / events belong to a parent context (emulated ranks)
+  // Engine options (sc_set_option): tuning and test knobs of the decomposition
+  // kernel, per context -- never read from the environment on the product path.
+  struct Options {
+    long long ctas = 0;           // cap on the CTA count (0: auto)
+    long long delta = 1;          // sparse delta passes between dense refreshes
+    long long delta_div = 32;     // delta pass only if <= n / delta_div columns flipped
+    long long delta_refresh = 64; // dense refresh every delta_refresh sweeps
+    long long two_phase = -1;     // dot-pass form: -1 auto (by residency), 0 fused single read, 1 two-phase
+    long long stages = 0;         // TMA ring depth (0: auto)
+    long long res_rows = -1;      // cap on SMEM-resident rows per CTA (-1: as many as fit)
+    long long fuse_update = 1;    // rank-1 update fused into the next term's first dot pass
+    long long variant = 0;        // kernel tile override nw*1000000 + vpt*10000 + rg*100 + cps (0: auto)
+    long long profile = 0;        // print the clock64 breakdown (SCB_PROFILE builds; 2: per CTA)
+  } opts;
   std::string err;
   // cached device arena and pinned staging
   void* arena = nullptr;

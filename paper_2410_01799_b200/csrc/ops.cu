@@ -375,12 +375,6 @@ cudaError_t launch_expand_t(const ExpandParams& p, cudaStream_t st) {
 
 cudaError_t launch_expand(const ExpandParams& p, cudaStream_t st) {
   if (p.P <= 0 || p.Q <= 0 || p.nterms <= 0) return cudaSuccess;
-  // SCB_XTILE: tuning override (0: 16 rows x 8 warps x 2 CTAs/SM, 1: 24 x 4 x 3)
-  static const int tile = [] {
-    const char* e = std::getenv("SCB_XTILE");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (tile == 1) return launch_expand_t<24, 4, 3>(p, st);
   return launch_expand_t<16, 8, 2>(p, st);
 }
 

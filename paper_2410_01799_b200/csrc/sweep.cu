@@ -2,6 +2,7 @@
 // signed-cut kernel (sweep_impl.cuh).  The kernel families are instantiated in
 // separate translation units (sweep_k_{f32,f64}{m,t}.cu) that nvcc compiles in
 // parallel; this file only dispatches to them.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -24,7 +25,7 @@ void* kernel_for(const Variant& v) {
 }
 }  // namespace
 
-int pick_variant(int dtype, long long pitch, Variant* v) {
+int pick_variant(int dtype, long long pitch, Variant* v, long long override_code) {
   // nw consumer warps (+1 producer warp); a thread owns vpt 16-byte vectors of
   // every row and keeps two groups of rg rows in registers (current + lagged).
   const int epv = dtype == 0 ? 4 : 2;
@@ -55,11 +56,13 @@ int pick_variant(int dtype, long long pitch, Variant* v) {
     // vectors (8192 f32 / 4096 f64 columns, one TMA stage each, two-phase pass)
     v->vpt = 8; v->rg = 1;
   }
-  if (const char* e = std::getenv("SCB_VARIANT")) {  // tuning override "nw,vpt,rg[,cps]"
+  if (override_code > 0) {  // tuning override nw*1000000 + vpt*10000 + rg*100 + cps (engine option "variant")
     Variant t = *v;
-    if (std::sscanf(e, "%d,%d,%d,%d", &t.nw, &t.vpt, &t.rg, &t.cps) >= 3 && kernel_for(t) != nullptr &&
-        static_cast<long long>(t.nw) * 32 * t.vpt >= nv)
-      *v = t;
+    t.nw = static_cast<int>(override_code / 1000000);
+    t.vpt = static_cast<int>((override_code / 10000) % 100);
+    t.rg = static_cast<int>((override_code / 100) % 100);
+    t.cps = std::max(1, static_cast<int>(override_code % 100));
+    if (kernel_for(t) != nullptr && static_cast<long long>(t.nw) * 32 * t.vpt >= nv) *v = t;
   }
   return 0;
 }
@@ -76,8 +79,10 @@ cudaError_t set_smem_limit(const Variant& v, size_t bytes) {
 
 int blocks_per_sm(const Variant& v, size_t smem_bytes) {
   void* f = kernel_for(v);
-  int nb = 0;
-  if (!f || set_smem_limit(v, smem_bytes) != cudaSuccess ||
+  int nb = 0, dev = 0, optin = 0;
+  if (!f || cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+      set_smem_limit(v, static_cast<size_t>(optin)) != cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, (v.nw + 1) * 32, smem_bytes) != cudaSuccess)
     return 0;
   return nb;

@@ -231,7 +231,7 @@ inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_r
 }
 
 // Returns 0 on success.
-int pick_variant(int dtype, long long pitch, Variant* v);
+int pick_variant(int dtype, long long pitch, Variant* v, long long override_code = 0);
 cudaError_t set_smem_limit(const Variant& v, size_t bytes);
 int blocks_per_sm(const Variant& v, size_t smem_bytes);  // co-resident CTAs at this smem
 cudaError_t launch_sweep(const Variant& v, const KParams& p, size_t smem_bytes, cudaStream_t st);

@@ -1,6 +1,7 @@
-"""Same-box, same-process A/B of run-time engine settings (environment knobs read
-per call): AB_ENVS="SCB_FUSE_UPDATE=1;SCB_FUSE_UPDATE=0|SCB_DELTA=0" alternates the settings (";" between settings, "|" between variables)
-for AB_ROUNDS rounds on the 4096^2 f32 config-2 matrix, AB_W cuts per call."""
+"""Same-box, same-process A/B of engine options (sc_set_option):
+AB_OPTS="fuse_update=1;fuse_update=0|delta=0" alternates the settings (";" between
+settings, "|" between options) for AB_ROUNDS rounds on the 4096^2 f32 config-2
+matrix (or AB_SHAPE), AB_W cuts per call."""
 import os
 import sys
 
@@ -16,22 +17,15 @@ a = sc.fill_normal(SEED, M * N, np.float32).reshape(M, N)
 if dtype == "f64":
     a = a.astype(np.float64)
 cfg = sc.DecomposeConfig(width=int(os.environ.get("AB_W", 512)), search=sc.SearchConfig(seed=SEED))
-settings = [s for s in os.environ.get("AB_ENVS", "").split(";")]
+settings = [s for s in os.environ.get("AB_OPTS", "").split(";")]
 eng = sc.Engine(0)
 eng.run(a, sc.DecomposeConfig(width=4, search=sc.SearchConfig(seed=SEED)), dtype=dtype)
 res = {}
 for rnd in range(int(os.environ.get("AB_ROUNDS", 3))):
     for st in settings:
-        kv = [x.split("=", 1) for x in st.split("|") if x]
-        old = {k: os.environ.get(k) for k, _ in kv}
-        for k, v in kv:
-            os.environ[k] = v
-        dec, rep, _ = eng.run(a, cfg, dtype=dtype)
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+        kv = {k: int(v) for k, v in (x.split("=", 1) for x in st.split("|") if x)}
+        with eng.options(**kv):
+            dec, rep, _ = eng.run(a, cfg, dtype=dtype)
         res.setdefault(st, []).append((rep.kernel_ms, rep.passes, rep.dense_passes, rep.delta_passes,
                                        hash(dec.factors[0].tobytes())))
 for st, v in res.items():

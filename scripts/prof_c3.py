@@ -1,9 +1,9 @@
-"""Phase split of the order-3 C3 pass (needs an SCB_PROFILE=1 build and SCB_PROF=1)."""
+"""Phase split of the order-3 C3 pass (needs an SCB_PROFILE=1 build; engine option profile=1)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2410_01799_b200 as sc
 from paper_2410_01799_b200 import workloads as wl
-eng = sc.Engine(0)
+eng = sc.Engine(0, profile=1)
 img = wl.c3_blob_image()
 for w in (4, 64):
     dec, rep, _ = eng.run(img, sc.DecomposeConfig(width=w, search=sc.SearchConfig(seed=2)), dtype="f32")

@@ -16,5 +16,5 @@ for name, a32, w, seed in cases:
     dec, rep, _ = eng.run(a32, cfg, dtype="f32")
     od = ref.greedy_decompose(a32.astype(np.float64), w, seed=seed, flush_width=1)
     same = [all((dec.factors[i][k] == od.signs[i][k]).all() for i in range(2)) for k in range(w)]
-    print(name, os.environ.get("SCB_VARIANT", "default"), "identical", same, "gpu sweeps", rep.sweeps.tolist(),
+    print(name, "variant option %d" % eng.get_option("variant"), "identical", same, "gpu sweeps", rep.sweeps.tolist(),
           "ref", od.iterations.tolist(), "c", rep._cut_values.tolist(), od.cut_value.tolist(), flush=True)

@@ -141,6 +141,39 @@ int main() {
       CHECK(std::fabs(rc.coefficients[k] - gc.coefficients[k]) <= 1e-9 * std::fabs(rc.coefficients[k]) + 1e-13,
             "correct_coefficients %zu", k);
   }
+  {  // batch_decompose (sc_batch_decompose, LPT over devices): every job equals the reference's
+    std::vector<DenseTensor> ins;
+    std::vector<DecomposeConfig> cfgs;
+    const std::size_t shapes[][2] = {{40, 70}, {128, 33}, {9, 9}, {300, 64}, {64, 257}};
+    for (std::size_t i = 0; i < 5; ++i) {
+      ins.push_back(randn({shapes[i][0], shapes[i][1]}, 100 + i));
+      DecomposeConfig c;
+      c.width = 4 + i;
+      c.record_curve = true;
+      c.search.seed = 7 * i + 1;
+      cfgs.push_back(c);
+    }
+    const auto out = b200::batch_decompose(ins, cfgs, b200::DType::kF64, {0});
+    CHECK(out.size() == ins.size(), "batch size");
+    for (std::size_t i = 0; i < out.size() && i < ins.size(); ++i) {
+      auto [rd, rr] = greedy_decompose(ins[i], cfgs[i]);
+      const auto& [gd, gr] = out[i];
+      CHECK(rd.width() == gd.width(), "batch job %zu width", i);
+      for (std::size_t f = 0; f < rd.factors.size(); ++f) CHECK(rd.factors[f] == gd.factors[f], "batch job %zu factor %zu", i, f);
+      for (std::size_t k = 0; k < rd.coefficients.size() && k < gd.coefficients.size(); ++k)
+        CHECK(std::fabs(rd.coefficients[k] - gd.coefficients[k]) <= 1e-10 * std::fabs(rd.coefficients[k]),
+              "batch job %zu coef %zu", i, k);
+    }
+    bool threw = false;
+    try {
+      std::vector<DecomposeConfig> bad = cfgs;
+      bad[2].search.restarts = 0;
+      b200::batch_decompose(ins, bad, b200::DType::kF64, {0});
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw, "batch: invalid config must throw invalid_argument");
+  }
   std::printf(fails ? "SHIM FAILED (%d)\n" : "SHIM OK\n", fails);
   return fails ? 1 : 0;
 }

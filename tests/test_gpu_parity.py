@@ -357,13 +357,13 @@ def test_sharded_world1_equals_engine(engine, ref, shape, dtype):
 
 
 # ------------------------------------------------- both dot-pass forms stay exact
-@pytest.mark.parametrize("two_phase", ["0", "1"])
-def test_dot_pass_forms_f32_1024_trajectory(engine, ref, monkeypatch, two_phase):
+@pytest.mark.parametrize("two_phase", [0, 1])
+def test_dot_pass_forms_f32_1024_trajectory(engine, ref, two_phase):
     """The fused single-read pass (default once R exceeds L2) and the two-phase
     pass (default while R is L2-resident), forced on the same C1-shaped input."""
-    monkeypatch.setenv("SCB_2PH", two_phase)
     a = ref.fill_normal(0, 1024 * 1024).reshape(1024, 1024).astype(np.float32)
-    dec, rep, _ = run(engine, a, 48, seed=0, dtype="f32")
+    with engine.options(two_phase=two_phase):
+        dec, rep, _ = run(engine, a, 48, seed=0, dtype="f32")
     od = ref.greedy_decompose(a.astype(np.float64), 48, seed=0)
     assert (dec.factors[0] == od.signs[0]).all() and (dec.factors[1] == od.signs[1]).all()
     assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F32_TOL
@@ -381,16 +381,16 @@ def test_fused_pass_default_beyond_l2(engine, ref):
 
 
 # ------------------------------------------------------------- delta passes
-def test_delta_passes_keep_the_trajectory(engine, ref, monkeypatch):
+def test_delta_passes_keep_the_trajectory(engine, ref):
     """Sparse delta passes (cached y = Rt, z = R^T s updated from the flipped
     columns / rows, dense refresh every 64 sweeps) against dense-only passes and
     the reference on the same input: identical signs and sweeps, c to 1e-12."""
     a = ref.fill_normal(11, 1024 * 1024).reshape(1024, 1024).astype(np.float32)
     out = {}
-    for mode in ("0", "1"):
-        monkeypatch.setenv("SCB_DELTA", mode)
-        out[mode] = run(engine, a, 40, seed=3, dtype="f32")
-    (d0, r0, _), (d1, r1, _) = out["0"], out["1"]
+    for mode in (0, 1):
+        with engine.options(delta=mode):
+            out[mode] = run(engine, a, 40, seed=3, dtype="f32")
+    (d0, r0, _), (d1, r1, _) = out[0], out[1]
     assert all((x == y).all() for x, y in zip(d0.factors, d1.factors))
     assert np.array_equal(r0.sweeps, r1.sweeps)
     assert np.max(np.abs(r1._cut_values - r0._cut_values) / np.abs(r0._cut_values)) <= 1e-12
@@ -399,32 +399,30 @@ def test_delta_passes_keep_the_trajectory(engine, ref, monkeypatch):
     assert sweeps_ok(r1.sweeps, od.iterations)
 
 
-@pytest.mark.parametrize("refresh,div", [("1", "32"), ("4", "1"), ("64", "1000000")])
-def test_delta_policy_extremes(engine, ref, monkeypatch, refresh, div):
+@pytest.mark.parametrize("refresh,div", [(1, 32), (4, 1), (64, 1000000)])
+def test_delta_policy_extremes(engine, ref, refresh, div):
     """Every refresh cadence / flip threshold gives the reference's signs: all
     dense (refresh 1), delta even after many flips (div 1), delta only on
     near-converged sweeps (div huge)."""
-    monkeypatch.setenv("SCB_DELTA_REFRESH", refresh)
-    monkeypatch.setenv("SCB_DELTA_DIV", div)
     a = ref.fill_normal(12, 300 * 257).reshape(300, 257)
-    dec, rep, _ = run(engine, a, 12, seed=4)
+    with engine.options(delta_refresh=refresh, delta_div=div):
+        dec, rep, _ = run(engine, a, 12, seed=4)
     od = ref.greedy_decompose(a, 12, seed=4)
     assert (dec.factors[0] == od.signs[0]).all() and (dec.factors[1] == od.signs[1]).all()
     assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F64_TOL
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-def test_delta_gathers_many_flips_tall_bands(engine, monkeypatch, dtype):
+def test_delta_gathers_many_flips_tall_bands(engine, dtype):
     """Delta passes with up to n flipped columns (div 1: lanes walk their flips 8 at
     a time) on bands taller than one 4-row-per-warp group (6000 rows: 41 per CTA),
     against dense-only passes on the same input: identical signs and sweeps."""
     a = sc.fill_normal(21, 6000 * 1536, np.float32).reshape(6000, 1536)
     out = {}
-    for mode, div in (("0", "32"), ("1", "1")):
-        monkeypatch.setenv("SCB_DELTA", mode)
-        monkeypatch.setenv("SCB_DELTA_DIV", div)
-        out[mode] = run(engine, a if dtype == "f32" else a.astype(np.float64), 6, seed=5, dtype=dtype)
-    (d0, r0, _), (d1, r1, _) = out["0"], out["1"]
+    for mode, div in ((0, 32), (1, 1)):
+        with engine.options(delta=mode, delta_div=div):
+            out[mode] = run(engine, a if dtype == "f32" else a.astype(np.float64), 6, seed=5, dtype=dtype)
+    (d0, r0, _), (d1, r1, _) = out[0], out[1]
     assert all((x == y).all() for x, y in zip(d0.factors, d1.factors))
     assert np.array_equal(r0.sweeps, r1.sweeps)
     assert np.max(np.abs(r1._cut_values - r0._cut_values) / np.abs(r0._cut_values)) <= 1e-12

@@ -69,16 +69,16 @@ def test_emulated_world1_is_the_engine(engine, ref):
 
 
 @pytest.mark.parametrize("world", [2, 8])
-def test_emulated_dense_only_and_delta_agree(engine, ref, monkeypatch, world):
+def test_emulated_dense_only_and_delta_agree(engine, ref, world):
     """Delta passes over the rank partials (only ranks with a flipped row send a
     partial) against dense-only passes, both sharded."""
     a = ref.fill_normal(17, 2048 * 1024).reshape(2048, 1024).astype(np.float32)
     cfg = _cfg(20, 9)
     out = {}
-    for mode in ("0", "1"):
-        monkeypatch.setenv("SCB_DELTA", mode)
-        out[mode] = sharded.emulated(a, cfg, world, dtype="f32", engine=engine)
-    (d0, r0, _), (d1, r1, _) = out["0"], out["1"]
+    for mode in (0, 1):
+        with engine.options(delta=mode):
+            out[mode] = sharded.emulated(a, cfg, world, dtype="f32", engine=engine)
+    (d0, r0, _), (d1, r1, _) = out[0], out[1]
     assert all((x == y).all() for x, y in zip(d0.factors, d1.factors))
     assert np.array_equal(r0.sweeps, r1.sweeps)
     assert np.max(np.abs(r1._cut_values - r0._cut_values) / np.abs(r0._cut_values)) <= 1e-12
@@ -103,3 +103,25 @@ def test_emulation_rejects_bad_layouts(engine):
         sharded.emulated(a, _cfg(2, 0), 4, dtype="f32", engine=engine)  # 25-row bands < 37 CTAs
     with pytest.raises(sc.InvalidArgument):
         sharded.emulated(a, _cfg(2, 0), 9, dtype="f32", engine=engine)
+
+
+# ------------------------------------------------ batch over devices (C ABI)
+def test_batch_decompose_equals_single_runs(engine, ref):
+    """sc_batch_decompose (LPT over the listed devices, one context and host thread per
+    device): every job's result equals Engine.run of that input; device list [0, 0]
+    runs two contexts on the one GPU concurrently."""
+    shapes = [(300, 200), (64, 1024), (1000, 96), (33, 33), (512, 512)]
+    arrs = [ref.fill_normal(40 + i, m * n).reshape(m, n).astype(np.float32) for i, (m, n) in enumerate(shapes)]
+    cfgs = [_cfg(6 + i, 3 * i + 1) for i in range(len(shapes))]
+    for devices in ((0,), (0, 0)):
+        out = sc.batch_decompose(arrs, cfgs, dtype="f32", devices=devices)
+        for a, cfg, (dec, rep, dev) in zip(arrs, cfgs, out):
+            d1, r1, _ = engine.run(a, cfg, dtype="f32")
+            assert dev == 0
+            assert all((x == y).all() for x, y in zip(dec.factors, d1.factors))
+            assert np.array_equal(rep.sweeps, r1.sweeps)
+            assert np.array_equal(rep._cut_values, r1._cut_values)
+    bad = list(cfgs)
+    bad[1] = sc.DecomposeConfig(width=2, search=sc.SearchConfig(restarts=0))
+    with pytest.raises(sc.InvalidArgument):
+        sc.batch_decompose(arrs, bad, dtype="f32")
