@@ -150,7 +150,9 @@ const char* sc_last_error(const sc_ctx* ctx);
  * "res_rows" (cap on SMEM-resident rows, -1 none), "fuse_update" (rank-1 update
  * fused into the next term's first dot pass, 1), "variant" (tile override
  * nw*1000000 + vpt*10000 + rg*100 + cps, 0 auto), "profile" (clock64 breakdown of
- * SCB_PROFILE builds to stderr, 0).  No option changes results except through the
+ * SCB_PROFILE builds to stderr, 0), "poison" (test hook: fill the device arena with
+ * NaN bytes before each call, so any read of a never-written word shows, 0).  No
+ * option changes results except through the
  * documented summation orders (signs and sweep counts are option-independent). */
 sc_status sc_set_option(sc_ctx* ctx, const char* name, int64_t value);
 sc_status sc_get_option(const sc_ctx* ctx, const char* name, int64_t* value);

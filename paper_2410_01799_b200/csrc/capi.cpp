@@ -160,7 +160,7 @@ sc_status sc_set_option(sc_ctx* ctx, const char* name, int64_t value) {
   } const table[] = {{"ctas", &o.ctas},           {"delta", &o.delta},         {"delta_div", &o.delta_div},
                      {"delta_refresh", &o.delta_refresh}, {"two_phase", &o.two_phase}, {"stages", &o.stages},
                      {"res_rows", &o.res_rows},   {"fuse_update", &o.fuse_update}, {"variant", &o.variant},
-                     {"profile", &o.profile}};
+                     {"profile", &o.profile},     {"poison", &o.poison}};
   for (const auto& e : table)
     if (std::strcmp(e.name, name) == 0) {
       *e.field = value;
@@ -178,7 +178,7 @@ sc_status sc_get_option(const sc_ctx* ctx, const char* name, int64_t* value) {
   } const table[] = {{"ctas", o.ctas},           {"delta", o.delta},         {"delta_div", o.delta_div},
                      {"delta_refresh", o.delta_refresh}, {"two_phase", o.two_phase}, {"stages", o.stages},
                      {"res_rows", o.res_rows},   {"fuse_update", o.fuse_update}, {"variant", o.variant},
-                     {"profile", o.profile}};
+                     {"profile", o.profile},     {"poison", o.poison}};
   for (const auto& e : table)
     if (std::strcmp(e.name, name) == 0) {
       *value = e.v;
@@ -555,6 +555,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
 
   cudaStream_t st = ctx->stream;
   uint64_t h2d = 0, d2h = 0;
+  if (ctx->opts.poison) SC_CUDA(ctx, cudaMemsetAsync(ctx->arena, 0xff, ctx->arena_bytes, st));
   const cudaMemcpyKind in_kind = p->data_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   if (static_cast<uint64_t>(pitch) != n) SC_CUDA(ctx, cudaMemsetAsync(dR, 0, m * rowB, st));
   SC_CUDA(ctx, cudaMemcpy2DAsync(dR, rowB, p->data, n * es, n * es, m, in_kind, st));

@@ -13,28 +13,36 @@
 // the rest are streamed every pass, one row per stage, by a TMA bulk-copy
 // producer thread (cp.async.bulk + mbarrier ring).
 //
-// Consumer warps (no block-wide barrier inside the row loop): every warp owns
-// a column segment of every row.  Rows are taken in groups; for group g each
-// warp loads its segment from shared memory ONCE into registers, (in the first
-// pass of a term) applies the previous term's rank-1 deflation
-// R -= alpha s t^T in place (flush_pending with one term, decompose.hpp:200-214),
-// sums its part of y_i = sum_j t_j R_ij (matvec_signed, inc/kernels.hpp:61-71)
-// in f64 and publishes it through an mbarrier ring; it then takes the combined
-// y of group g-1 (fixed warp order), records s'_i = [y_i < 0] (sgn_vector,
-// sign_vector.hpp:107-114) and adds s'_i R_i of group g-1 -- still in its
-// registers -- into its f64 column accumulators (matvec_signed_t,
-// inc/kernels.hpp:74-88).  The lag hides the cross-warp combine latency.
+// Passes (one per sweep; SURVEY §3.2 "equivalent GPU sweep schedule"):
+//   * dense dot pass: y = R t, s' = sgn(y) (sgn_vector, sign_vector.hpp:107-114),
+//     z = R^T s' (matvec_signed / _t, kernels.hpp:61-88), all in f64 from f32 or
+//     f64 storage.  Two forms: two-phase (A: per-warp row partials, B: y and s',
+//     C: z streaming the rows again -- while R is L2-resident) and fused single
+//     read (rows in registers, a one-group lag between the dot of g and the z
+//     update of g-1 -- once R spills to HBM).  Wide rows go as column chunks.
+//   * delta dot pass (the GPU form of the reference's delta caches,
+//     kernels.hpp:92-156): y += 2 t'_c R[:, c] over the flipped columns only; the
+//     CTA publishes its flipped rows, and the column owners add 2 s'_i R[i, cols]
+//     for them to their z state.  A dense refresh runs every 64 sweeps.
+//   * the first dot pass of each term also applies the previous term's rank-1
+//     deflation R -= alpha s t^T (flush_pending with one term,
+//     decompose.hpp:200-214) to every row as it streams it, writes R back and
+//     accumulates ||R||^2 (north-star kernel 3: sweeps + 1 passes per cut).
+//   * maintenance passes (norm of the input, the final update and write-back).
 //
 // Cross-CTA exchange per pass (no float atomics, deterministic):
-//   * every CTA stores its column partials and its c / ||R||^2 partials
-//     (double-buffered by pass parity), then one flat counter grid barrier;
-//     every CTA reduces the G scalar partials in one fixed order, so all CTAs
-//     take the identical decision (stop rule c <= c_prev, max_sweeps cap,
-//     restart / term bookkeeping);
-//   * column slices are reduced in a fixed order by their owner CTA and
-//     t' = sgn(z) is packed with __ballot_sync into the reference's LSB-first
-//     words (stored with the pass index in the high half as a sanity tag);
-//     a second barrier publishes them.
+//   * every CTA stores its c / ||R||^2 partials (pass-parity slots) and, in dense
+//     passes, its column partial row (in delta passes its flip words), then one
+//     flat counter grid barrier; every CTA reduces the G slots in one fixed
+//     order, so all CTAs take the identical decision (stop rule c <= c_prev,
+//     max_sweeps cap, restart / term bookkeeping);
+//   * the owner CTA of each 32-column word reduces its columns in a fixed order
+//     (dense: the G partials; delta: the flipped rows) and publishes
+//     t' = sgn(z), packed with __ballot_sync into the reference's LSB-first
+//     words, tagged with the pass index; the next pass polls the tags (no second
+//     barrier).
+//   * row-sharded (MR instantiations, world > 1): the same per rank, then the
+//     rank partials cross NVLink behind one bounded system-scope barrier.
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -1190,7 +1198,9 @@ struct DeltaArgs {
   int* nfrows;        // [2] run totals: flipped rows read (from global), dz partials written
   int local_dz;       // 1: this CTA forms the dz partial of its flipped rows (order-k mode); 0: it
                       //    publishes its flip words and the column owners read the flipped rows
-  unsigned long long* flipw;  // [sw] this pass's (flip mask | s' << 32) words of the band (local_dz == 0)
+  unsigned long long* flipw;  // [sw_all] this pass's (flip mask | s' << 32) words of the band (local_dz == 0)
+  int sw_all;                 // words per CTA record (from the largest band; bands one row shorter leave
+                              // their last word empty -- written as 0, never left stale)
   unsigned long long* prof;  // SCB_PROFILE builds: [6] thread-0 cycle sums of the delta pass sections
   long long pitch;
   unsigned rowB;
@@ -1371,10 +1381,11 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
     // 2 s'_i R[i, cols] to its z state.  No dz partial row here: the pass costs every
     // CTA the same whatever its rows did (no arrival spread at the barrier).
     int nf = 0;
-    for (int w = lane; w < sw; w += 32) {
-      uint32_t f = s_nxt[w] ^ s_cur[w];
+    for (int w = lane; w < a.sw_all; w += 32) {
+      uint32_t f = w < sw ? (s_nxt[w] ^ s_cur[w]) : 0u;
       if (w == sw - 1 && (rows_g & 31)) f &= (1u << (rows_g & 31)) - 1u;
-      if (warp == 0) __stcg(a.flipw + w, static_cast<unsigned long long>(f) | (static_cast<unsigned long long>(s_nxt[w]) << 32));
+      const uint32_t sn = w < sw ? s_nxt[w] : 0u;
+      if (warp == 0) __stcg(a.flipw + w, static_cast<unsigned long long>(f) | (static_cast<unsigned long long>(sn) << 32));
       nf += __popc(f);
     }
     if (warp == 0) {
@@ -2261,6 +2272,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         dl.nfrows = &ctl->nfrows;
         dl.local_dz = TS ? 1 : 0;
         dl.flipw = p.flipw + (static_cast<size_t>(P & 1) * G + g) * p.sw;
+        dl.sw_all = p.sw;
         dl.prof = prof ? p.prof + static_cast<size_t>(p.G) * 16 + g * 8 : nullptr;
         dl.pitch = pitch;
         dl.rowB = static_cast<unsigned>(rowB);

@@ -570,3 +570,23 @@ def test_order_k_many_sweeps_with_delta_passes(engine, ref, shape, dtype):
     assert sweeps_ok(rep.sweeps, od.iterations)
     assert max(rep.sweeps) >= 4  # several sweeps: delta passes between the dense first pass and the stop
     np.testing.assert_allclose(rep._cut_values, od.cut_value, rtol=F32_TOL if dtype == "f32" else F64_TOL)
+
+
+# ------------------------------------------------- uninitialised-memory hygiene
+@pytest.mark.parametrize("shape,dtype,width", [((14336, 2048), "f32", 12), ((2000, 300), "f64", 20), ((32000, 512), "f32", 8),
+                                               ((4095, 1000), "f32", 16), ((3001, 4100), "f32", 6)])
+def test_poisoned_arena_same_results(engine, shape, dtype, width):
+    """Every exchange word a pass reads was written earlier in the same call: with the
+    device arena filled with NaN bytes first (engine option 'poison') the results are
+    bit-identical.  Bands of uneven height (m not a multiple of the CTA count) leave
+    the last flip word of the shorter bands empty; it must be written as 0."""
+    m, n = shape
+    a = sc.fill_normal(m + n, m * n, np.float32).reshape(m, n)
+    a = a if dtype == "f32" else a.astype(np.float64)
+    cfg = sc.DecomposeConfig(width=width, search=sc.SearchConfig(seed=3))
+    d0, r0, _ = engine.run(a, cfg, dtype=dtype)
+    with engine.options(poison=1):
+        d1, r1, _ = engine.run(a, cfg, dtype=dtype)
+    assert all((x == y).all() for x, y in zip(d0.factors, d1.factors))
+    assert np.array_equal(r0._cut_values, r1._cut_values)
+    assert np.array_equal(r0.sweeps, r1.sweeps)
