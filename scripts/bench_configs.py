@@ -50,6 +50,9 @@ def line(name, a, dec, rep, dtype, extra=None):
          "cuts_per_s": rep.width / s, "kernel_s": s, "sweeps_mean": float(sw.mean()), "sweeps_max": int(sw.max()),
          "passes": rep.passes, "algorithmic_GBps": alg / s / 1e9, "hbm_peak_GBps": peak(),
          "frac_algorithmic": alg / s / 1e9 / peak(),
+         "physical_GBps": rep.device_bytes / s / 1e9, "frac_physical": rep.device_bytes / s / 1e9 / peak(),
+         "dense_passes": rep.dense_passes, "delta_passes": rep.delta_passes,
+         "us_per_pass": rep.kernel_ms * 1e3 / max(1, rep.passes),
          "rel_residual": rep.final_residual_norm / rep.input_norm,
          "e2e_s": rep.total_ms * 1e-3, "kernel_launches": rep.kernel_launches}
     if extra:
