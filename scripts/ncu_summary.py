@@ -1,10 +1,10 @@
 """Summarise one round's ncu captures into profiles/<tag>/ (tracked).
 
-usage: python scripts/ncu_summary.py <capture tag>[:<profiles dir>] [bench_json]
-inputs (gpurun_out/): launches_<tag>.csv  (--metrics gpu__time_duration.sum launch list of bench.py)
-                      sweep_<tag>.ncu-rep (--set full capture of one sweep_kernel launch of bench.py)
-outputs: profiles/<tag>/launches.csv, launches_summary.txt, sweep_kernel_full.txt,
-         profiles/latest_kernel_traffic.json (read by bench.py for roofline.traffic)
+usage: python scripts/ncu_summary.py --rep gpurun_out/X.ncu-rep --out profiles/r02/X.txt --desc "..." \
+           --cuts N [--launches gpurun_out/launches.csv] [--traffic]
+outputs: the summary text, launches.csv / launches_summary.txt beside it, and with --traffic
+         profiles/latest_kernel_traffic.json (read by bench.py for roofline.traffic when its
+         cuts per launch match the bench width)
 """
 import collections
 import csv
@@ -42,8 +42,7 @@ FULL_METRICS = [
 ]
 
 
-def launches(tag, dst):
-    src = os.path.join(OUT, f"launches_{tag}.csv")
+def launches(src, dst, desc):
     lines = open(src).read().splitlines()
     start = next(i for i, ln in enumerate(lines) if ln.startswith('"ID"'))
     rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
@@ -59,8 +58,7 @@ def launches(tag, dst):
     tot = sum(v[1] for v in agg.values())
     shutil.copy(src, os.path.join(dst, "launches.csv"))
     with open(os.path.join(dst, "launches_summary.txt"), "w") as f:
-        f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none launch list of\n"
-                f"#   python bench.py --steps 2 --warmup 3 --no-cpu-baseline   (tag {tag})\n"
+        f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none launch list of\n#   {desc}\n"
                 f"# per-launch times are cold-cache and serialised: compare SHARES, not absolutes\n")
         f.write(f"{'launches':>8} {'total ms':>10} {'share':>7}  kernel\n")
         for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -68,9 +66,7 @@ def launches(tag, dst):
     return agg
 
 
-def full(tag, dst):
-    os.makedirs(dst, exist_ok=True)
-    rep = os.path.join(OUT, f"sweep_{tag}.ncu-rep")
+def full(rep, out_txt, desc, cuts, traffic_json=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, u, v = rows[0], rows[1], rows[2]
@@ -78,10 +74,10 @@ def full(tag, dst):
     stalls = sorted(((x, float(v[i] or 0)) for i, x in enumerate(h)
                      if x.startswith("smsp__average_warps_issue_stalled_") and x.endswith("_per_issue_active.ratio")),
                     key=lambda t: -t[1])[:10]
-    with open(os.path.join(dst, "sweep_kernel_full.txt"), "w") as f:
-        f.write(f"# ncu --set full --clock-control none -k regex:sweep_kernel -c 1 of\n"
-                f"#   python bench.py --steps 1 --warmup 0 --no-cpu-baseline   (tag {tag}; 64-cut launch)\n")
+    with open(out_txt, "w") as f:
+        f.write(f"# ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -c 1 of\n#   {desc}\n")
         f.write(f"kernel: {v[h.index('Kernel Name')] if 'Kernel Name' in h else '?'}\n")
+        f.write(f"cuts per launch              {cuts:>18d}\n")
         for name, label in FULL_METRICS:
             if name in get:
                 f.write(f"{label:28s} {get[name][0]:>18s} {get[name][1]}\n")
@@ -97,31 +93,41 @@ def full(tag, dst):
         return val * mult / to
 
     traffic = {
-        "tag": tag,
-        "kernel": "sweep_kernel (64-cut greedy decomposition of 4096x4096 f32, seed 1)",
+        "kernel": desc,
+        "cuts_per_launch": cuts,
         "dram_bytes_per_launch": num("dram__bytes_read.sum", 1) + num("dram__bytes_write.sum", 1),
         "dram_read_bytes": num("dram__bytes_read.sum", 1),
         "dram_write_bytes": num("dram__bytes_write.sum", 1),
         "duration_s_under_ncu": num("gpu__time_duration.sum", 1),
         "l2_bytes_per_launch": (float(get["lts__t_sectors.sum"][0].replace(",", "")) * 32.0
                                 if "lts__t_sectors.sum" in get else None),
-        "source": f"profiles/{os.path.basename(dst)}/sweep_kernel_full.txt",
+        "source": os.path.relpath(out_txt, ROOT),
     }
-    with open(os.path.join(ROOT, "profiles", "latest_kernel_traffic.json"), "w") as f:
-        json.dump(traffic, f, indent=1)
+    if traffic_json:
+        with open(traffic_json, "w") as f:
+            json.dump(traffic, f, indent=1)
     return traffic
 
 
 def main():
-    tag, _, name = sys.argv[1].partition(":")  # capture tag[:profiles dir name]
-    dst = os.path.join(ROOT, "profiles", name or tag)
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rep", required=True, help="gpurun_out/<name>.ncu-rep (--set full, one sweep_kernel launch)")
+    ap.add_argument("--out", required=True, help="profiles/<round>/<name>.txt")
+    ap.add_argument("--desc", required=True)
+    ap.add_argument("--cuts", type=int, required=True)
+    ap.add_argument("--launches", default="", help="gpurun_out/<launch list>.csv")
+    ap.add_argument("--traffic", action="store_true", help="also write profiles/latest_kernel_traffic.json")
+    args = ap.parse_args()
+    dst = os.path.dirname(os.path.abspath(args.out))
     os.makedirs(dst, exist_ok=True)
-    agg = launches(tag, dst)
-    tr = full(tag, dst)
-    if len(sys.argv) > 2:
-        shutil.copy(sys.argv[2], os.path.join(dst, "bench.json"))
-    print(open(os.path.join(dst, "launches_summary.txt")).read())
-    print(open(os.path.join(dst, "sweep_kernel_full.txt")).read())
+    if args.launches:
+        launches(args.launches, dst, args.desc)
+        print(open(os.path.join(dst, "launches_summary.txt")).read())
+    tr = full(args.rep, args.out, args.desc, args.cuts,
+              os.path.join(ROOT, "profiles", "latest_kernel_traffic.json") if args.traffic else None)
+    print(open(args.out).read())
     print(json.dumps(tr, indent=1))
 
 
