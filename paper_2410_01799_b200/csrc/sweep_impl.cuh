@@ -1201,7 +1201,9 @@ struct DeltaArgs {
   unsigned long long* flipw;  // [sw_all] this pass's (flip mask | s' << 32) words of the band (local_dz == 0)
   int sw_all;                 // words per CTA record (from the largest band; bands one row shorter leave
                               // their last word empty -- written as 0, never left stale)
-  unsigned long long* prof;  // SCB_PROFILE builds: [6] thread-0 cycle sums of the delta pass sections
+#ifdef SCB_PROFILE
+  unsigned long long* prof;  // [6] thread-0 cycle sums of the delta pass sections
+#endif
   long long pitch;
   unsigned rowB;
   int rows_g, nres, Q, NV, P;
@@ -2273,7 +2275,9 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         dl.local_dz = TS ? 1 : 0;
         dl.flipw = p.flipw + (static_cast<size_t>(P & 1) * G + g) * p.sw;
         dl.sw_all = p.sw;
+#ifdef SCB_PROFILE
         dl.prof = prof ? p.prof + static_cast<size_t>(p.G) * 16 + g * 8 : nullptr;
+#endif
         dl.pitch = pitch;
         dl.rowB = static_cast<unsigned>(rowB);
         dl.rows_g = rows_g;
