@@ -14,11 +14,11 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libsigcut_b200.so")
+LIB = os.environ.get("SCB_LIB_OUT") or os.path.join(HERE, "libsigcut_b200.so")  # SCB_LIB_OUT: A/B and profile builds
 SOURCES = ["sweep.cu", "sweep_k_f32m.cu", "sweep_k_f32t.cu", "sweep_k_f64m.cu", "sweep_k_f64t.cu", "sweep_k_vr.cu",
            "ops.cu", "capi.cpp", "ops.cpp"]
 HEADERS = ["sweep.h", "sweep_impl.cuh", "rng.h", "ops.h", "ctx.h"]
-OBJDIR = os.path.join(HERE, "build")
+OBJDIR = os.environ.get("SCB_OBJDIR") or os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-cudart", "static",
