@@ -160,7 +160,7 @@ sc_status sc_set_option(sc_ctx* ctx, const char* name, int64_t value) {
   } const table[] = {{"ctas", &o.ctas},           {"delta", &o.delta},         {"delta_div", &o.delta_div},
                      {"delta_refresh", &o.delta_refresh}, {"two_phase", &o.two_phase}, {"stages", &o.stages},
                      {"res_rows", &o.res_rows},   {"fuse_update", &o.fuse_update}, {"variant", &o.variant},
-                     {"profile", &o.profile},     {"poison", &o.poison}};
+                     {"profile", &o.profile},     {"poison", &o.poison},       {"fast_delta", &o.fast_delta}};
   for (const auto& e : table)
     if (std::strcmp(e.name, name) == 0) {
       *e.field = value;
@@ -178,7 +178,7 @@ sc_status sc_get_option(const sc_ctx* ctx, const char* name, int64_t* value) {
   } const table[] = {{"ctas", o.ctas},           {"delta", o.delta},         {"delta_div", o.delta_div},
                      {"delta_refresh", o.delta_refresh}, {"two_phase", o.two_phase}, {"stages", o.stages},
                      {"res_rows", o.res_rows},   {"fuse_update", o.fuse_update}, {"variant", o.variant},
-                     {"profile", o.profile},     {"poison", o.poison}};
+                     {"profile", o.profile},     {"poison", o.poison},       {"fast_delta", o.fast_delta}};
   for (const auto& e : table)
     if (std::strcmp(e.name, name) == 0) {
       *value = e.v;
@@ -460,6 +460,8 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   const uint64_t nstart = std::max<uint64_t>(w, 1) * p->restarts;
 
   // ---- device arena ----
+  // barrier-free delta passes: one self-tagged record per CTA and pass parity, whole 128-byte lines
+  const int rstride = ((2 * (sw + 1) + 15) / 16) * 16;
   const size_t need = ((m * rowB + 255) & ~size_t(255)) + ((2 * G * rowB * 8 / es + 255) & ~size_t(255)) +
                       ((G * sizeof(scb::Slot) + 255) & ~size_t(255)) + 4 * 256 +
                       ((2 * static_cast<size_t>(tw32) * 8 * scb::kTbStride + 255) & ~size_t(255)) +
@@ -471,7 +473,8 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
                       ((nstart * axw64 * 8 + 255) & ~size_t(255)) +
                       ((std::max<uint64_t>(w, 1) * axw64 * 8 + 255) & ~size_t(255)) +
                       2 * ((static_cast<size_t>(pitch) * 8 + 255) & ~size_t(255)) +
-                      ((2 * static_cast<size_t>(G) * sw * 8 + 255) & ~size_t(255));
+                      ((2 * static_cast<size_t>(G) * sw * 8 + 255) & ~size_t(255)) +
+                      ((2 * static_cast<size_t>(G) * rstride * 8 + 255) & ~size_t(255));
   if (need > ctx->arena_bytes) {
     if (ctx->arena) cudaFree(ctx->arena);
     ctx->arena = nullptr;
@@ -510,6 +513,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   double* zfull = carve<double>(cur, static_cast<size_t>(pitch));
   double* zstate = carve<double>(cur, static_cast<size_t>(pitch));
   unsigned long long* flipw = carve<unsigned long long>(cur, 2 * static_cast<size_t>(G) * sw);
+  unsigned long long* drec = carve<unsigned long long>(cur, 2 * static_cast<size_t>(G) * rstride);
 
   // ---- host staging (pinned) for the start vectors ----
   const size_t t0_bytes = nstart * wn * 8, ax0_bytes = nstart * axw64 * 8;
@@ -575,6 +579,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
     SC_CUDA(ctx, cudaMemsetAsync(tb64, 0, 2 * static_cast<size_t>(tw32) * 8 * scb::kTbStride, st));
   }
   SC_CUDA(ctx, cudaMemsetAsync(tbest, 0, static_cast<size_t>(tw32) * 4, st));
+  SC_CUDA(ctx, cudaMemsetAsync(drec, 0, 2 * static_cast<size_t>(G) * rstride * 8, st));
   SC_CUDA(ctx, cudaMemsetAsync(stats, 0, 64, st));
   if (!sh) SC_CUDA(ctx, cudaMemsetAsync(ctr + 4, 0xff, 4, st));
   if (w > 0) SC_CUDA(ctx, cudaMemsetAsync(S_out, 0, w * wm * 8, st));
@@ -627,6 +632,10 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   kp.zfull = zfull;
   kp.zstate = zstate;
   kp.flipw = flipw;
+  kp.drec = drec;
+  kp.rstride = rstride;
+  // one GPU, matrices, whole rows, one record-polling thread per CTA of the grid
+  kp.fast_delta = (ctx->opts.fast_delta && !tensor && !sh && !vr && cpr == 1 && var.nw * 32 >= G) ? 1 : 0;
   // Sparse delta passes between dense refreshes (matrices, any row length: the dz of
   // flipped rows walks every column chunk).
   kp.delta = ctx->opts.delta ? 1 : 0;

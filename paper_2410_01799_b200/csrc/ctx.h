@@ -33,6 +33,7 @@ struct sc_ctx {
     long long fuse_update = 1;    // rank-1 update fused into the next term's first dot pass
     long long variant = 0;        // kernel tile override nw*1000000 + vpt*10000 + rg*100 + cps (0: auto)
     long long profile = 0;        // print the clock64 breakdown (SCB_PROFILE builds; 2: per CTA)
+    long long fast_delta = 1;     // delta passes exchange self-tagged records instead of meeting at a grid barrier
     long long poison = 0;         // test hook: fill the device arena with NaN bytes before each call
                                   // (any read of a never-written exchange word then shows up)
   } opts;

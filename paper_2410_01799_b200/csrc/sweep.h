@@ -70,6 +70,7 @@ struct Ctl {
   int has_dz;           // this CTA wrote a z partial in a delta pass
   int nfrows, ndz;      // run totals: flipped streamed rows read by delta passes, dz partials written
   int keep;             // t unchanged since the last dot pass: y, s, z stay exactly as cached
+  volatile int zerr;    // an owner warp of this CTA saw a non-finite z (carried into the next record)
   unsigned rank_dz;     // world > 1: ranks whose rank partial holds a delta-pass dz
   double cred[64];  // per-warp partials (axial step: 4 outputs x up to 16 warps)
   int axn[8], axoff[8];  // order-k: n_1..n_{k-1} and their axis-word offsets (shared-memory copies)
@@ -130,6 +131,14 @@ struct KParams {
   int delta_refresh;   // dense refresh every delta_refresh sweeps
   double* zstate;      // [pitch] z = R^T s of the previous pass (owners' columns)
   unsigned long long* flipw;  // [2][G][sw] per-CTA (flip | s' << 32) words of a matrix delta pass, by parity
+  // Barrier-free delta passes (one GPU, matrices, whole rows): every CTA publishes one
+  // self-tagged record per pass -- sw pairs {P << 32 | flip word, P << 32 | s' word} and
+  // one pair {tag | hi(c), tag | lo(c)} with its objective partial (tag bit 31: the CTA saw
+  // a non-finite y, or a non-finite z as an owner in the previous pass) -- and polls
+  // the others' records instead of meeting them at a grid barrier.
+  unsigned long long* drec;   // [2][G][rstride] records by pass parity
+  int rstride;                // u64 words per record (a multiple of 16: whole 128-byte lines)
+  int fast_delta;             // 1: delta passes exchange records (else slots + flip words behind the barrier)
   // wide rows: every row is streamed as cpr column chunks of chunk_cols
   // elements (one stage each); cpr == 1, chunk_cols == pitch otherwise
   int cpr;
@@ -179,8 +188,10 @@ constexpr int kRing = 4;  // dot-partial ring depth (groups)
 
 // Shared-memory carve-up (byte offsets from the dynamic smem base).
 struct Layout {
-  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, ypart, txor, dzmask, ybak, zst, fws, fbuf, total;
+  size_t stage, res, ctl, ring, rred, yrow, tws, uws, zseg, sb, ax, ypart, txor, dzmask, ybak, zst, fws, fbuf, clist, total;
 };
+
+constexpr int kCList = 256;  // flipped-column list entries per gather round (barrier-free delta pass)
 
 constexpr int kFBuf = 64;  // per-warp flipped-row list entries (owners' delta-pass dz)
 
@@ -226,6 +237,8 @@ inline __host__ __device__ Layout make_layout(size_t rowB, int stages, int res_r
   o += static_cast<size_t>(G) * sw * 8;
   L.fbuf = o;  // [nw][kFBuf]: per-warp flipped-row lists (owners)
   o += static_cast<size_t>(nw) * kFBuf * 4;
+  L.clist = o;  // [kCList]: flipped columns of this pass, ascending, bit 31 = the new t bit
+  o += static_cast<size_t>(kCList) * 4;
   L.total = o;
   return L;
 }

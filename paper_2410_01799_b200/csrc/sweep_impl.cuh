@@ -1482,6 +1482,269 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Barrier-free delta pass, front half (one GPU, matrices, whole rows).  The same
+// arithmetic as delta_pass, but the exchange is a chain of self-tagged words with
+// no grid barrier in it:
+//   1. warp 0 polls the pass-tagged t words the owners published, forms t XOR the
+//      previous t and lists the flipped columns in ascending order (prefix scan);
+//   2. every warp updates y of its rows from that list (lanes stride the list, one
+//      L2 round trip per four rows), y_j += 2 sum_c t'_c R[j, c];
+//   3. warp 0 takes s' = sgn(y), the band's objective partial sum_j s_j y_j, and
+//      publishes the CTA's record {flip words, s' words, c partial}, each 64-bit word
+//      carrying the pass index;
+//   4. every thread polls one record: all CTAs need the c partials (the decision is
+//      taken identically everywhere), the column owners also the flip words (fws).
+// The caller then runs the owners' column reduction (col_reduce, delta form) beside
+// the controller decision, exactly as after a barrier pass.  Nobody can run more
+// than one pass ahead: pass P + 1 needs every owner's t word, which needs every
+// CTA's record of pass P.  Records and t words are double-buffered by parity.
+struct FastArgs {
+  const unsigned long long* tw;      // tagged t words of this pass
+  unsigned long long* rec_out;       // this CTA's record of this pass
+  const unsigned long long* rec_in;  // record of CTA 0 of this pass's parity
+  const void* Rrows;                 // global row 0 of this CTA's band
+  unsigned* errp;
+  long long pitch;
+  unsigned res, yrow, s_cur, s_nxt, tws, txor, clist, fws, ctl, rowB;
+  int rows_g, nres, Q, G, sw, rstride, P, owner;
+};
+
+__device__ __forceinline__ void ld_relaxed64x2(const unsigned long long* p, unsigned long long& a,
+                                               unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_relaxed64x2(unsigned long long* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+template <typename E, int NW>
+__device__ __noinline__ void fast_delta_front(const FastArgs a) {
+  constexpr int CT = NW * 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows_g = a.rows_g, nres = a.nres, Q = a.Q, P = a.P;
+  extern __shared__ __align__(128) unsigned char smem[];
+  Ctl* ctl = reinterpret_cast<Ctl*>(smem + a.ctl);
+  double* yrow = reinterpret_cast<double*>(smem + a.yrow);
+  const uint32_t* s_cur = reinterpret_cast<const uint32_t*>(smem + a.s_cur);
+  uint32_t* s_nxt = reinterpret_cast<uint32_t*>(smem + a.s_nxt);
+  uint32_t* tws = reinterpret_cast<uint32_t*>(smem + a.tws);
+  uint32_t* txor = reinterpret_cast<uint32_t*>(smem + a.txor);
+  uint32_t* tprev = txor + Q;
+  uint32_t* clist = reinterpret_cast<uint32_t*>(smem + a.clist);
+  unsigned long long* fws = reinterpret_cast<unsigned long long*>(smem + a.fws);
+  const E* Rg = static_cast<const E*>(a.Rrows);
+
+  // list entries [base, base + kCList) of the flipped columns (ascending), from the
+  // staged t XOR words: lane l covers words 4l..4l+3 of every block of 128
+  auto list_chunk = [&](int base) {
+    int run = 0;
+    for (int i0 = 0; i0 < Q; i0 += 128) {
+      uint32_t xs[4], tn[4];
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 4 * lane + u;
+        xs[u] = i < Q ? txor[i] : 0u;
+        tn[u] = i < Q ? tws[i] : 0u;
+        cnt += __popc(xs[u]);
+      }
+      int inc = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      int pos = run + inc - cnt - base;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t x = xs[u];
+        const int c0 = (i0 + 4 * lane + u) * 32;
+        while (x) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1;
+          if (pos >= 0 && pos < kCList) clist[pos] = static_cast<uint32_t>(c0 + b) | (((tn[u] >> b) & 1u) << 31);
+          ++pos;
+        }
+      }
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    return run;
+  };
+
+  // ---- 1. this pass's t (warp 0) ----
+  if (warp == 0) {
+    for (int i0 = 0; i0 < Q; i0 += 128) {
+      unsigned long long v[4];
+      bool need[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        need[u] = i0 + 4 * lane + u < Q;
+        v[u] = 0ull;
+      }
+      for (;;) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (need[u]) v[u] = ld_relaxed64(a.tw + static_cast<size_t>(i0 + 4 * lane + u) * kTbStride);
+        bool pend = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (need[u]) {
+            if (static_cast<int>(static_cast<unsigned>(v[u] >> 32) - static_cast<unsigned>(P)) >= 0)
+              need[u] = false;
+            else
+              pend = true;
+          }
+        if (!pend) break;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 4 * lane + u;
+        if (i < Q) {
+          const uint32_t tn = static_cast<uint32_t>(v[u]);
+          txor[i] = tn ^ tprev[i];
+          tprev[i] = tn;
+          tws[i] = tn;
+        }
+      }
+    }
+    __syncwarp();
+    const int total = list_chunk(0);
+    if (lane == 0) {
+      ctl->nflip = total;
+      ctl->keep = total == 0;
+      ctl->err_pre[0] = UINT_MAX;
+      ctl->err_pre[1] = UINT_MAX;
+      ctl->err_pre[2] = UINT_MAX;
+    }
+  }
+  consumer_sync(CT);
+  const int nfl = ctl->nflip;
+
+  // ---- 2. y update: warp w takes rows w, w + NW, ... four at a time ----
+  for (int base = 0;;) {
+    const int cn = min(kCList, nfl - base);
+    for (int j0 = warp; j0 < rows_g; j0 += 4 * NW) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k0 = 0; k0 < cn; k0 += 128) {
+        uint32_t e[4];
+        E v[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u * 32 + lane;
+          e[u] = k < cn ? clist[k] : 0xffffffffu;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int jr = j0 + r * NW;
+          const bool ok = jr < rows_g;
+          const bool res = jr < nres;
+          const E* row = res ? reinterpret_cast<const E*>(smem + a.res + static_cast<size_t>(jr) * a.rowB)
+                             : Rg + static_cast<size_t>(ok ? jr : j0) * a.pitch;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t col = e[u] & 0x7fffffffu;
+            v[r][u] = (ok && e[u] != 0xffffffffu) ? (res ? row[col] : __ldcg(row + col)) : E(0);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double d = static_cast<double>(v[r][u]);
+            acc[r] += (e[u] >> 31) ? -d : d;
+          }
+      }
+      const double s = warp_reduce_rows<4>(acc, lane);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (lane == holder_lane<4>(r) && j0 + r * NW < rows_g) yrow[j0 + r * NW] += 2.0 * s;
+    }
+    base += kCList;
+    if (base >= nfl) break;
+    consumer_sync(CT);  // more flips than one list holds: next chunk of the list
+    if (warp == 0) list_chunk(base);
+    consumer_sync(CT);
+  }
+  consumer_sync(CT);
+
+  // ---- 3. s' = sgn(y), flips, objective partial; publish the record (warp 0) ----
+  if (warp == 0) {
+    const unsigned long long tag = static_cast<unsigned long long>(static_cast<unsigned>(P)) << 32;
+    const int swl = (rows_g + 31) / 32;
+    bool bad = false;
+    int nfr = 0;
+    for (int w = 0; w < a.sw; ++w) {
+      const int j = w * 32 + lane;
+      const bool ok = j < rows_g;
+      const double y = ok ? yrow[j] : 0.0;
+      bad |= ok && !isfinite(y);
+      const uint32_t sn = __ballot_sync(0xffffffffu, ok && y < 0.0);
+      const uint32_t f = w < swl ? (sn ^ s_cur[w]) : 0u;  // bits past rows_g are zero in both
+      if (lane == 0) {
+        s_nxt[w] = sn;
+        st_relaxed64x2(a.rec_out + 2 * w, tag | f, tag | sn);
+      }
+      nfr += __popc(f);
+    }
+    // this CTA's c partial: sum_i s_i y_i in row order (lane-strided, fixed tree)
+    double cl = 0.0;
+    for (int j = lane; j < rows_g; j += 32) cl += flipd(yrow[j], ((s_cur[j >> 5] >> (j & 31)) & 1u) << 31);
+    cl = warp_sum(cl);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      if (bad) atomicMin(a.errp + ERR_Y, static_cast<unsigned>(P));
+      const unsigned long long tagc = tag | ((bad || ctl->zerr) ? (1ull << 63) : 0ull);
+      st_relaxed64x2(a.rec_out + 2 * a.sw, tagc | static_cast<uint32_t>(__double2hiint(cl)),
+                     tagc | static_cast<uint32_t>(__double2loint(cl)));
+      ctl->nfrows += nfr;  // flipped rows the owners read (traffic accounting)
+    }
+  }
+
+  // ---- 4. everyone's record: c partials (all CTAs), flip words (owners) ----
+  {
+    const unsigned uP = static_cast<unsigned>(P);
+    const int nfw = a.owner ? a.G * a.sw : 0;
+    bool nc = tid < a.G, nf = tid < nfw;
+    const int gq = nf ? tid / a.sw : 0;
+    const unsigned long long* pc = a.rec_in + static_cast<size_t>(nc ? tid : 0) * a.rstride + 2 * a.sw;
+    const unsigned long long* pf = a.rec_in + static_cast<size_t>(gq) * a.rstride + 2 * (tid - gq * a.sw);
+    double cmine = 0.0;
+    bool flag = false;
+    while (nc || nf) {
+      unsigned long long c0 = 0, c1 = 0, f0 = 0, f1 = 0;
+      if (nc) ld_relaxed64x2(pc, c0, c1);
+      if (nf) ld_relaxed64x2(pf, f0, f1);
+      if (nc && (static_cast<unsigned>(c0 >> 32) & 0x7fffffffu) == uP &&
+          (static_cast<unsigned>(c1 >> 32) & 0x7fffffffu) == uP) {
+        nc = false;
+        cmine = __hiloint2double(static_cast<int>(static_cast<uint32_t>(c0)), static_cast<int>(static_cast<uint32_t>(c1)));
+        flag = (c0 >> 63) != 0ull;
+      }
+      if (nf && static_cast<unsigned>(f0 >> 32) == uP && static_cast<unsigned>(f1 >> 32) == uP) {
+        nf = false;
+        fws[tid] = static_cast<unsigned long long>(static_cast<uint32_t>(f0)) | (f1 << 32);
+      }
+    }
+    for (int idx = tid + CT; idx < nfw; idx += CT) {  // tall bands: more flip words than threads
+      const int g2 = idx / a.sw;
+      const unsigned long long* q = a.rec_in + static_cast<size_t>(g2) * a.rstride + 2 * (idx - g2 * a.sw);
+      unsigned long long f0, f1;
+      do {
+        ld_relaxed64x2(q, f0, f1);
+      } while (static_cast<unsigned>(f0 >> 32) != uP || static_cast<unsigned>(f1 >> 32) != uP);
+      fws[idx] = static_cast<unsigned long long>(static_cast<uint32_t>(f0)) | (f1 << 32);
+    }
+    const double cs = warp_sum(cmine);
+    if (lane == 0) {
+      ctl->cred[warp] = cs;
+      ctl->nred[warp] = 0.0;
+    }
+    if (flag) ctl->err_pre[0] = uP;  // some CTA saw a non-finite value: every CTA stops at this pass
+  }
+  consumer_sync(CT);
+}
+
+// ---------------------------------------------------------------------------
 // Order-k tensors (axial_run, search.hpp:191-213) on the matrix view
 // M = n_0 x N', N' = n_1 ... n_{k-1} (row-major, last axis fastest).  Axis 0 of
 // a sweep is the dot pass (y = M kron(s_1..s_{k-1}), s_0 = sgn(y)); its column
@@ -1771,6 +2034,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     ctl->since_dense = 0;
     ctl->has_dz = 0;
     ctl->keep = 0;
+    ctl->zerr = 0;
     ctl->term = 0;
     ctl->restart = 0;
     ctl->tsel = -1;
@@ -2074,7 +2338,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
             z = zs + z;
           __stcg(p.zstate + col, z);
         }
-        if (valid && !isfinite(z)) atomicMin(const_cast<unsigned*>(errp) + ERR_Z, static_cast<unsigned>(P));
+        if (valid && !isfinite(z)) {
+          atomicMin(const_cast<unsigned*>(errp) + ERR_Z, static_cast<unsigned>(P));
+          ctl->zerr = 1;
+        }
         if (mode == 1) {  // order-k: Z = M^T s_0 for the axial step
           if (valid) __stcg(p.zfull + col, z);
         } else {
@@ -2148,6 +2415,47 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     const uint32_t* s_upd = sb + ctl->best * p.sw;
     const double alpha = ctl->alpha;
 
+    // Barrier-free delta pass (one GPU, matrices, whole rows): t staging, y update,
+    // signs and the record exchange in one lean function; then the owners' column
+    // reduction beside the decision, as after a barrier pass.
+    const bool fast = !TS && !MR && (kind & F_DELTA) && p.fast_delta;
+    if (fast) {
+      FastArgs fa;
+      fa.tw = p.tb64 + static_cast<size_t>(ctl->tsel) * p.Q * kTbStride;
+      fa.rec_in = p.drec + static_cast<size_t>(P & 1) * G * p.rstride;
+      fa.rec_out = const_cast<unsigned long long*>(fa.rec_in) + static_cast<size_t>(g) * p.rstride;
+      fa.Rrows = R + static_cast<size_t>(r0) * pitch;
+      fa.errp = const_cast<unsigned*>(errp);
+      fa.pitch = pitch;
+      fa.res = static_cast<unsigned>(L.res);
+      fa.yrow = static_cast<unsigned>(L.yrow);
+      fa.s_cur = static_cast<unsigned>(reinterpret_cast<const unsigned char*>(s_cur) - smem);
+      fa.s_nxt = static_cast<unsigned>(reinterpret_cast<unsigned char*>(s_nxt) - smem);
+      fa.tws = static_cast<unsigned>(L.tws);
+      fa.txor = static_cast<unsigned>(L.txor);
+      fa.clist = static_cast<unsigned>(L.clist);
+      fa.fws = static_cast<unsigned>(L.fws);
+      fa.ctl = static_cast<unsigned>(L.ctl);
+      fa.rowB = static_cast<unsigned>(rowB);
+      fa.rows_g = rows_g;
+      fa.nres = nres;
+      fa.Q = p.Q;
+      fa.G = G;
+      fa.sw = p.sw;
+      fa.rstride = p.rstride;
+      fa.P = P;
+      fa.owner = g < p.Q ? 1 : 0;
+      fast_delta_front<E, NW>(fa);
+      if (g == 0 && tid == 32) nflip_sum += static_cast<unsigned>(ctl->nflip);
+      if (g == 0 && tid == 0) ++dot_passes[1];
+      gcount += static_cast<unsigned>((rows_g + RG - 1) / RG);
+      if (prof && tid == 0) {
+        const long long t = clock64();
+        pacc[1] += t - t_pass0;
+        pten[5] += t - t_pass0;
+        t_pass0 = t;
+      }
+    } else {
     // ---- stage the sign words of this pass in shared memory ----
     if (kind & F_DOT) {
       if (ctl->tsel < 0) {
@@ -2448,6 +2756,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       }
     }
     consumer_sync(CT);
+    }  // !fast
     if (MR && p.world > 1) {
       // Rank stage: this rank's column partials -> one rank partial zr (local
       // owners), its slots -> one rank slot; then the cross-rank barrier, after
