@@ -125,6 +125,8 @@ sc_status sc_create(sc_ctx** out, int device) {
   ctx->num_sms = prop.multiProcessorCount;
   ctx->smem_optin = prop.sharedMemPerBlockOptin;
   ctx->smem_per_sm = prop.sharedMemPerMultiprocessor;
+  ctx->l2_persist_max = static_cast<size_t>(prop.persistingL2CacheMaxSize);
+  ctx->l2_window_max = static_cast<size_t>(prop.accessPolicyMaxWindowSize);
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
     delete ctx;
@@ -160,7 +162,8 @@ sc_status sc_set_option(sc_ctx* ctx, const char* name, int64_t value) {
   } const table[] = {{"ctas", &o.ctas},           {"delta", &o.delta},         {"delta_div", &o.delta_div},
                      {"delta_refresh", &o.delta_refresh}, {"two_phase", &o.two_phase}, {"stages", &o.stages},
                      {"res_rows", &o.res_rows},   {"fuse_update", &o.fuse_update}, {"variant", &o.variant},
-                     {"profile", &o.profile},     {"poison", &o.poison},       {"fast_delta", &o.fast_delta}};
+                     {"profile", &o.profile},     {"poison", &o.poison},       {"fast_delta", &o.fast_delta},
+                     {"l2_persist", &o.l2_persist}};
   for (const auto& e : table)
     if (std::strcmp(e.name, name) == 0) {
       *e.field = value;
@@ -178,7 +181,8 @@ sc_status sc_get_option(const sc_ctx* ctx, const char* name, int64_t* value) {
   } const table[] = {{"ctas", o.ctas},           {"delta", o.delta},         {"delta_div", o.delta_div},
                      {"delta_refresh", o.delta_refresh}, {"two_phase", o.two_phase}, {"stages", o.stages},
                      {"res_rows", o.res_rows},   {"fuse_update", o.fuse_update}, {"variant", o.variant},
-                     {"profile", o.profile},     {"poison", o.poison},       {"fast_delta", o.fast_delta}};
+                     {"profile", o.profile},     {"poison", o.poison},       {"fast_delta", o.fast_delta},
+                     {"l2_persist", o.l2_persist}};
   for (const auto& e : table)
     if (std::strcmp(e.name, name) == 0) {
       *value = e.v;
@@ -354,10 +358,34 @@ sc_status run_decompose(sc_ctx* ctx, const sc_problem* p, sc_result* res, const 
   // the process: always the device's opt-in limit, so concurrent engines never
   // lower it under each other's launches (the launch passes the real size)
   SC_CUDA(ctx, scb::set_smem_limit(S.var, ctx->smem_optin));
+  // Option l2_persist: the remainder R as a persisting-L2 access window for the launch, so
+  // the delta passes' latency-critical gathers are not evicted to DRAM by the exchange
+  // buffers and write-backs (hit ratio scaled down when R exceeds the carve-out).
+  const size_t r_bytes = S.m * S.rowB;
+  const bool persist = ctx->opts.l2_persist && ctx->l2_persist_max > 0 && ctx->l2_window_max > 0 && r_bytes > 0;
+  if (persist) {
+    const size_t carve = ctx->l2_persist_max;
+    SC_CUDA(ctx, cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+    cudaStreamAttrValue av{};
+    av.accessPolicyWindow.base_ptr = S.dR;
+    av.accessPolicyWindow.num_bytes = std::min(r_bytes, ctx->l2_window_max);
+    av.accessPolicyWindow.hitRatio =
+        static_cast<float>(std::min(1.0, static_cast<double>(carve) / static_cast<double>(av.accessPolicyWindow.num_bytes)));
+    av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    SC_CUDA(ctx, cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &av));
+  }
   SC_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   SC_CUDA(ctx, scb::launch_sweep(S.var, S.kp, S.smem, ctx->stream));
   SC_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
-  return finish_run(ctx, p, res, S);
+  if (persist) {
+    cudaStreamAttrValue av{};
+    av.accessPolicyWindow.num_bytes = 0;
+    SC_CUDA(ctx, cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &av));
+  }
+  const sc_status fin = finish_run(ctx, p, res, S);
+  if (persist) cudaCtxResetPersistingL2Cache();
+  return fin;
 }
 
 sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc_ctx::Shard* sh, RunState& S,
@@ -635,7 +663,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   kp.drec = drec;
   kp.rstride = rstride;
   // one GPU, matrices, whole rows, one record-polling thread per CTA of the grid
-  kp.fast_delta = (ctx->opts.fast_delta && !tensor && !sh && !vr && cpr == 1 && var.nw * 32 >= G) ? 1 : 0;
+  kp.fast_delta = (ctx->opts.fast_delta && !tensor && !sh && !vr && cpr == 1 && var.nw * 32 >= G && Q <= 4 * G) ? 1 : 0;
   // Sparse delta passes between dense refreshes (matrices, any row length: the dz of
   // flipped rows walks every column chunk).
   kp.delta = ctx->opts.delta ? 1 : 0;
@@ -672,8 +700,8 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   const bool prof = ctx->opts.profile != 0;
   unsigned long long* dprof = nullptr;
   if (prof) {
-    SC_CUDA(ctx, cudaMalloc(&dprof, static_cast<size_t>(G) * 24 * 8));
-    SC_CUDA(ctx, cudaMemsetAsync(dprof, 0, static_cast<size_t>(G) * 24 * 8, st));
+    SC_CUDA(ctx, cudaMalloc(&dprof, static_cast<size_t>(G) * (32 + 128) * 8));
+    SC_CUDA(ctx, cudaMemsetAsync(dprof, 0, static_cast<size_t>(G) * (32 + 128) * 8, st));
   }
   kp.prof = dprof;
   // SearchDiagnostics::sweep_values of term 0, every restart (the host keeps the winner's)
@@ -759,15 +787,43 @@ sc_status finish_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, RunState&
   res->kernel_ms = kms;
   res->kernel_launches = 1;
   if (prof) {
-    std::vector<unsigned long long> hp(static_cast<size_t>(G) * 24);
+    std::vector<unsigned long long> hp(static_cast<size_t>(G) * (32 + 128));
     cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost);
     {
-      double d[6] = {0, 0, 0, 0, 0, 0};
+      double d[16] = {0};
       for (int g = 0; g < G; ++g)
-        for (int i = 0; i < 6; ++i) d[i] += static_cast<double>(hp[static_cast<size_t>(G) * 16 + g * 8 + i]);
+        for (int i = 0; i < 16; ++i) d[i] += static_cast<double>(hp[static_cast<size_t>(G) * 16 + g * 16 + i]);
       const double nd = std::max<double>(1.0, static_cast<double>(h_stats[3])) * G;
-      std::fprintf(stderr, "[scb prof delta] per delta pass per CTA: fliplists %.0f gathers %.0f sync %.0f signs %.0f dz %.0f | CTAs with dz per pass %.2f\n",
-                   d[0] / nd, d[1] / nd, d[2] / nd, d[3] / nd, d[4] / nd, d[5] / std::max<double>(1.0, static_cast<double>(h_stats[3])));
+      if (S.kp.fast_delta) {  // clock64 stamps of eight consecutive passes: spread over the CTAs
+        static const char* nm[13] = {"t arrived", "list done", "gather done", "record out", "c reduced", "", "", "", "flips staged", "z partial", "t published", "rows counted", "rows listed"};
+        for (int ps = 0; ps < 8; ++ps) {
+          unsigned long long base = ~0ull;
+          for (int g = 0; g < G; ++g) {
+            const unsigned long long v = hp[static_cast<size_t>(G) * 32 + (static_cast<size_t>(g) * 8 + ps) * 16 + 0];
+            if (v) base = std::min(base, v);
+          }
+          if (base == ~0ull) continue;
+          std::fprintf(stderr, "[scb stamps] pass +%d:", ps);
+          for (int k = 0; k < 13; ++k) {
+            if (!nm[k][0]) continue;
+            double mn = 1e300, mx = -1e300, sum = 0; int cnt = 0;
+            for (int g = 0; g < G; ++g) {
+              const unsigned long long v = hp[static_cast<size_t>(G) * 32 + (static_cast<size_t>(g) * 8 + ps) * 16 + k];
+              if (!v) continue;
+              const double d = static_cast<double>(static_cast<long long>(v - base));
+              mn = std::min(mn, d); mx = std::max(mx, d); sum += d; ++cnt;
+            }
+            if (cnt) std::fprintf(stderr, " %s %.0f/%.0f/%.0f", nm[k], mn, sum / cnt, mx);
+          }
+          std::fprintf(stderr, "\n");
+        }
+      }
+      if (S.kp.fast_delta)
+        std::fprintf(stderr, "[scb prof fast delta] per delta pass per CTA: thread 0: t wait %.0f list+sync %.0f gathers+bar %.0f signs+publish %.0f c poll %.0f decision %.0f | thread 32: flip poll+bar %.0f list+gather %.0f final+publish %.0f\n",
+                     d[0] / nd, d[1] / nd, d[2] / nd, d[3] / nd, d[4] / nd, d[7] / nd, d[8] / nd, d[9] / nd, d[10] / nd);
+      else
+        std::fprintf(stderr, "[scb prof delta] per delta pass per CTA: fliplists %.0f gathers %.0f sync %.0f signs %.0f dz %.0f | CTAs with dz per pass %.2f | column reduction (thread 32) %.0f decision %.0f\n",
+                     d[0] / nd, d[1] / nd, d[2] / nd, d[3] / nd, d[4] / nd, d[5] / std::max<double>(1.0, static_cast<double>(h_stats[3])), d[6] / nd, d[7] / nd);
     }
     cudaFree(dprof);
     double acc[16] = {0};

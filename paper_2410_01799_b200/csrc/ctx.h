@@ -17,6 +17,7 @@ struct sc_ctx {
   int num_sms = 0;
   size_t smem_optin = 0;
   size_t smem_per_sm = 0;
+  size_t l2_persist_max = 0, l2_window_max = 0;  // persisting-L2 carve-out and access-window limits
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool borrowed = false;  // stream / events belong to a parent context (emulated ranks)
@@ -34,6 +35,7 @@ struct sc_ctx {
     long long variant = 0;        // kernel tile override nw*1000000 + vpt*10000 + rg*100 + cps (0: auto)
     long long profile = 0;        // print the clock64 breakdown (SCB_PROFILE builds; 2: per CTA)
     long long fast_delta = 1;     // delta passes exchange self-tagged records instead of meeting at a grid barrier
+    long long l2_persist = 0;     // R as a persisting-L2 access window during the launch
     long long poison = 0;         // test hook: fill the device arena with NaN bytes before each call
                                   // (any read of a never-written exchange word then shows up)
   } opts;

@@ -47,6 +47,22 @@ struct UpdArgs {
   unsigned uws, s_upd;  // smem offsets: t of the update (Q words), s of the update (band words)
 };
 
+// Pass-invariant operands of the barrier-free delta pass (filled once per launch).
+struct FastConst {
+  const void* Rrows;  // global row 0 of the CTA's band
+  const void* R;
+  unsigned long long* drec;
+  unsigned long long* tb64;
+  double* zstate;
+  unsigned* errp;
+  unsigned long long* prof;  // [16] cycle sums (SCB_PROFILE builds) or nullptr
+  long long pitch;
+  unsigned res, yrow, sb, tws, txor, clist, fws, fbuf, zseg, rowB;  // shared-memory offsets, row bytes
+  int rows_g, nres, Q, G, sw, rstride, n, g, rows_base, rows_rem;
+  int nls;  // 32-column words this CTA owns (words g, g + G, ...; 0: not an owner)
+  int shared_list;  // 1: the owners' flipped-row list is built by col_reduce (many flip words)
+};
+
 // Per-CTA controller block in shared memory.
 struct Ctl {
   unsigned long long full[kMaxStages];   // TMA -> dot warps
@@ -57,6 +73,7 @@ struct Ctl {
   volatile int aborted;  // world > 1: a cross-rank spin of this CTA timed out / saw the abort word
   volatile int upd_done;  // fused-update dot pass P: phase A's write-back is complete (P + 1)
   UpdArgs ua;
+  FastConst fc;
   volatile int kind_ring[4];
   // controller state (thread 0 writes, consumers read after a named barrier)
   int kind, pp, term, restart, tsel, utsel, best_tsel, best_sweeps, best_restart;

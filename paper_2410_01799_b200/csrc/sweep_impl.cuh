@@ -1482,33 +1482,24 @@ __device__ __noinline__ void delta_pass(const DeltaArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Barrier-free delta pass, front half (one GPU, matrices, whole rows).  The same
-// arithmetic as delta_pass, but the exchange is a chain of self-tagged words with
-// no grid barrier in it:
+// Barrier-free delta pass (one GPU, matrices, whole rows).  The same arithmetic as
+// delta_pass + the owners' column reduction, but the exchange is a chain of
+// self-tagged words with no grid barrier in it and the CTA meets only twice:
 //   1. warp 0 polls the pass-tagged t words the owners published, forms t XOR the
 //      previous t and lists the flipped columns in ascending order (prefix scan);
 //   2. every warp updates y of its rows from that list (lanes stride the list, one
 //      L2 round trip per four rows), y_j += 2 sum_c t'_c R[j, c];
-//   3. warp 0 takes s' = sgn(y), the band's objective partial sum_j s_j y_j, and
-//      publishes the CTA's record {flip words, s' words, c partial}, each 64-bit word
-//      carrying the pass index;
-//   4. every thread polls one record: all CTAs need the c partials (the decision is
-//      taken identically everywhere), the column owners also the flip words (fws).
-// The caller then runs the owners' column reduction (col_reduce, delta form) beside
-// the controller decision, exactly as after a barrier pass.  Nobody can run more
-// than one pass ahead: pass P + 1 needs every owner's t word, which needs every
-// CTA's record of pass P.  Records and t words are double-buffered by parity.
-struct FastArgs {
-  const unsigned long long* tw;      // tagged t words of this pass
-  unsigned long long* rec_out;       // this CTA's record of this pass
-  const unsigned long long* rec_in;  // record of CTA 0 of this pass's parity
-  const void* Rrows;                 // global row 0 of this CTA's band
-  unsigned* errp;
-  long long pitch;
-  unsigned res, yrow, s_cur, s_nxt, tws, txor, clist, fws, ctl, rowB;
-  int rows_g, nres, Q, G, sw, rstride, P, owner;
-};
-
+//   3. warp 0 takes s' = sgn(y) and publishes the band's {flip, s'} words, then its
+//      objective partial sum_j s_j y_j -- every 64-bit word carries the pass index;
+//   4. warps 1.. of the column owners poll every CTA's flip words, list the flipped
+//      rows (each warp extracts its own slice of the one ascending list, no CTA-wide
+//      step), add 2 s'_i R[i, cols] to their z state and publish t' = sgn(z), tagged
+//      for the next pass; meanwhile warp 0 polls the c partials and reduces them in
+//      the fixed order of the barrier passes, and thread 0 takes the decision.
+// Nobody can run more than one pass ahead: pass P + 1 needs every owner's t word,
+// which needs every CTA's record of pass P.  Records and t words are
+// double-buffered by parity.  Pass-invariant operands sit in shared memory
+// (Ctl::fc), so the call passes four scalars.
 __device__ __forceinline__ void ld_relaxed64x2(const unsigned long long* p, unsigned long long& a,
                                                unsigned long long& b) {
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
@@ -1517,62 +1508,72 @@ __device__ __forceinline__ void st_relaxed64x2(unsigned long long* p, unsigned l
   asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
+#ifdef SCB_POLL_SLEEP
+#define SCB_POLL_BACKOFF() __nanosleep(SCB_POLL_SLEEP)
+#else
+#define SCB_POLL_BACKOFF() do {} while (0)
+#endif
+constexpr int kStamp0 = 3000;  // SCB_PROFILE builds: passes [kStamp0, kStamp0 + 8) record clock64 stamps per CTA
 template <typename E, int NW>
-__device__ __noinline__ void fast_delta_front(const FastArgs a) {
+__device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, const int tsel, const int cur_nxt) {
   constexpr int CT = NW * 32;
+  constexpr int NP = NW - 1;  // owner warps (warp 0 runs the objective reduction and the decision)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rows_g = a.rows_g, nres = a.nres, Q = a.Q, P = a.P;
   extern __shared__ __align__(128) unsigned char smem[];
-  Ctl* ctl = reinterpret_cast<Ctl*>(smem + a.ctl);
-  double* yrow = reinterpret_cast<double*>(smem + a.yrow);
-  const uint32_t* s_cur = reinterpret_cast<const uint32_t*>(smem + a.s_cur);
-  uint32_t* s_nxt = reinterpret_cast<uint32_t*>(smem + a.s_nxt);
-  uint32_t* tws = reinterpret_cast<uint32_t*>(smem + a.tws);
-  uint32_t* txor = reinterpret_cast<uint32_t*>(smem + a.txor);
+  Ctl* ctl = reinterpret_cast<Ctl*>(smem + ctl_off);
+  const FastConst& F = ctl->fc;
+  const int rows_g = F.rows_g, nres = F.nres, Q = F.Q, G = F.G, sw = F.sw;
+  const unsigned uP = static_cast<unsigned>(P);
+  double* yrow = reinterpret_cast<double*>(smem + F.yrow);
+  const uint32_t* s_cur = reinterpret_cast<const uint32_t*>(smem + F.sb) + (cur_nxt & 3) * sw;
+  uint32_t* s_nxt = reinterpret_cast<uint32_t*>(smem + F.sb) + (cur_nxt >> 2) * sw;
+  uint32_t* tws = reinterpret_cast<uint32_t*>(smem + F.tws);
+  uint32_t* txor = reinterpret_cast<uint32_t*>(smem + F.txor);
   uint32_t* tprev = txor + Q;
-  uint32_t* clist = reinterpret_cast<uint32_t*>(smem + a.clist);
-  unsigned long long* fws = reinterpret_cast<unsigned long long*>(smem + a.fws);
-  const E* Rg = static_cast<const E*>(a.Rrows);
+  uint32_t* clist = reinterpret_cast<uint32_t*>(smem + F.clist);
+  unsigned long long* fws = reinterpret_cast<unsigned long long*>(smem + F.fws);
+  const E* Rg = static_cast<const E*>(F.Rrows);
+  const unsigned long long* rec_in = F.drec + static_cast<size_t>(P & 1) * G * F.rstride;
+#ifdef SCB_PROFILE
+  long long ft0 = clock64();
+#define SCB_FT(k) do { if (F.prof && (tid == 0 || tid == 32)) { const long long t1_ = clock64(); if (tid == ((k) >= 8 ? 32 : 0)) { F.prof[k] += t1_ - ft0; \
+    if (P >= kStamp0 && P < kStamp0 + 8) F.prof[static_cast<size_t>(G - F.g) * 16 + (static_cast<size_t>(F.g) * 8 + (P - kStamp0)) * 16 + (k)] = t1_; } ft0 = t1_; } } while (0)
+#else
+#define SCB_FT(k) do {} while (0)
+#endif
 
-  // list entries [base, base + kCList) of the flipped columns (ascending), from the
-  // staged t XOR words: lane l covers words 4l..4l+3 of every block of 128
-  auto list_chunk = [&](int base) {
-    int run = 0;
-    for (int i0 = 0; i0 < Q; i0 += 128) {
-      uint32_t xs[4], tn[4];
-      int cnt = 0;
+  // list entries [base, base + kCList) of the flipped columns (ascending): lane l
+  // covers words 4l..4l+3 of every block of 128 t words
+  auto emit = [&](const uint32_t (&xs)[4], const uint32_t (&tn)[4], int i0, int base, int run) -> int {
+    int cnt = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + 4 * lane + u;
-        xs[u] = i < Q ? txor[i] : 0u;
-        tn[u] = i < Q ? tws[i] : 0u;
-        cnt += __popc(xs[u]);
-      }
-      int inc = cnt;
+    for (int u = 0; u < 4; ++u) cnt += __popc(xs[u]);
+    int inc = cnt;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-      }
-      int pos = run + inc - cnt - base;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        uint32_t x = xs[u];
-        const int c0 = (i0 + 4 * lane + u) * 32;
-        while (x) {
-          const int b = __ffs(x) - 1;
-          x &= x - 1;
-          if (pos >= 0 && pos < kCList) clist[pos] = static_cast<uint32_t>(c0 + b) | (((tn[u] >> b) & 1u) << 31);
-          ++pos;
-        }
-      }
-      run += __shfl_sync(0xffffffffu, inc, 31);
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
     }
-    return run;
+    int pos = run + inc - cnt - base;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t x = xs[u];
+      const int c0 = (i0 + 4 * lane + u) * 32;
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        if (pos >= 0 && pos < kCList) clist[pos] = static_cast<uint32_t>(c0 + b) | (((tn[u] >> b) & 1u) << 31);
+        ++pos;
+      }
+    }
+    return run + __shfl_sync(0xffffffffu, inc, 31);
   };
 
   // ---- 1. this pass's t (warp 0) ----
   if (warp == 0) {
+    const unsigned long long* tw = F.tb64 + static_cast<size_t>(tsel) * Q * kTbStride;
+    int run = 0;
+#pragma unroll 1
     for (int i0 = 0; i0 < Q; i0 += 128) {
       unsigned long long v[4];
       bool need[4];
@@ -1584,72 +1585,79 @@ __device__ __noinline__ void fast_delta_front(const FastArgs a) {
       for (;;) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (need[u]) v[u] = ld_relaxed64(a.tw + static_cast<size_t>(i0 + 4 * lane + u) * kTbStride);
+          if (need[u]) v[u] = ld_relaxed64(tw + static_cast<size_t>(i0 + 4 * lane + u) * kTbStride);
         bool pend = false;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if (need[u]) {
-            if (static_cast<int>(static_cast<unsigned>(v[u] >> 32) - static_cast<unsigned>(P)) >= 0)
+            if (static_cast<int>(static_cast<unsigned>(v[u] >> 32) - uP) >= 0)
               need[u] = false;
             else
               pend = true;
           }
         if (!pend) break;
       }
+      uint32_t xs[4], tn[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 4 * lane + u;
+        tn[u] = static_cast<uint32_t>(v[u]);
+        xs[u] = i < Q ? (tn[u] ^ tprev[i]) : 0u;
+      }
+      if (i0 == 0) SCB_FT(0);
+      run = emit(xs, tn, i0, 0, run);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = i0 + 4 * lane + u;
         if (i < Q) {
-          const uint32_t tn = static_cast<uint32_t>(v[u]);
-          txor[i] = tn ^ tprev[i];
-          tprev[i] = tn;
-          tws[i] = tn;
+          txor[i] = xs[u];
+          tprev[i] = tn[u];
+          tws[i] = tn[u];
         }
       }
     }
-    __syncwarp();
-    const int total = list_chunk(0);
     if (lane == 0) {
-      ctl->nflip = total;
-      ctl->keep = total == 0;
+      ctl->nflip = run;
+      ctl->keep = run == 0;
       ctl->err_pre[0] = UINT_MAX;
       ctl->err_pre[1] = UINT_MAX;
       ctl->err_pre[2] = UINT_MAX;
     }
   }
   consumer_sync(CT);
+  SCB_FT(1);
   const int nfl = ctl->nflip;
 
   // ---- 2. y update: warp w takes rows w, w + NW, ... four at a time ----
   for (int base = 0;;) {
     const int cn = min(kCList, nfl - base);
+#pragma unroll 1
     for (int j0 = warp; j0 < rows_g; j0 += 4 * NW) {
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int k0 = 0; k0 < cn; k0 += 128) {
-        uint32_t e[4];
-        E v[4][4];
+#pragma unroll 1
+      for (int k0 = 0; k0 < cn; k0 += 64) {  // two list entries per lane and round, four rows: 8 loads in flight
+        uint32_t e[2];
+        E v[4][2];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 2; ++u) {
           const int k = k0 + u * 32 + lane;
           e[u] = k < cn ? clist[k] : 0xffffffffu;
         }
+        // (every row is current in global R; SMEM-resident rows are read from L2 like the
+        // rest -- one load path keeps this once-per-pass code short)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int jr = j0 + r * NW;
           const bool ok = jr < rows_g;
-          const bool res = jr < nres;
-          const E* row = res ? reinterpret_cast<const E*>(smem + a.res + static_cast<size_t>(jr) * a.rowB)
-                             : Rg + static_cast<size_t>(ok ? jr : j0) * a.pitch;
+          const E* row = Rg + static_cast<size_t>(ok ? jr : j0) * F.pitch;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t col = e[u] & 0x7fffffffu;
-            v[r][u] = (ok && e[u] != 0xffffffffu) ? (res ? row[col] : __ldcg(row + col)) : E(0);
-          }
+          for (int u = 0; u < 2; ++u)
+            v[r][u] = (ok && e[u] != 0xffffffffu) ? __ldcg(row + (e[u] & 0x7fffffffu)) : E(0);
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < 2; ++u) {
             const double d = static_cast<double>(v[r][u]);
             acc[r] += (e[u] >> 31) ? -d : d;
           }
@@ -1661,87 +1669,219 @@ __device__ __noinline__ void fast_delta_front(const FastArgs a) {
     }
     base += kCList;
     if (base >= nfl) break;
-    consumer_sync(CT);  // more flips than one list holds: next chunk of the list
-    if (warp == 0) list_chunk(base);
+    consumer_sync(CT);  // more flips than one list holds: the next chunk of the list
+    if (warp == 0) {
+      int run = 0;
+#pragma unroll 1
+      for (int i0 = 0; i0 < Q; i0 += 128) {
+        uint32_t xs[4], tn[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + 4 * lane + u;
+          xs[u] = i < Q ? txor[i] : 0u;
+          tn[u] = i < Q ? tws[i] : 0u;
+        }
+        run = emit(xs, tn, i0, base, run);
+      }
+    }
     consumer_sync(CT);
   }
-  consumer_sync(CT);
+  // only warp 0 waits for every row's y; the other warps go on to the records
+  if (warp != 0) {
+    asm volatile("bar.arrive 3, %0;" ::"r"(CT) : "memory");
+  } else {
+    asm volatile("bar.sync 3, %0;" ::"r"(CT) : "memory");
+  }
+  SCB_FT(2);
 
-  // ---- 3. s' = sgn(y), flips, objective partial; publish the record (warp 0) ----
   if (warp == 0) {
-    const unsigned long long tag = static_cast<unsigned long long>(static_cast<unsigned>(P)) << 32;
-    const int swl = (rows_g + 31) / 32;
+    // ---- 3. s' = sgn(y), flips, then the objective partial; publish both ----
+    unsigned long long* rec_out = const_cast<unsigned long long*>(rec_in) + static_cast<size_t>(F.g) * F.rstride;
+    const unsigned long long tag = static_cast<unsigned long long>(uP) << 32;
     bool bad = false;
     int nfr = 0;
-    for (int w = 0; w < a.sw; ++w) {
+#pragma unroll 1
+    for (int w = 0; w < sw; ++w) {
       const int j = w * 32 + lane;
       const bool ok = j < rows_g;
       const double y = ok ? yrow[j] : 0.0;
       bad |= ok && !isfinite(y);
       const uint32_t sn = __ballot_sync(0xffffffffu, ok && y < 0.0);
-      const uint32_t f = w < swl ? (sn ^ s_cur[w]) : 0u;  // bits past rows_g are zero in both
+      const uint32_t f = sn ^ s_cur[w];  // bits past rows_g are zero in both
       if (lane == 0) {
+        st_relaxed64x2(rec_out + 2 * w, tag | f, tag | sn);
         s_nxt[w] = sn;
-        st_relaxed64x2(a.rec_out + 2 * w, tag | f, tag | sn);
       }
       nfr += __popc(f);
     }
     // this CTA's c partial: sum_i s_i y_i in row order (lane-strided, fixed tree)
     double cl = 0.0;
+#pragma unroll 1
     for (int j = lane; j < rows_g; j += 32) cl += flipd(yrow[j], ((s_cur[j >> 5] >> (j & 31)) & 1u) << 31);
     cl = warp_sum(cl);
     bad = __any_sync(0xffffffffu, bad);
     if (lane == 0) {
-      if (bad) atomicMin(a.errp + ERR_Y, static_cast<unsigned>(P));
+      if (bad) atomicMin(F.errp + ERR_Y, uP);
       const unsigned long long tagc = tag | ((bad || ctl->zerr) ? (1ull << 63) : 0ull);
-      st_relaxed64x2(a.rec_out + 2 * a.sw, tagc | static_cast<uint32_t>(__double2hiint(cl)),
+      st_relaxed64x2(rec_out + 2 * sw, tagc | static_cast<uint32_t>(__double2hiint(cl)),
                      tagc | static_cast<uint32_t>(__double2loint(cl)));
       ctl->nfrows += nfr;  // flipped rows the owners read (traffic accounting)
     }
+    SCB_FT(3);
+    // ---- 4a. every CTA's c partial, reduced in the order of the barrier passes:
+    // CTA 32 k + lane in "warp" k (butterfly), then k ascending (thread 0) ----
+    bool flag = false;
+#pragma unroll 1
+    for (int k = 0; k < NW; ++k) {
+      const int gi = k * 32 + lane;
+      if (k * 32 >= G) {  // no CTAs here: the barrier passes add zeros
+        if (lane == 0) {
+          ctl->cred[k] = 0.0;
+          ctl->nred[k] = 0.0;
+        }
+        continue;
+      }
+      double c = 0.0;
+      if (gi < G) {
+        const unsigned long long* pc = rec_in + static_cast<size_t>(gi) * F.rstride + 2 * sw;
+        unsigned long long c0, c1;
+        do {
+          ld_relaxed64x2(pc, c0, c1);
+          SCB_POLL_BACKOFF();
+        } while ((static_cast<unsigned>(c0 >> 32) & 0x7fffffffu) != uP || (static_cast<unsigned>(c1 >> 32) & 0x7fffffffu) != uP);
+        c = __hiloint2double(static_cast<int>(static_cast<uint32_t>(c0)), static_cast<int>(static_cast<uint32_t>(c1)));
+        flag |= (c0 >> 63) != 0ull;
+      }
+      c = warp_sum(c);
+      if (lane == 0) {
+        ctl->cred[k] = c;
+        ctl->nred[k] = 0.0;
+      }
+    }
+    flag = __any_sync(0xffffffffu, flag);
+    if (flag && lane == 0) ctl->err_pre[0] = uP;  // some CTA saw a non-finite value: every CTA stops at this pass
+    __syncwarp();
+    SCB_FT(4);
+    return;
   }
 
-  // ---- 4. everyone's record: c partials (all CTAs), flip words (owners) ----
-  {
-    const unsigned uP = static_cast<unsigned>(P);
-    const int nfw = a.owner ? a.G * a.sw : 0;
-    bool nc = tid < a.G, nf = tid < nfw;
-    const int gq = nf ? tid / a.sw : 0;
-    const unsigned long long* pc = a.rec_in + static_cast<size_t>(nc ? tid : 0) * a.rstride + 2 * a.sw;
-    const unsigned long long* pf = a.rec_in + static_cast<size_t>(gq) * a.rstride + 2 * (tid - gq * a.sw);
-    double cmine = 0.0;
-    bool flag = false;
-    while (nc || nf) {
-      unsigned long long c0 = 0, c1 = 0, f0 = 0, f1 = 0;
-      if (nc) ld_relaxed64x2(pc, c0, c1);
-      if (nf) ld_relaxed64x2(pf, f0, f1);
-      if (nc && (static_cast<unsigned>(c0 >> 32) & 0x7fffffffu) == uP &&
-          (static_cast<unsigned>(c1 >> 32) & 0x7fffffffu) == uP) {
-        nc = false;
-        cmine = __hiloint2double(static_cast<int>(static_cast<uint32_t>(c0)), static_cast<int>(static_cast<uint32_t>(c1)));
-        flag = (c0 >> 63) != 0ull;
-      }
-      if (nf && static_cast<unsigned>(f0 >> 32) == uP && static_cast<unsigned>(f1 >> 32) == uP) {
-        nf = false;
-        fws[tid] = static_cast<unsigned long long>(static_cast<uint32_t>(f0)) | (f1 << 32);
-      }
-    }
-    for (int idx = tid + CT; idx < nfw; idx += CT) {  // tall bands: more flip words than threads
-      const int g2 = idx / a.sw;
-      const unsigned long long* q = a.rec_in + static_cast<size_t>(g2) * a.rstride + 2 * (idx - g2 * a.sw);
-      unsigned long long f0, f1;
-      do {
-        ld_relaxed64x2(q, f0, f1);
-      } while (static_cast<unsigned>(f0 >> 32) != uP || static_cast<unsigned>(f1 >> 32) != uP);
-      fws[idx] = static_cast<unsigned long long>(static_cast<uint32_t>(f0)) | (f1 << 32);
-    }
-    const double cs = warp_sum(cmine);
-    if (lane == 0) {
-      ctl->cred[warp] = cs;
-      ctl->nred[warp] = 0.0;
-    }
-    if (flag) ctl->err_pre[0] = uP;  // some CTA saw a non-finite value: every CTA stops at this pass
+  // ---- 4b. owners (warps 1..): flip words of every CTA, then the column update ----
+  const int nls = F.nls;
+  if (nls == 0) return;
+  const int lw = warp - 1, lt = tid - 32;
+  // z state of this warp's column word (final warps only), issued early
+  const int colz = (F.g + lw * G) * 32 + lane;
+  double zs = 0.0;
+  if (lw < nls && colz < F.n) zs = __ldcg(F.zstate + colz);
+  const int items = G * sw;
+#pragma unroll 1
+  for (int idx = lt; idx < items; idx += NP * 32) {
+    const int g2 = sw == 1 ? idx : idx / sw;
+    const unsigned long long* q = rec_in + static_cast<size_t>(g2) * F.rstride + 2 * (idx - g2 * sw);
+    unsigned long long f0, f1;
+    do {
+      ld_relaxed64x2(q, f0, f1);
+      SCB_POLL_BACKOFF();
+    } while (static_cast<unsigned>(f0 >> 32) != uP || static_cast<unsigned>(f1 >> 32) != uP);
+    fws[idx] = static_cast<unsigned long long>(static_cast<uint32_t>(f0)) | (f1 << 32);
   }
-  consumer_sync(CT);
+  asm volatile("bar.sync 2, %0;" ::"r"(NP * 32) : "memory");
+  SCB_FT(8);
+  if (F.shared_list) return;  // many flip words (tall bands): the caller runs col_reduce's shared row list
+  // this warp's slice of the one ascending list of flipped rows (every warp scans
+  // all flip words; lane l covers entries [l per, (l + 1) per))
+  const int per = (items + 31) / 32;
+  const int i0 = min(items, lane * per), i1 = min(items, i0 + per);
+  int cnt = 0;
+#pragma unroll 1
+  for (int i = i0; i < i1; ++i) cnt += __popc(static_cast<uint32_t>(fws[i]));
+  int inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, inc, 31);
+  SCB_FT(11);
+  const int k0 = (total * lw) / NP, k1 = (total * (lw + 1)) / NP;
+  uint32_t* buf = reinterpret_cast<uint32_t*>(smem + F.fbuf) + lw * kFBuf;
+  const E* Rc = static_cast<const E*>(F.R) + F.g * 32 + lane;  // column of word 0; word j: + j * G * 32
+  // this warp's partial of every owned word accumulates in its own zseg slot
+  double* zseg = reinterpret_cast<double*>(smem + F.zseg);
+#pragma unroll 1
+  for (int j = 0; j < nls; ++j) zseg[(j * NW + lw) * 32 + lane] = 0.0;
+#pragma unroll 1
+  for (int c0 = k0; c0 < k1; c0 += kFBuf) {
+    const int c1 = min(c0 + kFBuf, k1);
+    {
+      int pos = inc - cnt;
+      int gp = sw == 1 ? i0 : i0 / sw, w = i0 - gp * sw;
+#pragma unroll 1
+      for (int i = i0; i < i1; ++i) {
+        const unsigned long long fw = fws[i];
+        uint32_t f = static_cast<uint32_t>(fw);
+        const uint32_t sn = static_cast<uint32_t>(fw >> 32);
+        const int rb = gp * F.rows_base + min(gp, F.rows_rem) + w * 32;
+        while (f) {
+          const int b = __ffs(f) - 1;
+          f &= f - 1;
+          if (pos >= c0 && pos < c1) buf[pos - c0] = static_cast<uint32_t>(rb + b) | (((sn >> b) & 1u) << 31);
+          ++pos;
+        }
+        if (++w == sw) {
+          w = 0;
+          ++gp;
+        }
+      }
+    }
+    __syncwarp();
+    SCB_FT(12);
+#pragma unroll 1
+    for (int k = 0; k < c1 - c0; k += 8) {
+      uint32_t e[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) e[u] = (k + u < c1 - c0) ? buf[k + u] : 0xffffffffu;
+#pragma unroll 1
+      for (int j = 0; j < nls; ++j) {  // eight row loads of one owned word in flight
+        E v[8];
+        const E* Rj = Rc + static_cast<size_t>(j) * G * 32;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = e[u] != 0xffffffffu ? __ldcg(Rj + static_cast<size_t>(e[u] & 0x7fffffffu) * F.pitch) : E(0);
+        double a = zseg[(j * NW + lw) * 32 + lane];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e[u] != 0xffffffffu) a = fma(static_cast<double>(v[u]), (e[u] >> 31) ? -2.0 : 2.0, a);
+        zseg[(j * NW + lw) * 32 + lane] = a;
+      }
+    }
+    __syncwarp();
+  }
+  SCB_FT(9);
+  if (lw >= nls) {  // partial delivered; only the word's final warp waits
+    asm volatile("bar.arrive 4, %0;" ::"r"(NP * 32) : "memory");
+    return;
+  }
+  asm volatile("bar.sync 4, %0;" ::"r"(NP * 32) : "memory");
+  {
+    double z = 0.0;
+#pragma unroll
+    for (int w = 0; w < NP; ++w) z += zseg[(lw * NW + w) * 32 + lane];
+    const bool valid = colz < F.n;
+    z = zs + z;
+    if (valid) __stcg(F.zstate + colz, z);
+    if (valid && !isfinite(z)) {
+      atomicMin(F.errp + ERR_Z, uP);
+      ctl->zerr = 1;
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, valid && z < 0.0);
+    const int qq = F.g + lw * G;
+    if (lane == 0)
+      st_relaxed64(F.tb64 + (static_cast<size_t>(tsel ^ 1) * Q + qq) * kTbStride,
+                   (static_cast<unsigned long long>(uP + 1u) << 32) | word);
+  }
+  SCB_FT(10);
+#undef SCB_FT
 }
 
 // ---------------------------------------------------------------------------
@@ -2035,6 +2175,48 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     ctl->has_dz = 0;
     ctl->keep = 0;
     ctl->zerr = 0;
+    {  // pass-invariant operands of the barrier-free delta pass
+      FastConst& fc = ctl->fc;
+      fc.Rrows = R + static_cast<size_t>(r0) * pitch;
+      fc.R = R;
+      fc.drec = p.drec;
+      fc.tb64 = p.tb64;
+      fc.zstate = p.zstate;
+      fc.errp = p.err_pass;
+#ifdef SCB_PROFILE
+      fc.prof = p.prof ? p.prof + static_cast<size_t>(p.G) * 16 + g * 16 : nullptr;
+#else
+      fc.prof = nullptr;
+#endif
+      fc.pitch = pitch;
+      fc.res = static_cast<unsigned>(L.res);
+      fc.yrow = static_cast<unsigned>(L.yrow);
+      fc.sb = static_cast<unsigned>(L.sb);
+      fc.tws = static_cast<unsigned>(L.tws);
+      fc.txor = static_cast<unsigned>(L.txor);
+      fc.clist = static_cast<unsigned>(L.clist);
+      fc.fws = static_cast<unsigned>(L.fws);
+      fc.fbuf = static_cast<unsigned>(L.fbuf);
+      fc.zseg = static_cast<unsigned>(L.zseg);
+      fc.rowB = static_cast<unsigned>(rowB);
+      fc.rows_g = rows_g;
+      fc.nres = nres;
+      fc.Q = p.Q;
+      fc.G = G;
+      fc.sw = p.sw;
+      fc.rstride = p.rstride;
+      fc.n = p.n;
+      fc.g = g;
+      fc.rows_base = p.rows_base;
+      fc.rows_rem = p.rows_rem;
+      int nls = 0;
+      for (int j = 0; j < 4; ++j)
+        if (g + j * G < p.Q) nls = j + 1;
+      fc.nls = nls;
+      // tall bands (many flip words per pass): one row list built by all owner warps
+      // together (col_reduce) beats every warp scanning all the words
+      fc.shared_list = G * p.sw > 256 ? 1 : 0;
+    }
     ctl->term = 0;
     ctl->restart = 0;
     ctl->tsel = -1;
@@ -2073,7 +2255,11 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     for (int P = 0;; ++P) {
       while (ctl->decided <= P) {
         if (ctl->abort) goto drain;
+#ifdef SCB_PROD_SLEEP
+        __nanosleep(SCB_PROD_SLEEP);
+#else
         __nanosleep(32);
+#endif
       }
       {
         const int kind = ctl->kind_ring[P & 3];
@@ -2420,32 +2606,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     // reduction beside the decision, as after a barrier pass.
     const bool fast = !TS && !MR && (kind & F_DELTA) && p.fast_delta;
     if (fast) {
-      FastArgs fa;
-      fa.tw = p.tb64 + static_cast<size_t>(ctl->tsel) * p.Q * kTbStride;
-      fa.rec_in = p.drec + static_cast<size_t>(P & 1) * G * p.rstride;
-      fa.rec_out = const_cast<unsigned long long*>(fa.rec_in) + static_cast<size_t>(g) * p.rstride;
-      fa.Rrows = R + static_cast<size_t>(r0) * pitch;
-      fa.errp = const_cast<unsigned*>(errp);
-      fa.pitch = pitch;
-      fa.res = static_cast<unsigned>(L.res);
-      fa.yrow = static_cast<unsigned>(L.yrow);
-      fa.s_cur = static_cast<unsigned>(reinterpret_cast<const unsigned char*>(s_cur) - smem);
-      fa.s_nxt = static_cast<unsigned>(reinterpret_cast<unsigned char*>(s_nxt) - smem);
-      fa.tws = static_cast<unsigned>(L.tws);
-      fa.txor = static_cast<unsigned>(L.txor);
-      fa.clist = static_cast<unsigned>(L.clist);
-      fa.fws = static_cast<unsigned>(L.fws);
-      fa.ctl = static_cast<unsigned>(L.ctl);
-      fa.rowB = static_cast<unsigned>(rowB);
-      fa.rows_g = rows_g;
-      fa.nres = nres;
-      fa.Q = p.Q;
-      fa.G = G;
-      fa.sw = p.sw;
-      fa.rstride = p.rstride;
-      fa.P = P;
-      fa.owner = g < p.Q ? 1 : 0;
-      fast_delta_front<E, NW>(fa);
+      fast_delta<E, NW>(static_cast<unsigned>(L.ctl), P, ctl->tsel, ctl->cur | (ctl->nxt << 2));
       if (g == 0 && tid == 32) nflip_sum += static_cast<unsigned>(ctl->nflip);
       if (g == 0 && tid == 0) ++dot_passes[1];
       gcount += static_cast<unsigned>((rows_g + RG - 1) / RG);
@@ -2584,7 +2745,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         dl.flipw = p.flipw + (static_cast<size_t>(P & 1) * G + g) * p.sw;
         dl.sw_all = p.sw;
 #ifdef SCB_PROFILE
-        dl.prof = prof ? p.prof + static_cast<size_t>(p.G) * 16 + g * 8 : nullptr;
+        dl.prof = prof ? p.prof + static_cast<size_t>(p.G) * 16 + g * 16 : nullptr;
 #endif
         dl.pitch = pitch;
         dl.rowB = static_cast<unsigned>(rowB);
@@ -2840,12 +3001,15 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
 
     // Matrix dot pass: owners reduce z and publish the next t right away (it does
     // not depend on the decision), taking the decision off every CTA's critical path.
-    if (!TS && (kind & F_DOT) && warp >= 1) {  // warp 0 runs the decision below meanwhile
+    if (!TS && (kind & F_DOT) && warp >= 1 && (!fast || (ctl->fc.shared_list && ctl->fc.nls > 0))) {  // warp 0: the decision
+      const long long tc0 = (prof && tid == 32) ? clock64() : 0;
       if (MR && p.world > 1)
         col_reduce_global(P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
       else
         col_reduce(0, P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
+      if (prof && tid == 32 && (kind & F_DELTA)) prof[static_cast<size_t>(p.G) * 16 + g * 16 + 6] += clock64() - tc0;
     }
+    const long long td0 = (prof && tid == 0) ? clock64() : 0;
 
     // ------------------------------ decision ------------------------------
     if (tid == 0) {
@@ -3023,6 +3187,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       __threadfence_block();
       ctl->decided = P + 2;
       if ((next & K_TERM) && g == 0) p.stats[1] = static_cast<unsigned long long>(P + 1);
+      if (prof && (kind & F_DELTA)) prof[static_cast<size_t>(p.G) * 16 + g * 16 + 7] += clock64() - td0;
     }
     consumer_sync(CT);
     if (prof && tid == 0) {
