@@ -145,11 +145,13 @@ const char* sc_last_error(const sc_ctx* ctx);
 
 /* Engine options of this context (tuning / test knobs; the defaults are the
  * measured best).  Names: "ctas" (CTA cap, 0 auto), "delta" (sparse delta passes,
- * 1), "delta_div" (32), "delta_refresh" (64), "two_phase" (dot-pass form: -1 auto,
+ * 1), "delta_div" (0 = auto: 8 with the barrier-free delta pass, else 32), "delta_refresh" (64), "two_phase" (dot-pass form: -1 auto,
  * 0 fused single read, 1 two-phase), "stages" (TMA ring depth, 0 auto),
  * "res_rows" (cap on SMEM-resident rows, -1 none), "fuse_update" (rank-1 update
  * fused into the next term's first dot pass, 1), "variant" (tile override
- * nw*1000000 + vpt*10000 + rg*100 + cps, 0 auto), "profile" (clock64 breakdown of
+ * nw*1000000 + vpt*10000 + rg*100 + cps, 0 auto), "fast_delta" (delta
+ * passes exchange self-tagged records instead of meeting at a grid barrier, 1),
+ * "l2_persist" (R as a persisting-L2 window during the launch, 0), "profile" (clock64 breakdown of
  * SCB_PROFILE builds to stderr, 0), "poison" (test hook: fill the device arena with
  * NaN bytes before each call, so any read of a never-written word shows, 0).  No
  * option changes results except through the

@@ -201,7 +201,8 @@ class Engine:
 
     def set_option(self, name: str, value: int) -> None:
         """Engine option of this context (sc_set_option): ctas, delta, delta_div,
-        delta_refresh, two_phase, stages, res_rows, fuse_update, variant, profile."""
+        delta_refresh, two_phase, stages, res_rows, fuse_update, variant, fast_delta,
+        l2_persist, profile, poison."""
         self._check(self.lib.sc_set_option(self.handle, name.encode(), int(value)))
 
     def get_option(self, name: str) -> int:

@@ -430,6 +430,21 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   if (scb::pick_variant(dt, pitch, &var, ctx->opts.variant) != 0)
     return set_err(ctx, SC_NOT_SUPPORTED, "row length %llu exceeds the fused-kernel envelope",
                    static_cast<unsigned long long>(n));
+  // One GPU, matrices, f32 rows of 2049..4096 columns: 16 consumer warps x 2 vectors instead of
+  // 8 x 4 -- four warps per scheduler hide the per-row latency chain of the dense passes
+  // (14336 x 4096: 67.5 -> 53.8 ms per 64 cuts, 32000 x 4096: 76.5 -> 58.9 ms; 4096^2 and
+  // 1024 x 4096 unchanged).  Order-k and row-sharded runs keep the 8-warp tile.
+  if (!tensor && !sh && ctx->opts.variant == 0 && dt == SC_F32 && var.nw == 8 && var.vpt == 4 && var.rg == 1) {
+    var.nw = 16;
+    var.vpt = 2;
+  }
+  // f64 rows of 2049..4096 columns: the same 16-warp tile once R spills to HBM (14336 x 4096 f64:
+  // 36.3 -> 34.1 ms per 32 cuts; L2-resident 4096^2 f64 is 3% faster with 8 warps)
+  if (!tensor && !sh && ctx->opts.variant == 0 && dt == SC_F64 && var.nw == 8 && var.vpt == 8 && var.rg == 1 &&
+      pitch <= 4096 && m * static_cast<uint64_t>(pitch) * 8 > (uint64_t{160} << 20)) {
+    var.nw = 16;
+    var.vpt = 4;
+  }
   var.tensor = tensor ? 1 : 0;  // order-k kernels are separate instantiations
   var.mr = (sh && sh->world > 1 && !vr) ? 1 : 0;  // the multi-rank exchange is compiled in separately
   if (var.mr && !scb::has_vr(var))
@@ -664,11 +679,14 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   kp.rstride = rstride;
   // one GPU, matrices, whole rows, one record-polling thread per CTA of the grid
   kp.fast_delta = (ctx->opts.fast_delta && !tensor && !sh && !vr && cpr == 1 && var.nw * 32 >= G && Q <= 4 * G) ? 1 : 0;
+  // delta pass only if the last sweep flipped <= n / delta_div columns.  Auto (0): n / 8 with the
+  // barrier-free delta pass (4096^2 w=512: 355.6 ms at 32, 344.5 at 16, 338.9 at 8, 338.2 at 4),
+  // n / 32 for the barrier passes (order-k, row-sharded, chunked rows: measured best in round 1)
+  kp.delta_div = static_cast<int>(ctx->opts.delta_div > 0 ? ctx->opts.delta_div : (kp.fast_delta ? 8 : 32));
   // Sparse delta passes between dense refreshes (matrices, any row length: the dz of
   // flipped rows walks every column chunk).
   kp.delta = ctx->opts.delta ? 1 : 0;
   kp.fuse_update = ctx->opts.fuse_update ? 1 : 0;
-  kp.delta_div = static_cast<int>(std::max<long long>(1, ctx->opts.delta_div));
   kp.delta_refresh = static_cast<int>(std::max<long long>(1, ctx->opts.delta_refresh));
   // Dot-pass form: the two-phase pass reads R twice per sweep but has no per-row
   // serial chain -- the better choice while R stays in SMEM / L2; once R spills
@@ -868,9 +886,11 @@ sc_status finish_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, RunState&
                    mn[1] / np_, mx[1] / np_, mn[2] / np_, mx[2] / np_, mn[3] / np_, mx[3] / np_, mn[4] / np_, mx[4] / np_,
                    mn[5] / np_, mx[5] / np_);
     }
-    std::fprintf(stderr, "[scb passes] dense dot %llu, delta dot %llu, total %llu\n",
+    std::fprintf(stderr, "[scb passes] dense dot %llu, delta dot %llu, total %llu | per delta pass: %.1f flipped columns, %.1f flipped rows\n",
                  static_cast<unsigned long long>(h_stats[2]), static_cast<unsigned long long>(h_stats[3]),
-                 static_cast<unsigned long long>(h_stats[1]));
+                 static_cast<unsigned long long>(h_stats[1]),
+                 static_cast<double>(h_stats[7]) / std::max<double>(1.0, static_cast<double>(h_stats[3])),
+                 static_cast<double>(h_stats[5]) / std::max<double>(1.0, static_cast<double>(h_stats[3])));
     std::fprintf(stderr, "[scb prof2] per pass: stagewait=%.0f A=%.0f B=%.0f C=%.0f\n",
                  acc[8] / std::max<double>(1.0, static_cast<double>(h_stats[1])),
                  acc[9] / std::max<double>(1.0, static_cast<double>(h_stats[1])),
@@ -919,7 +939,8 @@ sc_status finish_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, RunState&
     bytes += static_cast<double>(dense - fused) * (sb * (kp.two_phase ? 2.0 : 1.0) + 2.0 * zb * kp.G);
     bytes += static_cast<double>(fused) * (sb * 3.0 + 2.0 * zb * kp.G);
     bytes += static_cast<double>(maint) * sb + static_cast<double>(maint_upd) * sb + static_cast<double>(rrows) * rowB;
-    bytes += static_cast<double>(h_stats[7]) * static_cast<double>(srows) * 32.0 +
+    // (the barrier-free delta pass gathers every row of the band from L2, resident or not)
+    bytes += static_cast<double>(h_stats[7]) * static_cast<double>(kp.fast_delta ? S.m : srows) * 32.0 +
              static_cast<double>(h_stats[5]) * rowB + static_cast<double>(h_stats[6]) * 2.0 * zb;
     if (kp.world > 1) bytes += static_cast<double>(dense + delta) * 2.0 * zb;  // rank partials
     res->device_bytes = static_cast<uint64_t>(bytes);

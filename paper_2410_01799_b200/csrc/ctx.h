@@ -26,7 +26,7 @@ struct sc_ctx {
   struct Options {
     long long ctas = 0;           // cap on the CTA count (0: auto)
     long long delta = 1;          // sparse delta passes between dense refreshes
-    long long delta_div = 32;     // delta pass only if <= n / delta_div columns flipped
+    long long delta_div = 0;      // delta pass only if <= n / delta_div columns flipped (0: auto, 8 or 32 by path)
     long long delta_refresh = 64; // dense refresh every delta_refresh sweeps
     long long two_phase = -1;     // dot-pass form: -1 auto (by residency), 0 fused single read, 1 two-phase
     long long stages = 0;         // TMA ring depth (0: auto)

@@ -9,6 +9,7 @@ void* kernel_f64m(const Variant& v) {
   SCB_K(8, 2, 2)
   SCB_K(8, 4, 2)
   SCB_K(8, 8, 1)
+  SCB_K(16, 4, 1)
   SCB_K(16, 7, 1)
 #undef SCB_K
   return nullptr;

@@ -336,14 +336,21 @@ def test_order3_wide_trailing_axes(engine, ref):
                                          ((300, 16384), "f32")])
 def test_sharded_world1_equals_engine(engine, ref, shape, dtype):
     """sc_greedy_decompose_sharded with one rank: the peer-memory exchange path
-    (system-scope barrier off, peer tables of size 1) gives bit-identical results."""
+    (system-scope barrier off, peer tables of size 1) is bit-identical to the engine's
+    barrier passes; the default engine (barrier-free delta passes, another fixed
+    summation order in the y gathers) has the same signs and sweeps, c to 1e-12."""
     from paper_2410_01799_b200 import sharded
 
     m, n = shape
     a = ref.fill_normal(m * 7 + n, m * n).reshape(m, n)
     a = a.astype(np.float32) if dtype == "f32" else a
     cfg = sc.DecomposeConfig(width=6, record_curve=True, search=sc.SearchConfig(seed=5))
-    dec, rep, _ = engine.run(a, cfg, dtype=dtype)
+    fdec, frep, _ = engine.run(a, cfg, dtype=dtype)  # default engine: barrier-free delta passes
+    with engine.options(fast_delta=0, delta_div=32):  # the barrier passes the sharded path runs
+        dec, rep, _ = engine.run(a, cfg, dtype=dtype)
+    assert all((x == y).all() for x, y in zip(dec.factors, fdec.factors))
+    assert np.array_equal(rep.sweeps, frep.sweeps)
+    assert np.max(np.abs(rep._cut_values - frep._cut_values) / np.abs(rep._cut_values)) <= 1e-12
     se = sharded.ShardedEngine(m, n, dtype, 0, 1, device=0)
     try:
         sdec, srep, _ = se.decompose(a, cfg)
@@ -426,6 +433,69 @@ def test_delta_gathers_many_flips_tall_bands(engine, dtype):
     assert all((x == y).all() for x, y in zip(d0.factors, d1.factors))
     assert np.array_equal(r0.sweeps, r1.sweeps)
     assert np.max(np.abs(r1._cut_values - r0._cut_values) / np.abs(r0._cut_values)) <= 1e-12
+
+
+# ----------------------------------------------- barrier-free delta passes
+@pytest.mark.parametrize("m,n,dtype,w,restarts,div", [
+    (1024, 1024, "f32", 24, 1, 8),   # one row word per CTA, one column word per owner
+    (333, 257, "f64", 10, 2, 8),     # ragged band words and column words, restarts
+    (2000, 6000, "f32", 4, 1, 8),    # two column words per owner CTA (Q = 188 > G)
+    (6000, 1536, "f64", 4, 1, 8),    # 41-row bands: two flip words per CTA, shared row list
+    (120, 4096, "f32", 6, 1, 1),     # fewer CTAs than column words (some CTAs own two); few sweeps: div 1
+])
+def test_fast_delta_matches_barrier_delta(engine, m, n, dtype, w, restarts, div):
+    """The barrier-free delta pass (self-tagged records polled instead of a grid
+    barrier, engine option fast_delta) against the barrier delta pass on the same
+    input: identical signs, sweep counts and pass counts; c within 1e-12 (the y
+    gathers sum the flipped columns in a different fixed order)."""
+    a = sc.fill_normal(31, m * n, np.float32).reshape(m, n)
+    a = a if dtype == "f32" else a.astype(np.float64)
+    out = {}
+    for mode in (0, 1):
+        with engine.options(fast_delta=mode, delta_div=div):
+            out[mode] = run(engine, a, w, seed=6, dtype=dtype, restarts=restarts)
+    (d0, r0, _), (d1, r1, _) = out[0], out[1]
+    assert r1.delta_passes > 0
+    assert all((x == y).all() for x, y in zip(d0.factors, d1.factors))
+    assert np.array_equal(r0.sweeps, r1.sweeps)
+    assert (r0.passes, r0.dense_passes, r0.delta_passes) == (r1.passes, r1.dense_passes, r1.delta_passes)
+    assert np.max(np.abs(r1._cut_values - r0._cut_values) / np.abs(r0._cut_values)) <= 1e-12
+
+
+def test_fast_delta_many_flips_chunks_the_column_list(engine, ref):
+    """Delta passes after every sweep (div 1): early sweeps flip far more than the 256
+    columns one list round holds, so the list is rebuilt chunk by chunk; the
+    reference's signs all the same."""
+    a = ref.fill_normal(32, 512 * 2048).reshape(512, 2048)
+    with engine.options(fast_delta=1, delta_div=1, delta_refresh=1000):
+        dec, rep, _ = run(engine, a, 8, seed=7)
+    od = ref.greedy_decompose(a, 8, seed=7)
+    assert rep.delta_passes > rep.dense_passes
+    assert (dec.factors[0] == od.signs[0]).all() and (dec.factors[1] == od.signs[1]).all()
+    assert sweeps_ok(rep.sweeps, od.iterations)
+    assert np.max(np.abs(rep._cut_values - od.cut_value) / np.abs(od.cut_value)) <= F64_TOL
+
+
+@pytest.mark.timeout(120)
+def test_fast_delta_overflow_stops_every_cta(engine):
+    """A planted sign pattern with f64 magnitudes so large that y = R t overflows once
+    the signs align (a few sweeps in -- delta passes with div 1): the CTA that sees
+    it flags its record, every CTA takes the same stop decision (no hang) and the
+    call reports the reference's sgn_vector error, exactly as the barrier passes do."""
+    g = np.abs(sc.fill_normal(33, 256 * 256, np.float32).reshape(256, 256).astype(np.float64))
+    su = np.where(sc.fill_normal(34, 256, np.float32) < 0, -1.0, 1.0)
+    tv = np.where(sc.fill_normal(35, 256, np.float32) < 0, -1.0, 1.0)
+    a = np.outer(su, tv) * g * 1.05e306
+    outcomes = []
+    for mode in (0, 1):
+        with engine.options(fast_delta=mode, delta_div=1):
+            try:
+                run(engine, a, 2, seed=8)
+                outcomes.append("ok")
+            except sc.InvalidArgument as e:
+                assert "non-finite" in str(e)
+                outcomes.append("non-finite")
+    assert outcomes[0] == outcomes[1] == "non-finite"
 
 
 # ------------------------------------------------------------ SearchDiagnostics
