@@ -39,7 +39,11 @@ sys.path.insert(0, ROOT)
 M = N = 4096
 SEED = 1
 METRIC = "signed cuts/sec at 4096x4096 f32; achieved HBM GB/s vs B200 peak"
-SYNC_FLOOR_US = 1.25  # flat grid barrier over 148 CTAs on this B200 (scripts/micro/barrier3.cu)
+SYNC_FLOOR_US = 1.25  # flat grid barrier over 148 CTAs on this B200 (scripts/micro/barrier3.cu): ends every dense pass
+# Latency floor of one barrier-free delta pass: six dependent L2 trips -- the t words'
+# store and poll, the column gather, the records' store and poll, the flipped-row gather -- at the
+# ~250-cycle L2 hit latency of the microarchitecture guide, 1.965 GHz
+DELTA_FLOOR_US = 6 * 250 / 1965.0
 
 
 def bench_config(width, world):
@@ -349,12 +353,14 @@ def main():
             "algorithmic_achieved": alg_gbs, "algorithmic_frac": alg_gbs / peak,
             "algorithmic_bytes": "sum_j (2*sweeps_j+1)*m*n*4 per launch (SURVEY 8d / BASELINE); counts every "
                                  "half-iteration as a full read of R, so it exceeds 1 when R is on chip",
-            "binding": "per-pass synchronisation latency: R is on chip, and each pass is a chain of grid-wide "
-                       "exchanges (DESIGN.md 5)",
+            "binding": "per-pass exchange latency: R is on chip; a delta pass (95% of the passes) is a chain "
+                       "of two publish->poll exchanges and two L2 gathers with no grid barrier in it, a dense "
+                       "pass streams R from SMEM/L2 and ends in one grid barrier (DESIGN.md 4.6, 5)",
             "latency_model": {"passes_per_launch": passes_l, "dense_passes_per_launch": dense / args.steps,
                               "delta_passes_per_launch": delta / args.steps, "us_per_pass": us_per_pass,
-                              "grid_sync_floor_us": SYNC_FLOOR_US,
-                              "floor_frac": SYNC_FLOOR_US / us_per_pass},
+                              "delta_pass_floor_us": DELTA_FLOOR_US, "grid_sync_floor_us": SYNC_FLOOR_US,
+                              "floor_is": "six dependent L2 trips per delta pass at the 250-cycle L2 hit latency",
+                              "floor_frac": DELTA_FLOOR_US / us_per_pass},
         },
         "sweeps_per_cut_mean": float(np.mean(sweeps)),
         "clocks": clocks,

@@ -25,12 +25,12 @@ ls -la $O
 mkdir -p $O/r02
 python scripts/ncu_summary.py --rep $O/sweep_bench512.ncu-rep --out $O/r02/sweep_kernel_bench512_full.txt \
   --desc "python scripts/prof_case.py 512 (the bench workload: 4096^2 f32, 512 cuts, seed 1)" --cuts 512 \
-  --launches $O/launches_bench.csv > /dev/null 2>&1; echo "summary bench rc=$?"
+  --launches $O/launches_bench.csv --traffic > /dev/null 2>&1; echo "summary bench rc=$?"
 python scripts/ncu_summary.py --rep $O/sweep_gate16.ncu-rep --out $O/r02/sweep_kernel_gate16_full.txt \
   --desc "python scripts/prof_case.py 16 14336 4096 (C4 gate shape, HBM-resident, 16 cuts)" --cuts 16 > /dev/null 2>&1
 python scripts/ncu_summary.py --rep $O/sweep_c5.ncu-rep --out $O/r02/sweep_kernel_c5_full.txt \
   --desc "python scripts/prof_case.py 1 c5 (C5 65536^2 f32, 1 cut)" --cuts 1 > /dev/null 2>&1
 for x in bench512 gate16 c5; do python scripts/ncu_hotlines.py $O/sweep_$x.ncu-rep 40 > $O/r02/hotlines_$x.txt 2>&1; done
-cp profiles/latest_kernel_traffic.json $O/r02/ 2>/dev/null
+cp profiles/latest_kernel_traffic.json $O/r02/ 2>/dev/null  # written just above by --traffic
 rm -f $O/sweep_gate16.ncu-rep $O/sweep_c5.ncu-rep $O/sweep_bench512.ncu-rep
 ls -la $O/r02
