@@ -678,7 +678,7 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   kp.drec = drec;
   kp.rstride = rstride;
   // one GPU, matrices, whole rows, one record-polling thread per CTA of the grid
-  kp.fast_delta = (ctx->opts.fast_delta && !tensor && !sh && !vr && cpr == 1 && var.nw * 32 >= G && Q <= 4 * G) ? 1 : 0;
+  kp.fast_delta = (ctx->opts.fast_delta && !tensor && !sh && !vr && cpr == 1 && var.nw * 32 >= G && G <= 160 && Q <= 4 * G) ? 1 : 0;
   // delta pass only if the last sweep flipped <= n / delta_div columns.  Auto (0): n / 8 with the
   // barrier-free delta pass (4096^2 w=512: 355.6 ms at 32, 344.5 at 16, 338.9 at 8, 338.2 at 4),
   // n / 32 for the barrier passes (order-k, row-sharded, chunked rows: measured best in round 1)

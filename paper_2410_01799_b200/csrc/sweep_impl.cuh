@@ -1730,31 +1730,73 @@ __device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, con
     SCB_FT(3);
     // ---- 4a. every CTA's c partial, reduced in the order of the barrier passes:
     // CTA 32 k + lane in "warp" k (butterfly), then k ascending (thread 0) ----
+    // (all loads in flight together, then the butterflies side by side: this runs ahead
+    // of the decision, which the whole CTA waits for at the end of the pass).  In an owner
+    // CTA the polling starts once the owner warps hold every CTA's flip words: each CTA
+    // publishes its c pair right after its flip pair, so nothing is lost and the c
+    // records are not polled while they cannot be complete.
+    if (F.nls > 0 && F.cpar) asm volatile("bar.sync 5, %0;" ::"r"(CT) : "memory");
     bool flag = false;
+    if (!F.cpar) {  // short bands: one butterfly's loads at a time (less polling; the decision is not late here)
 #pragma unroll 1
-    for (int k = 0; k < NW; ++k) {
-      const int gi = k * 32 + lane;
-      if (k * 32 >= G) {  // no CTAs here: the barrier passes add zeros
+      for (int k = 0; k < NW; ++k) {
+        const int gi = k * 32 + lane;
+        double c = 0.0;
+        if (k * 32 < G) {
+          if (gi < G) {
+            const unsigned long long* pc = rec_in + static_cast<size_t>(gi) * F.rstride + 2 * sw;
+            unsigned long long c0, c1;
+            do {
+              ld_relaxed64x2(pc, c0, c1);
+            } while ((static_cast<unsigned>(c0 >> 32) & 0x7fffffffu) != uP || (static_cast<unsigned>(c1 >> 32) & 0x7fffffffu) != uP);
+            c = __hiloint2double(static_cast<int>(static_cast<uint32_t>(c0)), static_cast<int>(static_cast<uint32_t>(c1)));
+            flag |= (c0 >> 63) != 0ull;
+          }
+          c = warp_sum(c);
+        }
         if (lane == 0) {
-          ctl->cred[k] = 0.0;
+          ctl->cred[k] = c;
           ctl->nred[k] = 0.0;
         }
-        continue;
       }
+    } else {
+    constexpr int KC = 5;  // G <= 160 (host gate)
+    unsigned long long cw0[KC], cw1[KC];
+    unsigned need = 0;
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      cw0[k] = 0ull;
+      cw1[k] = 0ull;
+      if (k * 32 + lane < G) need |= 1u << k;
+    }
+    const unsigned long long* pc = rec_in + static_cast<size_t>(lane) * F.rstride + 2 * sw;
+    while (need) {
+#pragma unroll
+      for (int k = 0; k < KC; ++k)
+        if ((need >> k) & 1u) ld_relaxed64x2(pc + static_cast<size_t>(k) * 32 * F.rstride, cw0[k], cw1[k]);
+#pragma unroll
+      for (int k = 0; k < KC; ++k)
+        if (((need >> k) & 1u) && (static_cast<unsigned>(cw0[k] >> 32) & 0x7fffffffu) == uP &&
+            (static_cast<unsigned>(cw1[k] >> 32) & 0x7fffffffu) == uP)
+          need &= ~(1u << k);
+    }
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      if (k >= NW) break;
       double c = 0.0;
-      if (gi < G) {
-        const unsigned long long* pc = rec_in + static_cast<size_t>(gi) * F.rstride + 2 * sw;
-        unsigned long long c0, c1;
-        do {
-          ld_relaxed64x2(pc, c0, c1);
-          SCB_POLL_BACKOFF();
-        } while ((static_cast<unsigned>(c0 >> 32) & 0x7fffffffu) != uP || (static_cast<unsigned>(c1 >> 32) & 0x7fffffffu) != uP);
-        c = __hiloint2double(static_cast<int>(static_cast<uint32_t>(c0)), static_cast<int>(static_cast<uint32_t>(c1)));
-        flag |= (c0 >> 63) != 0ull;
+      if (k * 32 + lane < G) {
+        c = __hiloint2double(static_cast<int>(static_cast<uint32_t>(cw0[k])), static_cast<int>(static_cast<uint32_t>(cw1[k])));
+        flag |= (cw0[k] >> 63) != 0ull;
       }
-      c = warp_sum(c);
+      if (k * 32 < G) c = warp_sum(c);
       if (lane == 0) {
         ctl->cred[k] = c;
+        ctl->nred[k] = 0.0;
+      }
+    }
+    if (lane == 0)
+      for (int k = KC; k < NW; ++k) {
+        ctl->cred[k] = 0.0;
         ctl->nred[k] = 0.0;
       }
     }
@@ -1785,6 +1827,7 @@ __device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, con
     } while (static_cast<unsigned>(f0 >> 32) != uP || static_cast<unsigned>(f1 >> 32) != uP);
     fws[idx] = static_cast<unsigned long long>(static_cast<uint32_t>(f0)) | (f1 << 32);
   }
+  if (F.cpar) asm volatile("bar.arrive 5, %0;" ::"r"(CT) : "memory");  // warp 0 starts polling the c partials
   asm volatile("bar.sync 2, %0;" ::"r"(NP * 32) : "memory");
   SCB_FT(8);
   if (F.shared_list) return;  // many flip words (tall bands): the caller runs col_reduce's shared row list
@@ -2216,6 +2259,9 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       // tall bands (many flip words per pass): one row list built by all owner warps
       // together (col_reduce) beats every warp scanning all the words
       fc.shared_list = G * p.sw > 256 ? 1 : 0;
+      // c partials polled all at once (bands of more than 16 rows: the decision is the late
+      // part of the pass there; 4096^2 -7%) or one butterfly at a time (short bands: +2% otherwise)
+      fc.cpar = p.rows_max > 16 ? 1 : 0;
     }
     ctl->term = 0;
     ctl->restart = 0;
