@@ -60,6 +60,7 @@ struct FastConst {
   unsigned res, yrow, sb, tws, txor, clist, fws, fbuf, zseg, rowB;  // shared-memory offsets, row bytes
   int rows_g, nres, Q, G, sw, rstride, n, g, rows_base, rows_rem;
   int nls;  // 32-column words this CTA owns (words g, g + G, ...; 0: not an owner)
+  int direct;       // 1: each owner warp polls the flip words of its own CTA range (no staging)
   int cpar;         // 1: warp 0 polls every c partial at once (else one butterfly's worth at a time)
   int shared_list;  // 1: the owners' flipped-row list is built by col_reduce (many flip words)
 };

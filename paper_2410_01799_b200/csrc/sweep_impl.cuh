@@ -1816,29 +1816,57 @@ __device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, con
   double zs = 0.0;
   if (lw < nls && colz < F.n) zs = __ldcg(F.zstate + colz);
   const int items = G * sw;
+  int cnt = 0, inc, k0, k1;
+  int i0 = 0, i1 = 0;          // staged form: this lane's flip-word entries
+  uint32_t myf = 0, mysn = 0;  // direct form: this lane's flip word and new signs
+  int myrb = 0;                //              and the first row they stand for
+  if (F.direct) {
+    // Direct form (every warp's share of the flip words fits its lanes): warp lw takes
+    // the CTAs [gs, ge) -- lane l polls their l-th flip pair itself, so the warp moves
+    // on as soon as ITS CTAs have published, with no staging and no meeting of the
+    // owner warps before the final combine.  Rows stay in ascending order per warp.
+    const int gs = (lw * G) / NP, ge = ((lw + 1) * G) / NP;
+    const int e = gs * sw + lane;
+    if (e < ge * sw) {
+      const int g2 = sw == 1 ? e : e / sw, w = e - g2 * sw;
+      const unsigned long long* q = rec_in + static_cast<size_t>(g2) * F.rstride + 2 * w;
+      unsigned long long f0, f1;
+      do {
+        ld_relaxed64x2(q, f0, f1);
+      } while (static_cast<unsigned>(f0 >> 32) != uP || static_cast<unsigned>(f1 >> 32) != uP);
+      myf = static_cast<uint32_t>(f0);
+      mysn = static_cast<uint32_t>(f1);
+      myrb = g2 * F.rows_base + min(g2, F.rows_rem) + w * 32;
+    }
+    __syncwarp();
+    if (F.cpar) asm volatile("bar.arrive 5, %0;" ::"r"(CT) : "memory");  // warp 0 starts polling the c partials
+    SCB_FT(8);
+    cnt = __popc(myf);
+  } else {
 #pragma unroll 1
-  for (int idx = lt; idx < items; idx += NP * 32) {
-    const int g2 = sw == 1 ? idx : idx / sw;
-    const unsigned long long* q = rec_in + static_cast<size_t>(g2) * F.rstride + 2 * (idx - g2 * sw);
-    unsigned long long f0, f1;
-    do {
-      ld_relaxed64x2(q, f0, f1);
-      SCB_POLL_BACKOFF();
-    } while (static_cast<unsigned>(f0 >> 32) != uP || static_cast<unsigned>(f1 >> 32) != uP);
-    fws[idx] = static_cast<unsigned long long>(static_cast<uint32_t>(f0)) | (f1 << 32);
+    for (int idx = lt; idx < items; idx += NP * 32) {
+      const int g2 = sw == 1 ? idx : idx / sw;
+      const unsigned long long* q = rec_in + static_cast<size_t>(g2) * F.rstride + 2 * (idx - g2 * sw);
+      unsigned long long f0, f1;
+      do {
+        ld_relaxed64x2(q, f0, f1);
+        SCB_POLL_BACKOFF();
+      } while (static_cast<unsigned>(f0 >> 32) != uP || static_cast<unsigned>(f1 >> 32) != uP);
+      fws[idx] = static_cast<unsigned long long>(static_cast<uint32_t>(f0)) | (f1 << 32);
+    }
+    if (F.cpar) asm volatile("bar.arrive 5, %0;" ::"r"(CT) : "memory");  // warp 0 starts polling the c partials
+    asm volatile("bar.sync 2, %0;" ::"r"(NP * 32) : "memory");
+    SCB_FT(8);
+    if (F.shared_list) return;  // many flip words (tall bands): the caller runs col_reduce's shared row list
+    // this warp's slice of the one ascending list of flipped rows (every warp scans
+    // all flip words; lane l covers entries [l per, (l + 1) per))
+    const int per = (items + 31) / 32;
+    i0 = min(items, lane * per);
+    i1 = min(items, i0 + per);
+#pragma unroll 1
+    for (int i = i0; i < i1; ++i) cnt += __popc(static_cast<uint32_t>(fws[i]));
   }
-  if (F.cpar) asm volatile("bar.arrive 5, %0;" ::"r"(CT) : "memory");  // warp 0 starts polling the c partials
-  asm volatile("bar.sync 2, %0;" ::"r"(NP * 32) : "memory");
-  SCB_FT(8);
-  if (F.shared_list) return;  // many flip words (tall bands): the caller runs col_reduce's shared row list
-  // this warp's slice of the one ascending list of flipped rows (every warp scans
-  // all flip words; lane l covers entries [l per, (l + 1) per))
-  const int per = (items + 31) / 32;
-  const int i0 = min(items, lane * per), i1 = min(items, i0 + per);
-  int cnt = 0;
-#pragma unroll 1
-  for (int i = i0; i < i1; ++i) cnt += __popc(static_cast<uint32_t>(fws[i]));
-  int inc = cnt;
+  inc = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, inc, o);
@@ -1846,7 +1874,13 @@ __device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, con
   }
   const int total = __shfl_sync(0xffffffffu, inc, 31);
   SCB_FT(11);
-  const int k0 = (total * lw) / NP, k1 = (total * (lw + 1)) / NP;
+  if (F.direct) {
+    k0 = 0;
+    k1 = total;
+  } else {
+    k0 = (total * lw) / NP;
+    k1 = (total * (lw + 1)) / NP;
+  }
   uint32_t* buf = reinterpret_cast<uint32_t*>(smem + F.fbuf) + lw * kFBuf;
   const E* Rc = static_cast<const E*>(F.R) + F.g * 32 + lane;  // column of word 0; word j: + j * G * 32
   // this warp's partial of every owned word accumulates in its own zseg slot
@@ -1856,7 +1890,16 @@ __device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, con
 #pragma unroll 1
   for (int c0 = k0; c0 < k1; c0 += kFBuf) {
     const int c1 = min(c0 + kFBuf, k1);
-    {
+    if (F.direct) {
+      int pos = inc - cnt;
+      uint32_t f = myf;
+      while (f) {
+        const int b = __ffs(f) - 1;
+        f &= f - 1;
+        if (pos >= c0 && pos < c1) buf[pos - c0] = static_cast<uint32_t>(myrb + b) | (((mysn >> b) & 1u) << 31);
+        ++pos;
+      }
+    } else {
       int pos = inc - cnt;
       int gp = sw == 1 ? i0 : i0 / sw, w = i0 - gp * sw;
 #pragma unroll 1
@@ -2262,6 +2305,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       // c partials polled all at once (bands of more than 16 rows: the decision is the late
       // part of the pass there; 4096^2 -7%) or one butterfly at a time (short bands: +2% otherwise)
       fc.cpar = p.rows_max > 16 ? 1 : 0;
+      // every owner warp's share of the flip words fits its 32 lanes: direct form
+      fc.direct = (!fc.shared_list && ((G + (NW - 1) - 1) / (NW - 1) + 1) * p.sw <= 32) ? 1 : 0;
     }
     ctl->term = 0;
     ctl->restart = 0;
