@@ -718,8 +718,8 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   const bool prof = ctx->opts.profile != 0;
   unsigned long long* dprof = nullptr;
   if (prof) {
-    SC_CUDA(ctx, cudaMalloc(&dprof, static_cast<size_t>(G) * (32 + 128) * 8));
-    SC_CUDA(ctx, cudaMemsetAsync(dprof, 0, static_cast<size_t>(G) * (32 + 128) * 8, st));
+    SC_CUDA(ctx, cudaMalloc(&dprof, static_cast<size_t>(G) * 32 * 8));
+    SC_CUDA(ctx, cudaMemsetAsync(dprof, 0, static_cast<size_t>(G) * 32 * 8, st));
   }
   kp.prof = dprof;
   // SearchDiagnostics::sweep_values of term 0, every restart (the host keeps the winner's)
@@ -805,40 +805,26 @@ sc_status finish_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, RunState&
   res->kernel_ms = kms;
   res->kernel_launches = 1;
   if (prof) {
-    std::vector<unsigned long long> hp(static_cast<size_t>(G) * (32 + 128));
+    std::vector<unsigned long long> hp(static_cast<size_t>(G) * 32);
     cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost);
     {
       double d[16] = {0};
       for (int g = 0; g < G; ++g)
         for (int i = 0; i < 16; ++i) d[i] += static_cast<double>(hp[static_cast<size_t>(G) * 16 + g * 16 + i]);
       const double nd = std::max<double>(1.0, static_cast<double>(h_stats[3])) * G;
-      if (S.kp.fast_delta) {  // clock64 stamps of eight consecutive passes: spread over the CTAs
-        static const char* nm[13] = {"t arrived", "list done", "gather done", "record out", "c reduced", "", "", "", "flips staged", "z partial", "t published", "rows counted", "rows listed"};
-        for (int ps = 0; ps < 8; ++ps) {
-          unsigned long long base = ~0ull;
-          for (int g = 0; g < G; ++g) {
-            const unsigned long long v = hp[static_cast<size_t>(G) * 32 + (static_cast<size_t>(g) * 8 + ps) * 16 + 0];
-            if (v) base = std::min(base, v);
-          }
-          if (base == ~0ull) continue;
-          std::fprintf(stderr, "[scb stamps] pass +%d:", ps);
-          for (int k = 0; k < 13; ++k) {
-            if (!nm[k][0]) continue;
-            double mn = 1e300, mx = -1e300, sum = 0; int cnt = 0;
-            for (int g = 0; g < G; ++g) {
-              const unsigned long long v = hp[static_cast<size_t>(G) * 32 + (static_cast<size_t>(g) * 8 + ps) * 16 + k];
-              if (!v) continue;
-              const double d = static_cast<double>(static_cast<long long>(v - base));
-              mn = std::min(mn, d); mx = std::max(mx, d); sum += d; ++cnt;
-            }
-            if (cnt) std::fprintf(stderr, " %s %.0f/%.0f/%.0f", nm[k], mn, sum / cnt, mx);
-          }
+      if (S.kp.fast_delta && ctx->opts.profile >= 2) {
+        static const int slots[] = {0, 1, 2, 3, 4, 7, 8, 9, 10};
+        static const char* nm[] = {"t wait", "list+sync", "gathers+bar", "signs+publish", "c poll", "decision", "flip poll", "gather", "final+publish"};
+        const double npd = std::max<double>(1.0, static_cast<double>(h_stats[3]));
+        for (int q = 0; q < 9; ++q) {
+          std::fprintf(stderr, "[scb cta] %s:", nm[q]);
+          for (int g = 0; g < G; ++g) std::fprintf(stderr, " %.0f", static_cast<double>(hp[static_cast<size_t>(G) * 16 + g * 16 + slots[q]]) / npd);
           std::fprintf(stderr, "\n");
         }
       }
       if (S.kp.fast_delta)
-        std::fprintf(stderr, "[scb prof fast delta] per delta pass per CTA: thread 0: t wait %.0f list+sync %.0f gathers+bar %.0f signs+publish %.0f c poll %.0f decision %.0f | thread 32: flip poll+bar %.0f list+gather %.0f final+publish %.0f\n",
-                     d[0] / nd, d[1] / nd, d[2] / nd, d[3] / nd, d[4] / nd, d[7] / nd, d[8] / nd, d[9] / nd, d[10] / nd);
+        std::fprintf(stderr, "[scb prof fast delta] per delta pass per CTA: thread 0: t wait %.0f list+sync %.0f gathers+bar %.0f signs+publish %.0f c poll %.0f decision %.0f | thread 32: flip poll %.0f rows counted %.0f rows listed %.0f gather %.0f final+publish %.0f\n",
+                     d[0] / nd, d[1] / nd, d[2] / nd, d[3] / nd, d[4] / nd, d[7] / nd, d[8] / nd, d[11] / nd, d[12] / nd, d[9] / nd, d[10] / nd);
       else
         std::fprintf(stderr, "[scb prof delta] per delta pass per CTA: fliplists %.0f gathers %.0f sync %.0f signs %.0f dz %.0f | CTAs with dz per pass %.2f | column reduction (thread 32) %.0f decision %.0f\n",
                      d[0] / nd, d[1] / nd, d[2] / nd, d[3] / nd, d[4] / nd, d[5] / std::max<double>(1.0, static_cast<double>(h_stats[3])), d[6] / nd, d[7] / nd);

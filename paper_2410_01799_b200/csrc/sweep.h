@@ -76,6 +76,7 @@ struct Ctl {
   volatile int upd_done;  // fused-update dot pass P: phase A's write-back is complete (P + 1)
   UpdArgs ua;
   FastConst fc;
+  long long fprof[16];  // SCB_PROFILE builds: cycle sums of the barrier-free delta pass sections
   volatile int kind_ring[4];
   // controller state (thread 0 writes, consumers read after a named barrier)
   int kind, pp, term, restart, tsel, utsel, best_tsel, best_sweeps, best_restart;

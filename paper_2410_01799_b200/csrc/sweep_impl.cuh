@@ -1513,7 +1513,6 @@ __device__ __forceinline__ void st_relaxed64x2(unsigned long long* p, unsigned l
 #else
 #define SCB_POLL_BACKOFF() do {} while (0)
 #endif
-constexpr int kStamp0 = 3000;  // SCB_PROFILE builds: passes [kStamp0, kStamp0 + 8) record clock64 stamps per CTA
 template <typename E, int NW>
 __device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, const int tsel, const int cur_nxt) {
   constexpr int CT = NW * 32;
@@ -1536,8 +1535,7 @@ __device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, con
   const unsigned long long* rec_in = F.drec + static_cast<size_t>(P & 1) * G * F.rstride;
 #ifdef SCB_PROFILE
   long long ft0 = clock64();
-#define SCB_FT(k) do { if (F.prof && (tid == 0 || tid == 32)) { const long long t1_ = clock64(); if (tid == ((k) >= 8 ? 32 : 0)) { F.prof[k] += t1_ - ft0; \
-    if (P >= kStamp0 && P < kStamp0 + 8) F.prof[static_cast<size_t>(G - F.g) * 16 + (static_cast<size_t>(F.g) * 8 + (P - kStamp0)) * 16 + (k)] = t1_; } ft0 = t1_; } } while (0)
+#define SCB_FT(k) do { if (F.prof && (tid == 0 || tid == 32)) { const long long t1_ = clock64(); if (tid == ((k) >= 8 ? 32 : 0)) ctl->fprof[k] += t1_ - ft0; ft0 = t1_; } } while (0)
 #else
 #define SCB_FT(k) do {} while (0)
 #endif
@@ -1631,42 +1629,55 @@ __device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, con
   // ---- 2. y update: warp w takes rows w, w + NW, ... four at a time ----
   for (int base = 0;;) {
     const int cn = min(kCList, nfl - base);
+    // rows per warp and round: no more than the band gives every warp (the same per-lane
+    // sums and the same butterfly for every RPG, so the choice never changes a bit)
+    auto gather = [&](auto rpg_c) {
+      constexpr int RPG = decltype(rpg_c)::value;
 #pragma unroll 1
-    for (int j0 = warp; j0 < rows_g; j0 += 4 * NW) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int j0 = warp; j0 < rows_g; j0 += RPG * NW) {
+        double acc[RPG];
+#pragma unroll
+        for (int r = 0; r < RPG; ++r) acc[r] = 0.0;
 #pragma unroll 1
-      for (int k0 = 0; k0 < cn; k0 += 64) {  // two list entries per lane and round, four rows: 8 loads in flight
-        uint32_t e[2];
-        E v[4][2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int k = k0 + u * 32 + lane;
-          e[u] = k < cn ? clist[k] : 0xffffffffu;
-        }
-        // (every row is current in global R; SMEM-resident rows are read from L2 like the
-        // rest -- one load path keeps this once-per-pass code short)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int jr = j0 + r * NW;
-          const bool ok = jr < rows_g;
-          const E* row = Rg + static_cast<size_t>(ok ? jr : j0) * F.pitch;
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-            v[r][u] = (ok && e[u] != 0xffffffffu) ? __ldcg(row + (e[u] & 0x7fffffffu)) : E(0);
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int k0 = 0; k0 < cn; k0 += 64) {  // two list entries per lane and round: 2 RPG loads in flight
+          uint32_t e[2];
+          E v[RPG][2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const double d = static_cast<double>(v[r][u]);
-            acc[r] += (e[u] >> 31) ? -d : d;
+            const int k = k0 + u * 32 + lane;
+            e[u] = k < cn ? clist[k] : 0xffffffffu;
           }
-      }
-      const double s = warp_reduce_rows<4>(acc, lane);
+          // (every row is current in global R; SMEM-resident rows are read from L2 like the
+          // rest -- one load path keeps this once-per-pass code short)
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (lane == holder_lane<4>(r) && j0 + r * NW < rows_g) yrow[j0 + r * NW] += 2.0 * s;
-    }
+          for (int r = 0; r < RPG; ++r) {
+            const int jr = j0 + r * NW;
+            const bool ok = jr < rows_g;
+            const E* row = Rg + static_cast<size_t>(ok ? jr : j0) * F.pitch;
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+              v[r][u] = (ok && e[u] != 0xffffffffu) ? __ldcg(row + (e[u] & 0x7fffffffu)) : E(0);
+          }
+#pragma unroll
+          for (int r = 0; r < RPG; ++r)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const double d = static_cast<double>(v[r][u]);
+              acc[r] += (e[u] >> 31) ? -d : d;
+            }
+        }
+        const double s = warp_reduce_rows<RPG>(acc, lane);
+#pragma unroll
+        for (int r = 0; r < RPG; ++r)
+          if (lane == holder_lane<RPG>(r) && j0 + r * NW < rows_g) yrow[j0 + r * NW] += 2.0 * s;
+      }
+    };
+    if (rows_g > 2 * NW)
+      gather(std::integral_constant<int, 4>{});
+    else if (rows_g > NW)
+      gather(std::integral_constant<int, 2>{});
+    else
+      gather(std::integral_constant<int, 1>{});
     base += kCList;
     if (base >= nfl) break;
     consumer_sync(CT);  // more flips than one list holds: the next chunk of the list
@@ -2261,6 +2272,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     ctl->has_dz = 0;
     ctl->keep = 0;
     ctl->zerr = 0;
+    for (int k = 0; k < 16; ++k) ctl->fprof[k] = 0;
     {  // pass-invariant operands of the barrier-free delta pass
       FastConst& fc = ctl->fc;
       fc.Rrows = R + static_cast<size_t>(r0) * pitch;
@@ -3098,7 +3110,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
         col_reduce_global(P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
       else
         col_reduce(0, P, (kind & F_DELTA) != 0, (pp + 1) & 1, 1);
-      if (prof && tid == 32 && (kind & F_DELTA)) prof[static_cast<size_t>(p.G) * 16 + g * 16 + 6] += clock64() - tc0;
+      if (prof && tid == 32 && (kind & F_DELTA)) ctl->fprof[6] += clock64() - tc0;
     }
     const long long td0 = (prof && tid == 0) ? clock64() : 0;
 
@@ -3278,7 +3290,7 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       __threadfence_block();
       ctl->decided = P + 2;
       if ((next & K_TERM) && g == 0) p.stats[1] = static_cast<unsigned long long>(P + 1);
-      if (prof && (kind & F_DELTA)) prof[static_cast<size_t>(p.G) * 16 + g * 16 + 7] += clock64() - td0;
+      if (prof && (kind & F_DELTA)) ctl->fprof[7] += clock64() - td0;
     }
     consumer_sync(CT);
     if (prof && tid == 0) {
@@ -3307,6 +3319,8 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
     p.stats[3] = dot_passes[1];
   }
   if (prof && tid == 0) {
+    for (int k = 0; k < 16; ++k)  // fast-delta / decision sections (shared-memory accumulators)
+      if (ctl->fprof[k]) prof[static_cast<size_t>(p.G) * 16 + g * 16 + k] = static_cast<unsigned long long>(ctl->fprof[k]);
     for (int i = 0; i < 7; ++i) prof[g * 16 + i] = static_cast<unsigned long long>(pacc[i]);
     prof[g * 16 + 12] = static_cast<unsigned long long>(pten[0]);
     prof[g * 16 + 13] = static_cast<unsigned long long>(pten[1]);
