@@ -23,7 +23,7 @@ for rnd in range(int(os.environ.get("AB_ROUNDS", 3))):
         N.SIGNATURES = {k: v for k, v in ALL_SIGS.items() if hasattr(probe, k)}  # older builds: fewer symbols
         N._lib = None
         N.LIB_PATH = path
-        eng = sc.Engine(0)
+        eng = sc.Engine(0, **{k: int(v) for k, v in (x.split("=") for x in os.environ.get("AB_ENGINE_OPTS", "").split(",") if x)})
         dec, rep, _ = eng.run(a, cfg, dtype="f32")
         res.setdefault(path, []).append((rep.kernel_ms, rep.passes, tuple(rep.sweeps[:8])))
         del eng

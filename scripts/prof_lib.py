@@ -18,7 +18,8 @@ w = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 m = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
 n = int(sys.argv[3]) if len(sys.argv) > 3 else m
 dt = sys.argv[4] if len(sys.argv) > 4 else "f32"
-eng = sc.Engine(0, profile=2 if os.environ.get("PROF_CTA") else 1)
+opts = {k: int(v) for k, v in (x.split("=") for x in os.environ.get("PROF_OPTS", "").split(",") if x)}  # e.g. delta=0
+eng = sc.Engine(0, profile=2 if os.environ.get("PROF_CTA") else 1, **opts)
 a = sc.fill_normal(1, m * n, np.float32).reshape(m, n)
 dec, rep, _ = eng.run(a, sc.DecomposeConfig(width=w, search=sc.SearchConfig(seed=1)), dtype=dt)
 print("kernel_ms", rep.kernel_ms, "passes", rep.passes, "dense", rep.dense_passes, "delta", rep.delta_passes,
