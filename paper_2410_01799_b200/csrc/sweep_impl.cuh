@@ -3177,11 +3177,12 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
           return F_NORM | F_WB;
         }
       };
+      // (only the first ceil(G / 32) butterflies hold CTAs; the others added zeros)
       double cs = 0.0, ns = 0.0;
-      for (int w = 0; w < CW; ++w) {
-        cs += ctl->cred[w];
-        ns += ctl->nred[w];
-      }
+      const int nwz = min(CW, (G + 31) >> 5);
+      for (int w = 0; w < nwz; ++w) cs += ctl->cred[w];
+      if (kind & F_NORM)
+        for (int w = 0; w < nwz; ++w) ns += ctl->nred[w];
       int next;
       int need_reduce = 0;
       const unsigned ey = ctl->err_pre[0], ei = ctl->err_pre[1], ez = ctl->err_pre[2];
