@@ -1,6 +1,9 @@
 """Phase split of the order-3 C3 pass (needs an SCB_PROFILE=1 build; engine option profile=1)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2410_01799_b200 import _native as N
+if os.environ.get("SCB_LIB"):  # an SCB_PROFILE=1 build
+    N.LIB_PATH = os.environ["SCB_LIB"]
 import paper_2410_01799_b200 as sc
 from paper_2410_01799_b200 import workloads as wl
 eng = sc.Engine(0, profile=1)
