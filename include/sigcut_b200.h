@@ -29,6 +29,7 @@
  *   sc_gram_matrix       replaces  detail::build_gram (Gram part)   decompose.hpp:383-393
  *   sc_contract_terms    replaces  detail::contract_term            decompose.hpp:218-260
  *   sc_solve_gram        restates  sigcut::solve_gram               gram.hpp:83-107
+ *   sc_solve_gram_leading  the same for every leading block (lstsq's term loop), O(k^2) each
  *   sc_correct_coefficients replaces sigcut::correct_coefficients  decompose.hpp:418-428
  *   sc_lstsq_decompose   replaces  sigcut::lstsq_decompose          decompose.hpp:434-469
  *                        and (channel_axis >= 0) rgb_scalars_decompose :485-536
@@ -248,6 +249,14 @@ sc_status sc_contract_terms(sc_ctx* ctx, const sc_factors* d, int32_t a_dtype, c
  * channels, term-major.  SC_RUNTIME_ERROR when the factorisation fails. */
 sc_status sc_solve_gram(uint64_t width, uint64_t channels, const double* gram, const double* rhs, double* out,
                         char* msg, size_t msg_len);
+
+/* The same solve for every leading block k = 1..width of one system, as lstsq_decompose
+ * (decompose.hpp:434-469) needs it term by term: the factor grows by one row per block
+ * (the reference's column order leaves earlier rows unchanged), so block k costs O(k^2)
+ * and every result equals sc_solve_gram of that block bit for bit.  out: the k x channels
+ * solutions one after another, k = 1..width (width (width + 1) / 2 x channels doubles). */
+sc_status sc_solve_gram_leading(uint64_t width, uint64_t channels, const double* gram, const double* rhs, double* out,
+                                char* msg, size_t msg_len);
 
 /* correct_coefficients (decompose.hpp:418-428): refit with the signs held fixed;
  * keeps the old coefficients when the solve is not better.  coeffs_out: width x

@@ -31,6 +31,7 @@ from .api import (  # noqa: F401
     lstsq_decompose,
     rgb_scalars_decompose,
     solve_gram,
+    solve_gram_leading,
     start_vectors,
     truncated,
     unpack_signs,

@@ -149,6 +149,7 @@ SIGNATURES = {
     "sc_contract_terms": (C.c_int, [C.c_void_p, P(ScFactors), C.c_int32, C.c_void_p, C.c_int32, u64, u64,
                                     P(C.c_double), P(ScOpStats)]),
     "sc_solve_gram": (C.c_int, [u64, u64, P(C.c_double), P(C.c_double), P(C.c_double), C.c_char_p, C.c_size_t]),
+    "sc_solve_gram_leading": (C.c_int, [u64, u64, P(C.c_double), P(C.c_double), P(C.c_double), C.c_char_p, C.c_size_t]),
     "sc_correct_coefficients": (C.c_int, [C.c_void_p, P(ScFactors), C.c_int32, C.c_void_p, C.c_int32,
                                           P(C.c_double), P(ScOpStats)]),
     "sc_lstsq_decompose": (C.c_int, [C.c_void_p, P(ScProblem), C.c_int32, P(ScResult)]),

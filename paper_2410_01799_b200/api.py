@@ -565,6 +565,30 @@ def solve_gram(gram, rhs) -> np.ndarray:
     return out
 
 
+def solve_gram_leading(gram, rhs) -> List[np.ndarray]:
+    """solve_gram of every leading block k = 1..w of one system (what lstsq_decompose solves term
+    by term, decompose.hpp:434-469), with the factor grown one row per block: O(k^2) per block,
+    each result bit-identical to solve_gram(gram[:k, :k], rhs[:k])."""
+    g = np.ascontiguousarray(gram, np.float64)
+    w = g.shape[0] if g.ndim == 2 else 0
+    r = np.ascontiguousarray(rhs, np.float64).reshape(w, -1) if w else np.zeros((0, 1))
+    ch = r.shape[1]
+    out = np.zeros((w * (w + 1) // 2, ch))
+    if w == 0:
+        return []
+    msg = C.create_string_buffer(256)
+    st = N.lib().sc_solve_gram_leading(w, ch, g.ctypes.data_as(C.POINTER(C.c_double)),
+                                       r.ctypes.data_as(C.POINTER(C.c_double)),
+                                       out.ctypes.data_as(C.POINTER(C.c_double)), msg, 256)
+    if st != N.SC_OK:
+        raise _ERRORS.get(st, SigcutRuntimeError)(msg.value.decode())
+    res, off = [], 0
+    for k in range(1, w + 1):
+        res.append(out[off:off + k].copy())
+        off += k
+    return res
+
+
 def greedy_signed_cut(a, cfg: Optional[SearchConfig] = None, dtype: Optional[str] = None,
                       diag: Optional[SearchDiagnostics] = None) -> CutResult:
     return default_engine().greedy_signed_cut(a, cfg, dtype=dtype, diag=diag)

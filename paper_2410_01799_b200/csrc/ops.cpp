@@ -389,6 +389,57 @@ bool solve_gram(size_t w, size_t ch, const double* gram, const double* rhs, doub
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Incremental form of the same factorisation for the term-by-term solves of
+// lstsq_decompose (decompose.hpp:434-469 calls solve_gram afresh for every leading
+// block: O(k^3) per term).  In the reference's left-looking column order, entry
+// L[i][j] depends only on G[i][j] and on rows i and j of L to the left of column j,
+// so the factor of the bordered system keeps every earlier row bit for bit and gains
+// one row, computed here by the very same operations in the very same order: O(k^2)
+// per term, identical coefficients.  Lower triangle packed by rows.  A failed pivot
+// (ridge retry needed) hands the system back to solve_gram.
+struct IncCholesky {
+  std::vector<double> l;  // packed rows: row i at i (i + 1) / 2
+  size_t n = 0;
+  bool valid = true;
+  static size_t at(size_t i) { return i * (i + 1) / 2; }
+  // col: Gram column of the new term against terms 0..n (col[n] = its diagonal)
+  bool append(const double* col) {
+    const size_t i = n;
+    l.resize(at(i + 1));
+    double* ri = l.data() + at(i);
+    for (size_t j = 0; j < i; ++j) {
+      const double* rj = l.data() + at(j);
+      double v = col[j];
+      for (size_t p = 0; p < j; ++p) v -= ri[p] * rj[p];
+      ri[j] = v / rj[j];
+    }
+    double d = col[i];
+    for (size_t p = 0; p < i; ++p) d -= ri[p] * ri[p];
+    if (!(d > 0.0) || !std::isfinite(d)) {
+      l.resize(at(i));
+      valid = false;
+      return false;
+    }
+    ri[i] = std::sqrt(d);
+    n = i + 1;
+    return true;
+  }
+  void solve(double* x) const {  // cholesky_solve on the packed factor
+    for (size_t i = 0; i < n; ++i) {
+      const double* ri = l.data() + at(i);
+      double v = x[i];
+      for (size_t p = 0; p < i; ++p) v -= ri[p] * x[p];
+      x[i] = v / ri[i];
+    }
+    for (size_t i = n; i-- > 0;) {
+      double v = x[i];
+      for (size_t p = i + 1; p < n; ++p) v -= l[at(p) + i] * x[p];
+      x[i] = v / l[at(i) + i];
+    }
+  }
+};
+
 // gram_quadratic (decompose.hpp:397-410)
 double gram_quadratic(size_t w, size_t ch, const double* gram, const double* rhs, const double* c) {
   double value = 0.0;
@@ -697,6 +748,34 @@ sc_status sc_contract_terms(sc_ctx* ctx, const sc_factors* d, int32_t a_dtype, c
   return SC_OK;
 }
 
+sc_status sc_solve_gram_leading(uint64_t width, uint64_t channels, const double* gram, const double* rhs, double* out,
+                                char* msg, size_t msg_len) {
+  if ((width > 0 && (gram == nullptr || rhs == nullptr || out == nullptr)) || channels == 0)
+    return put_msg(msg, msg_len, SC_INVALID_ARGUMENT, "sc_solve_gram_leading: null argument");
+  IncCholesky chol;
+  std::vector<double> col(width), x(width), blk;
+  size_t off = 0;
+  for (uint64_t k = 1; k <= width; ++k) {
+    for (uint64_t j = 0; j < k; ++j) col[j] = gram[(k - 1) * width + j];
+    double* o = out + off * channels;
+    if (chol.valid && chol.append(col.data())) {
+      for (uint64_t c = 0; c < channels; ++c) {
+        for (uint64_t j = 0; j < k; ++j) x[j] = rhs[j * channels + c];
+        chol.solve(x.data());
+        for (uint64_t j = 0; j < k; ++j) o[j * channels + c] = x[j];
+      }
+    } else {
+      blk.resize(k * k);
+      for (uint64_t i = 0; i < k; ++i)
+        for (uint64_t j = 0; j < k; ++j) blk[i * k + j] = gram[i * width + j];
+      if (!solve_gram(k, channels, blk.data(), rhs, o))
+        return put_msg(msg, msg_len, SC_RUNTIME_ERROR, "solve_gram: factorization failed");
+    }
+    off += k;
+  }
+  return SC_OK;
+}
+
 sc_status sc_solve_gram(uint64_t width, uint64_t channels, const double* gram, const double* rhs, double* out,
                         char* msg, size_t msg_len) {
   if (width == 0) return SC_OK;
@@ -800,6 +879,7 @@ sc_status sc_lstsq_decompose(sc_ctx* ctx, const sc_problem* p, int32_t channel_a
   for (int i = 0; i < k; ++i) cut_words[i].assign(words64(p->shape[i]), 0);
   std::vector<double> gram, rhs;  // GramSystem (gram.hpp:17-43)
   std::vector<double> coef;
+  IncCholesky chol;
   size_t gw = 0;
   double first_value = 0.0;
   uint64_t done = 0;
@@ -855,20 +935,33 @@ sc_status sc_lstsq_decompose(sc_ctx* ctx, const sc_problem* p, int32_t channel_a
     st.d2h_bytes += (term + 1) * 8;
     // rhs block: contract_term(a, channel_axis, signs)
     if (sc_status s = contract(ctx, L, F, term, 1, p->dtype, dA, rb.data(), &st); s != SC_OK) return s;
-    // GramSystem::extend (gram.hpp:28-42)
-    std::vector<double> grown((gw + 1) * (gw + 1));
+    // GramSystem::extend (gram.hpp:28-42); rows at a fixed stride w, so a term costs O(k)
+    // here (the compact k x k copy is made only if the ridge retry is needed)
+    if (gram.empty()) gram.assign(static_cast<size_t>(w) * w, 0.0);
     for (size_t i = 0; i < gw; ++i) {
-      for (size_t j = 0; j < gw; ++j) grown[i * (gw + 1) + j] = gram[i * gw + j];
-      grown[i * (gw + 1) + gw] = col[i];
-      grown[gw * (gw + 1) + i] = col[i];
+      gram[i * w + gw] = col[i];
+      gram[gw * w + i] = col[i];
     }
-    grown[gw * (gw + 1) + gw] = col[gw];
-    gram.swap(grown);
+    gram[gw * w + gw] = col[gw];
     rhs.insert(rhs.end(), rb.begin(), rb.end());
     ++gw;
     coef.assign(gw * nch, 0.0);
-    if (!solve_gram(gw, nch, gram.data(), rhs.data(), coef.data()))
-      return set_err(ctx, SC_RUNTIME_ERROR, "solve_gram: factorization failed");
+    // the factor grows by one row per term (identical to solve_gram of the whole system);
+    // once a pivot fails, solve_gram with its ridge retries takes over for good
+    if (chol.valid && chol.append(col.data())) {
+      std::vector<double> x(gw);
+      for (int c = 0; c < nch; ++c) {
+        for (size_t j = 0; j < gw; ++j) x[j] = rhs[j * nch + c];
+        chol.solve(x.data());
+        for (size_t j = 0; j < gw; ++j) coef[j * nch + c] = x[j];
+      }
+    } else {
+      std::vector<double> blk(gw * gw);
+      for (size_t i = 0; i < gw; ++i)
+        for (size_t j = 0; j < gw; ++j) blk[i * gw + j] = gram[i * w + j];
+      if (!solve_gram(gw, nch, blk.data(), rhs.data(), coef.data()))
+        return set_err(ctx, SC_RUNTIME_ERROR, "solve_gram: factorization failed");
+    }
     // residual = a - expand(d) with the re-solved coefficients
     SC_CUDA(ctx, cudaMemcpyAsync(dcoef, coef.data(), gw * nch * 8, cudaMemcpyHostToDevice, ctx->stream));
     st.h2d_bytes += gw * nch * 8;

@@ -186,6 +186,25 @@ def test_solve_gram_ridge_and_failure_like_reference(ref):
         sc.solve_gram(np.array([[-1.0]]), np.array([1.0]))
 
 
+@pytest.mark.parametrize("w,nbits,ch,dup", [(1, 8, 1, None), (12, 64, 1, None), (40, 256, 3, None), (24, 96, 2, 9)])
+def test_solve_gram_leading_blocks_bit_identical(ref, w, nbits, ch, dup):
+    """The incremental factor of lstsq's term loop (one row per term, O(k^2)): every leading
+    block's solution equals the reference's solve_gram of that block bit for bit -- also after
+    a duplicated term made a pivot fail and the ridge retry took over (dup)."""
+    rng = np.random.default_rng(100 + w)
+    f = np.where(rng.standard_normal((w, nbits)) < 0, -1.0, 1.0)
+    if dup is not None:
+        f[dup] = f[dup - 3]  # term dup repeats an earlier one: singular from block dup + 1 on
+    gram = f @ f.T
+    rhs = rng.standard_normal((w, ch)) * nbits
+    blocks = sc.solve_gram_leading(gram, rhs)
+    assert len(blocks) == w
+    for k in range(1, w + 1):
+        theirs = ref.solve_gram(np.ascontiguousarray(gram[:k, :k]), np.ascontiguousarray(rhs[:k]))
+        assert blocks[k - 1].shape == (k, ch)
+        assert (bits(blocks[k - 1].reshape(-1)) == bits(np.asarray(theirs).reshape(-1))).all(), k
+
+
 def test_workload_generator_is_reference_stream(orc):
     from paper_2410_01799_b200.workloads import Xoshiro256pp
 
