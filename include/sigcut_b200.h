@@ -146,7 +146,7 @@ const char* sc_last_error(const sc_ctx* ctx);
 
 /* Engine options of this context (tuning / test knobs; the defaults are the
  * measured best).  Names: "ctas" (CTA cap, 0 auto), "delta" (sparse delta passes,
- * 1), "delta_div" (0 = auto: 8 with the barrier-free delta pass, else 32), "delta_refresh" (64), "two_phase" (dot-pass form: -1 auto,
+ * 1), "delta_div" (0 = auto: 4 with the barrier-free delta pass, else 32), "delta_refresh" (64), "two_phase" (dot-pass form: -1 auto,
  * 0 fused single read, 1 two-phase), "stages" (TMA ring depth, 0 auto),
  * "res_rows" (cap on SMEM-resident rows, -1 none), "fuse_update" (rank-1 update
  * fused into the next term's first dot pass, 1), "variant" (tile override

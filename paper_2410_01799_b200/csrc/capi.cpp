@@ -679,10 +679,11 @@ sc_status prepare_run(sc_ctx* ctx, const sc_problem* p, sc_result* res, const sc
   kp.rstride = rstride;
   // one GPU, matrices, whole rows, one record-polling thread per CTA of the grid
   kp.fast_delta = (ctx->opts.fast_delta && !tensor && !sh && !vr && cpr == 1 && var.nw * 32 >= G && G <= 160 && Q <= 4 * G) ? 1 : 0;
-  // delta pass only if the last sweep flipped <= n / delta_div columns.  Auto (0): n / 8 with the
-  // barrier-free delta pass (4096^2 w=512: 355.6 ms at 32, 344.5 at 16, 338.9 at 8, 338.2 at 4),
-  // n / 32 for the barrier passes (order-k, row-sharded, chunked rows: measured best in round 1)
-  kp.delta_div = static_cast<int>(ctx->opts.delta_div > 0 ? ctx->opts.delta_div : (kp.fast_delta ? 8 : 32));
+  // delta pass only if the last sweep flipped <= n / delta_div columns.  Auto (0): n / 4 with the
+  // barrier-free delta pass (4096^2 w=512 on the final kernel: 278.7 ms at 8, 276.7 at 6, 270.8
+  // at 4, 271.6 at 3; 2.5 dense passes per cut instead of 3.5), n / 32 for the barrier passes
+  // (order-k, row-sharded, chunked rows: measured best in round 1)
+  kp.delta_div = static_cast<int>(ctx->opts.delta_div > 0 ? ctx->opts.delta_div : (kp.fast_delta ? 4 : 32));
   // Sparse delta passes between dense refreshes (matrices, any row length: the dz of
   // flipped rows walks every column chunk).
   kp.delta = ctx->opts.delta ? 1 : 0;
