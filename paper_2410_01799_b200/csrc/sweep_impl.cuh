@@ -1748,29 +1748,6 @@ __device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, con
     // records are not polled while they cannot be complete.
     if (F.nls > 0 && F.cpar) asm volatile("bar.sync 5, %0;" ::"r"(CT) : "memory");
     bool flag = false;
-    if (!F.cpar) {  // short bands: one butterfly's loads at a time (less polling; the decision is not late here)
-#pragma unroll 1
-      for (int k = 0; k < NW; ++k) {
-        const int gi = k * 32 + lane;
-        double c = 0.0;
-        if (k * 32 < G) {
-          if (gi < G) {
-            const unsigned long long* pc = rec_in + static_cast<size_t>(gi) * F.rstride + 2 * sw;
-            unsigned long long c0, c1;
-            do {
-              ld_relaxed64x2(pc, c0, c1);
-            } while ((static_cast<unsigned>(c0 >> 32) & 0x7fffffffu) != uP || (static_cast<unsigned>(c1 >> 32) & 0x7fffffffu) != uP);
-            c = __hiloint2double(static_cast<int>(static_cast<uint32_t>(c0)), static_cast<int>(static_cast<uint32_t>(c1)));
-            flag |= (c0 >> 63) != 0ull;
-          }
-          c = warp_sum(c);
-        }
-        if (lane == 0) {
-          ctl->cred[k] = c;
-          ctl->nred[k] = 0.0;
-        }
-      }
-    } else {
     constexpr int KC = 5;  // G <= 160 (host gate)
     unsigned long long cw0[KC], cw1[KC];
     unsigned need = 0;
@@ -1810,7 +1787,6 @@ __device__ __noinline__ void fast_delta(const unsigned ctl_off, const int P, con
         ctl->cred[k] = 0.0;
         ctl->nred[k] = 0.0;
       }
-    }
     flag = __any_sync(0xffffffffu, flag);
     if (flag && lane == 0) ctl->err_pre[0] = uP;  // some CTA saw a non-finite value: every CTA stops at this pass
     __syncwarp();
@@ -2314,8 +2290,10 @@ __device__ __forceinline__ void sweep_body(const KParams& p, const int g) {
       // tall bands (many flip words per pass): one row list built by all owner warps
       // together (col_reduce) beats every warp scanning all the words
       fc.shared_list = G * p.sw > 256 ? 1 : 0;
-      // c partials polled all at once (bands of more than 16 rows: the decision is the late
-      // part of the pass there; 4096^2 -7%) or one butterfly at a time (short bands: +2% otherwise)
+      // Warp 0 polls every c partial at once (one butterfly at a time was 7% slower on 4096^2 and
+      // 10-13% on 1024^2, 512^2 and 1024 x 4096: the decision is the late part of the pass).  On
+      // bands of more than 16 rows it starts once the owner warps hold every flip word (cpar);
+      // on short bands that wait cost 2-4%, so there it polls from the start.
       fc.cpar = p.rows_max > 16 ? 1 : 0;
       // every owner warp's share of the flip words fits its 32 lanes: direct form
       fc.direct = (!fc.shared_list && ((G + (NW - 1) - 1) / (NW - 1) + 1) * p.sw <= 32) ? 1 : 0;
